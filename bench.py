@@ -1,0 +1,491 @@
+#!/usr/bin/env python
+"""Benchmark: achieved HBM GB/s of the KBLAS matrix-vector hot path on B200.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference]
+
+N=1 (default): DSYMV lower, N=32768, alpha=1, beta=0 — BASELINE.json
+configs[1], the configuration the metric is quoted on.  One step = one
+kblas_dsymv call (main streaming kernel + fixed-order epilogue) on
+HBM-resident operands.  The 8.6 GB matrix is 68x the 126 MB L2, so every
+step streams A from HBM (no flush needed).
+
+N>1 (torchrun, one process per GPU, NCCL): mgpu DSYMV lower over the 1D
+block-column-cyclic layout (nb=128) with per-GPU work fixed (weak scaling):
+n = 32768 * sqrt(N) rounded to nb, each rank streams its panel's stored
+triangle and the partial y vectors are combined by one NCCL reduce onto
+rank 0 (multidevice.py:276 restated over NCCL).
+
+`--impl reference` times the reference's CPU path for the same metric:
+the C restatement of the reference oracle (oracle/streamed.c, all host
+threads) on a bounded sample (DSYMV lower N=12288); rank 0 only.
+
+Other workloads for sweeps: --op {dsymv,zhemv,ssymv,chemv,dgemv,zgemv,
+sgemv,cgemv,dgemv_t,zgemv_c,...} --n N.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SPEC_HBM_GBS = 8000.0
+CPU_SAMPLE_N = 12288
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--op", default="dsymv")
+    ap.add_argument("--n", type=int, default=None)
+    ap.add_argument("--m", type=int, default=None)
+    ap.add_argument("--nb", type=int, default=128)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    return ap.parse_args()
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ------------------------------------------------------------------- ops
+OPS = {
+    # name: (tag, family, trans/uplo, hermitian)
+    "ssymv": ("s", "symv", "l", False), "dsymv": ("d", "symv", "l", False),
+    "chemv": ("c", "symv", "l", True), "zhemv": ("z", "symv", "l", True),
+    "ssymv_u": ("s", "symv", "u", False), "dsymv_u": ("d", "symv", "u", False),
+    "chemv_u": ("c", "symv", "u", True), "zhemv_u": ("z", "symv", "u", True),
+    "sgemv": ("s", "gemv", "n", False), "dgemv": ("d", "gemv", "n", False),
+    "cgemv": ("c", "gemv", "n", False), "zgemv": ("z", "gemv", "n", False),
+    "sgemv_t": ("s", "gemv", "t", False), "dgemv_t": ("d", "gemv", "t", False),
+    "cgemv_c": ("c", "gemv", "c", False), "zgemv_c": ("z", "gemv", "c", False),
+    "cgemv_t": ("c", "gemv", "t", False), "zgemv_t": ("z", "gemv", "t", False),
+}
+
+
+def alg_bytes(tag, family, m, n, op):
+    from paper_1410_1726_b200 import roofline
+    from paper_1410_1726_b200.core import precision
+
+    p = precision(tag)
+    return roofline.symv_bytes(p, n) if family == "symv" else roofline.gemv_bytes(p, m, n, op)
+
+
+def alg_flops(tag, family, m, n, op):
+    from paper_1410_1726_b200 import roofline
+    from paper_1410_1726_b200.core import precision
+
+    p = precision(tag)
+    return roofline.symv_flops(p, n) if family == "symv" else roofline.gemv_flops(p, m, n, op)
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(self.index)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [s.strip() for s in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        reasons = sorted({self.NAMES[k] for r in self.rows for k in range(4) if r[5 + k] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------ CPU legs
+def cpu_baseline(seconds: float, n: int = CPU_SAMPLE_N, max_calls: int | None = None):
+    """The oracle (C restatement of the reference's naive_symv_hemv, all
+    host threads) on DSYMV lower N=n; GB/s on the same algorithmic bytes."""
+    import numpy as np
+
+    from oracle import streamed  # CPU baseline leg only
+    from paper_1410_1726_b200 import roofline
+    from paper_1410_1726_b200.core import precision
+
+    rng = np.random.default_rng(0)
+    a = np.asfortranarray(rng.uniform(-1, 1, size=(n, n)))
+    x = rng.uniform(-1, 1, size=n)
+    y = rng.uniform(-1, 1, size=n)
+    threads = streamed.max_threads()
+    streamed.symv("l", 1.0, a, x, 0.0, y)  # warm
+    calls, t0 = 0, time.perf_counter()
+    while True:
+        streamed.symv("l", 1.0, a, x, 0.0, y)
+        calls += 1
+        el = time.perf_counter() - t0
+        if el >= seconds or (max_calls and calls >= max_calls):
+            break
+    gbs = roofline.symv_bytes(precision("d"), n) * calls / el / 1e9
+    return {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "port",
+            "sample": f"oracle/streamed.c DSYMV lower N={n} (host matrix, f64 accumulation), "
+                      f"{calls} calls in {el:.1f} s, {threads} threads"}
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU path (oracle port), rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import numpy as np
+
+    from oracle import streamed
+    from paper_1410_1726_b200 import roofline
+    from paper_1410_1726_b200.core import precision
+
+    n = CPU_SAMPLE_N
+    rng = np.random.default_rng(0)
+    a = np.asfortranarray(rng.uniform(-1, 1, size=(n, n)))
+    x = rng.uniform(-1, 1, size=n)
+    y = rng.uniform(-1, 1, size=n)
+    threads = streamed.max_threads()
+    for _ in range(args.warmup):
+        streamed.symv("l", 1.0, a, x, 0.0, y)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        streamed.symv("l", 1.0, a, x, 0.0, y)
+    el = time.perf_counter() - t0
+    nbytes = roofline.symv_bytes(precision("d"), n)
+    gbs = nbytes * args.steps / el / 1e9
+    sample = (f"oracle/streamed.c (C restatement of blockmv naive_symv_hemv) DSYMV lower N={n}, "
+              f"{threads} threads; bounded sample of configs[1] (DSYMV lower N=32768)")
+    print(json.dumps({
+        "impl": "reference", "metric": "achieved HBM GB/s (DSYMV lower, algorithmic bytes)", "value": round(gbs, 3),
+        "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(el / args.steps * 1e3, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic U(-1,1)",
+        "config": {"workload": f"DSYMV lower N={n} (CPU sample of configs[1])", "n": n, "uplo": "l"},
+        "cpu_baseline": {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": round(gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+# ------------------------------------------------------------- GPU arm
+def bench_single(args, dev, rank):
+    import torch
+
+    from paper_1410_1726_b200 import _lib
+    from paper_1410_1726_b200.core import precision
+
+    tag, family, op, herm = OPS[args.op]
+    p = precision(tag)
+    n = args.n or (32768 if family == "symv" else 16384)
+    m = n if family == "symv" else (args.m or n)
+    lib = _lib.load()
+    torch.manual_seed(0)
+    ld = -(-m // 32) * 32
+    # column-major A: a (n, ld) row-major tensor whose row j is column j
+    A = torch.empty(n, ld, dtype=p.torch_dtype, device=dev)
+    (torch.view_as_real(A) if p.is_complex else A).uniform_(-1, 1)
+    x_len, y_len = (n, m) if (family == "symv" or op == "n") else (m, n)
+    x = torch.empty(x_len, dtype=p.torch_dtype, device=dev)
+    y = torch.empty(y_len, dtype=p.torch_dtype, device=dev)
+    (torch.view_as_real(x) if p.is_complex else x).uniform_(-1, 1)
+    (torch.view_as_real(y) if p.is_complex else y).uniform_(-1, 1)
+    stream = torch.cuda.current_stream(dev)
+    sh = stream.cuda_stream
+    one, zero = _lib.scalar(tag, 1.0), _lib.scalar(tag, 0.0)
+    if family == "symv":
+        name = {("s", False): "ssymv", ("d", False): "dsymv", ("c", True): "chemv", ("z", True): "zhemv"}[(tag, herm)]
+        fn = getattr(lib, f"kblas_{name}_async")
+
+        def step():
+            rc = fn(op.encode(), n, one, A.data_ptr(), ld, x.data_ptr(), 1, zero, y.data_ptr(), 1, sh)
+            assert rc == 0, rc
+    else:
+        fn = getattr(lib, f"kblas_{tag}gemv_async")
+
+        def step():
+            rc = fn(op.encode(), m, n, one, A.data_ptr(), ld, x.data_ptr(), 1, zero, y.data_ptr(), 1, sh)
+            assert rc == 0, rc
+
+    nbytes = alg_bytes(tag, family, m, n, op)
+    nflops = alg_flops(tag, family, m, n, op)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    plan = _lib.last_plan()
+    clock = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
+    clock.start()
+    time.sleep(0.3)
+    # warm the clocks up to the sampler's first reading, then time exactly K steps
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    _lib.timing_enable(True)
+    l0 = _lib.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(dev)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    launches = _lib.launch_count() - l0
+    _lib.timing_enable(False)
+    kern_ms, kern_n = _lib.timing_read()
+    clocks = clock.stop()
+    total_ms = e0.elapsed_time(e1)
+    ms_step = total_ms / args.steps
+    gbs = nbytes / (ms_step * 1e-3) / 1e9
+    kern_avg = kern_ms / max(kern_n, 1)
+    res = dict(tag=tag, family=family, op=op, m=m, n=n, ld=ld, nbytes=nbytes, nflops=nflops, ms_step=ms_step,
+               gbs=gbs, kern_avg_ms=kern_avg, kern_launches=kern_n, launches=launches, plan=plan,
+               clocks=clocks, total_ms=total_ms)
+    # end to end through the public API with host (pinned) buffers
+    if not args.no_e2e and args.e2e_steps > 0:
+        res["e2e"] = e2e_single(args, A, x, y, tag, family, op, herm, m, n, ld, dev, nbytes)
+    return res
+
+
+def e2e_single(args, A, x, y, tag, family, op, herm, m, n, ld, dev, nbytes):
+    """Public API (paper_1410_1726_b200.symv_hemv / gemv) on numpy operands in
+    pinned host memory: each step copies the referenced part of A, x, y to
+    HBM, runs the kernels and reads y back."""
+    import torch
+
+    import paper_1410_1726_b200 as kb
+
+    p = kb.precision(tag)
+    hA = torch.empty(A.numel(), dtype=A.dtype, pin_memory=True)
+    hA.copy_(A.reshape(-1))
+    hx = torch.empty(x.numel(), dtype=x.dtype, pin_memory=True)
+    hx.copy_(x)
+    hy = torch.empty(y.numel(), dtype=y.dtype, pin_memory=True)
+    hy.copy_(y)
+    npA, npx, npy = hA.numpy(), hx.numpy(), hy.numpy()
+    view = kb.MatrixView(npA, m, n, ld, p)
+
+    def step():
+        if family == "symv":
+            return kb.symv_hemv(op, 1.0, kb.HermitianView(view, op), npx, 0.0, npy, hermitian=herm).y_out
+        return kb.gemv(op, 1.0, view, npx, 0.0, npy).y_out
+
+    step()
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        out = step()
+    torch.cuda.synchronize(dev)
+    el = (time.perf_counter() - t0) / args.e2e_steps
+    eb = p.element_bytes
+    if family == "symv":
+        blocks = [(b0, min(n, b0 + 256)) for b0 in range(0, n, 256)]
+        h2d_a = sum((b1 - b0) * ((m - b0) if op == "l" else b1) for b0, b1 in blocks) * eb
+    else:
+        h2d_a = n * ld * eb
+    x_len = n if (family == "symv" or op == "n") else m
+    y_len = len(out)
+    return {"value": round(nbytes / el / 1e9, 3), "unit": "GB/s",
+            "h2d_bytes_per_step": int(h2d_a + x_len * eb + y_len * eb), "d2h_bytes_per_step": int(y_len * eb),
+            "steps": args.e2e_steps, "ms_per_step": round(el * 1e3, 3),
+            "path": "paper_1410_1726_b200.symv_hemv on pinned numpy operands (H2D of the stored triangle, "
+                    "x, y; kernels; D2H of y)" if family == "symv" else
+                    "paper_1410_1726_b200.gemv on pinned numpy operands"}
+
+
+def bench_mgpu(args, dev, rank, world):
+    """Weak-scaling mgpu DSYMV: per-rank panel of the block-cyclic layout,
+    partial via the sm_100a kernels, NCCL reduce of y onto rank 0."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1410_1726_b200 import _lib
+    from paper_1410_1726_b200.core import precision
+    from paper_1410_1726_b200.dist import combine, panel_shape
+    from paper_1410_1726_b200.multidevice import partial_mv
+
+    tag, family, op, herm = OPS[args.op]
+    if family != "symv":
+        raise SystemExit("mgpu bench covers symv/hemv")
+    p = precision(tag)
+    nb = args.nb
+    n = args.n or int(round(32768 * math.sqrt(world) / nb)) * nb
+    rows, lc, ld = panel_shape(n, n, nb, world, rank)
+    from paper_1410_1726_b200.core import MatrixView
+
+    g = torch.Generator(device=dev).manual_seed(1000 + rank)
+    panel_t = torch.empty(max(lc, 1) * ld, dtype=p.torch_dtype, device=dev)
+    (torch.view_as_real(panel_t) if p.is_complex else panel_t).uniform_(-1, 1, generator=g)
+    panel = MatrixView(panel_t, n, lc, ld, p) if lc > 0 else None
+    x = torch.empty(n, dtype=p.torch_dtype, device=dev)
+    (torch.view_as_real(x) if p.is_complex else x).uniform_(-1, 1, generator=torch.Generator(device=dev).manual_seed(7))
+    out = torch.empty(n, dtype=p.torch_dtype, device=dev)
+
+    def step():
+        partial_mv(p, "s", op, n, n, 1.0, panel, x, out, world, rank, nb, herm)
+        combine(out, None, 0.0)
+
+    nbytes = alg_bytes(tag, "symv", n, n, op)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    clock = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
+    clock.start()
+    time.sleep(0.3)
+    _lib.timing_enable(True)
+    l0 = _lib.launch_count()
+    dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    launches = _lib.launch_count() - l0
+    _lib.timing_enable(False)
+    kern_ms, kern_n = _lib.timing_read()
+    clocks = clock.stop()
+    ms = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms_step = ms.item()
+    my_bytes = 0
+    for j in range(rank, -(-n // nb), world):
+        c0, c1 = j * nb, min(n, (j + 1) * nb)
+        my_bytes += ((c1 - c0) * (c1 - c0 + 1) // 2 + (n - c1) * (c1 - c0)) * p.element_bytes
+    return dict(tag=tag, family="symv", op=op, m=n, n=n, ld=ld, nbytes=nbytes, ms_step=ms_step,
+                gbs=nbytes / (ms_step * 1e-3) / 1e9, kern_avg_ms=kern_ms / max(kern_n, 1), kern_launches=kern_n,
+                launches=launches, plan=_lib.last_plan(), clocks=clocks, my_bytes=my_bytes, nb=nb)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}: launch N>1 under torchrun")
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    hbm_peak, peak_src = measured_peaks()
+    if world > 1:
+        res = bench_mgpu(args, dev, rank, world)
+    else:
+        res = bench_single(args, dev, rank)
+    tag, family, op = res["tag"], res["family"], res["op"]
+    achieved_kernel = (res.get("my_bytes", res["nbytes"]) / (res["kern_avg_ms"] * 1e-3) / 1e9
+                       if res["kern_avg_ms"] > 0 else None)
+    if rank == 0:
+        opname = args.op
+        if world > 1:
+            workload = (f"mgpu {opname} N={res['n']} 1D block-column-cyclic nb={res['nb']} over {world} GPUs, "
+                        f"NCCL reduce of y (weak scaling: n = 32768*sqrt(G))")
+        elif args.op == "dsymv" and res["n"] == 32768:
+            workload = "DSYMV lower N=32768 (BASELINE configs[1])"
+        else:
+            workload = f"{opname} m={res['m']} n={res['n']}"
+        prof_traffic = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+                prof_traffic = json.load(fh).get(f"{opname}_{res['n']}")
+        except Exception:
+            pass
+        line = {
+            "metric": "achieved HBM GB/s (DSYMV lower, algorithmic bytes)" if family == "symv"
+            else "achieved HBM GB/s (GEMV, algorithmic bytes)",
+            "value": round(res["gbs"], 2),
+            "unit": "GB/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": round(res["ms_step"], 5),
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": {"s": "f32", "d": "f64", "c": "c64", "z": "c128"}[tag],
+            "data": "synthetic U(-1,1), generated on device",
+            "config": {"workload": workload, "op": opname, "m": res["m"], "n": res["n"], "ld": res["ld"],
+                       "uplo_or_trans": op, "alpha": 1.0, "beta": 0.0,
+                       "l2": "inputs > 126 MB L2 (A streamed from HBM every step), no flush",
+                       "parallelism": f"{world} GPU" + ("s, one process each" if world > 1 else "")},
+            "pct_of_copy_peak": round(100 * res["gbs"] / hbm_peak, 2),
+            "gflops": round(res.get("nflops", 0) / (res["ms_step"] * 1e-3) / 1e9, 2) if res.get("nflops") else None,
+            "roofline": {"bound": "hbm", "achieved": round(achieved_kernel, 2) if achieved_kernel else None,
+                         "peak": hbm_peak, "unit": "GB/s",
+                         "frac": round(achieved_kernel / hbm_peak, 4) if achieved_kernel else None,
+                         "traffic": prof_traffic, "peak_source": peak_src,
+                         "kernel": res["plan"].split()[0] + "_kernel", "kernel_avg_ms": round(res["kern_avg_ms"], 5),
+                         "spec_peak_gbs": SPEC_HBM_GBS,
+                         "bytes_per_launch": res.get("my_bytes", res["nbytes"])},
+            "clocks": res["clocks"],
+            "gpu_launches": res["launches"],
+            "plan": res["plan"],
+        }
+        if "e2e" in res:
+            line["e2e"] = res["e2e"]
+        else:
+            line["e2e"] = None
+        if not args.no_cpu and world == 1:
+            line["cpu_baseline"] = cpu_baseline(args.cpu_seconds)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

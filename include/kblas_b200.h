@@ -1,0 +1,314 @@
+/*
+ * kblas_b200.h — C ABI of the B200-native KBLAS matrix-vector library.
+ *
+ * Drop-in boundary for the reference's GEMV / SYMV / HEMV hot path.  The
+ * reference (`blockmv`, /root/reference/pkg/src/blockmv) exposes these
+ * operations as Python functions; the paper it simulates
+ * names the C routines kblas_x{gemv,symv,hemv}[_offset|_mgpu][_async].
+ * Each entry point below cites the reference function whose behaviour it
+ * replaces.
+ *
+ * Conventions (all entry points)
+ *   - Column-major storage, BLAS argument order, device pointers.
+ *   - Element (i, j) of A lives at dA[j * lda + i].
+ *   - incx / incy must be 1 (the reference's scope).
+ *   - y is updated in place: y <- alpha * op(A) x + beta * y.
+ *   - beta == 0 writes y without reading it (NaN/Inf in y never propagate,
+ *     kernels.py:136-137, 382-383).
+ *   - alpha == 0 and beta == 1: quick return, nothing launched
+ *     (kernels.py:427-428).  alpha == 0 otherwise: y <- beta * y and A is
+ *     not read (BLAS semantics).
+ *   - Results are bit-deterministic: every cross-CTA reduction is a
+ *     fixed-order two-pass sum (no floating-point atomics).
+ *   - Synchronous variants launch on the legacy default stream (0);
+ *     `_async` variants take an explicit stream.
+ *
+ * Return codes
+ *   0   success
+ *   -k  argument k (1-based, BLAS xerbla numbering) is invalid
+ *   >0  CUDA error code (cudaError_t) from a launch or allocation
+ */
+#ifndef KBLAS_B200_H
+#define KBLAS_B200_H
+
+#include <cuComplex.h>
+#include <cuda_runtime_api.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------------ */
+/* GEMV: y = alpha * op(A) x + beta * y, op in {N, T, C}.              */
+/* Replaces blockmv.kernels.gemv (kernels.py:402-440); 'c' on a real   */
+/* precision behaves as 't' (kernels.py:422-423).                      */
+/* ------------------------------------------------------------------ */
+int kblas_sgemv(char trans, int m, int n, float alpha, const float *dA, int lda,
+                const float *dx, int incx, float beta, float *dy, int incy);
+int kblas_dgemv(char trans, int m, int n, double alpha, const double *dA, int lda,
+                const double *dx, int incx, double beta, double *dy, int incy);
+int kblas_cgemv(char trans, int m, int n, cuFloatComplex alpha, const cuFloatComplex *dA,
+                int lda, const cuFloatComplex *dx, int incx, cuFloatComplex beta,
+                cuFloatComplex *dy, int incy);
+int kblas_zgemv(char trans, int m, int n, cuDoubleComplex alpha, const cuDoubleComplex *dA,
+                int lda, const cuDoubleComplex *dx, int incx, cuDoubleComplex beta,
+                cuDoubleComplex *dy, int incy);
+
+int kblas_sgemv_async(char trans, int m, int n, float alpha, const float *dA, int lda,
+                      const float *dx, int incx, float beta, float *dy, int incy,
+                      cudaStream_t stream);
+int kblas_dgemv_async(char trans, int m, int n, double alpha, const double *dA, int lda,
+                      const double *dx, int incx, double beta, double *dy, int incy,
+                      cudaStream_t stream);
+int kblas_cgemv_async(char trans, int m, int n, cuFloatComplex alpha,
+                      const cuFloatComplex *dA, int lda, const cuFloatComplex *dx, int incx,
+                      cuFloatComplex beta, cuFloatComplex *dy, int incy, cudaStream_t stream);
+int kblas_zgemv_async(char trans, int m, int n, cuDoubleComplex alpha,
+                      const cuDoubleComplex *dA, int lda, const cuDoubleComplex *dx,
+                      int incx, cuDoubleComplex beta, cuDoubleComplex *dy, int incy,
+                      cudaStream_t stream);
+
+/* ------------------------------------------------------------------ */
+/* SYMV (s, d; and complex-symmetric c, z) / HEMV (c, z):              */
+/* y = alpha * A x + beta * y with A stored in one triangle (uplo).    */
+/* Replaces blockmv.kernels.symv / hemv / symv_hemv                    */
+/* (kernels.py:443-500).  The unreferenced triangle is never read      */
+/* except inside diagonal tiles, where it is masked (never used).      */
+/* HEMV ignores the imaginary part of the stored diagonal              */
+/* (kernels.py:353-354).                                               */
+/* ------------------------------------------------------------------ */
+int kblas_ssymv(char uplo, int n, float alpha, const float *dA, int lda, const float *dx,
+                int incx, float beta, float *dy, int incy);
+int kblas_dsymv(char uplo, int n, double alpha, const double *dA, int lda, const double *dx,
+                int incx, double beta, double *dy, int incy);
+int kblas_chemv(char uplo, int n, cuFloatComplex alpha, const cuFloatComplex *dA, int lda,
+                const cuFloatComplex *dx, int incx, cuFloatComplex beta, cuFloatComplex *dy,
+                int incy);
+int kblas_zhemv(char uplo, int n, cuDoubleComplex alpha, const cuDoubleComplex *dA, int lda,
+                const cuDoubleComplex *dx, int incx, cuDoubleComplex beta,
+                cuDoubleComplex *dy, int incy);
+/* complex symmetric (non-Hermitian): symv_hemv(..., hermitian=False)   */
+/* on a complex precision (kernels.py:466-469).                        */
+int kblas_csymv(char uplo, int n, cuFloatComplex alpha, const cuFloatComplex *dA, int lda,
+                const cuFloatComplex *dx, int incx, cuFloatComplex beta, cuFloatComplex *dy,
+                int incy);
+int kblas_zsymv(char uplo, int n, cuDoubleComplex alpha, const cuDoubleComplex *dA, int lda,
+                const cuDoubleComplex *dx, int incx, cuDoubleComplex beta,
+                cuDoubleComplex *dy, int incy);
+
+int kblas_ssymv_async(char uplo, int n, float alpha, const float *dA, int lda,
+                      const float *dx, int incx, float beta, float *dy, int incy,
+                      cudaStream_t stream);
+int kblas_dsymv_async(char uplo, int n, double alpha, const double *dA, int lda,
+                      const double *dx, int incx, double beta, double *dy, int incy,
+                      cudaStream_t stream);
+int kblas_chemv_async(char uplo, int n, cuFloatComplex alpha, const cuFloatComplex *dA,
+                      int lda, const cuFloatComplex *dx, int incx, cuFloatComplex beta,
+                      cuFloatComplex *dy, int incy, cudaStream_t stream);
+int kblas_zhemv_async(char uplo, int n, cuDoubleComplex alpha, const cuDoubleComplex *dA,
+                      int lda, const cuDoubleComplex *dx, int incx, cuDoubleComplex beta,
+                      cuDoubleComplex *dy, int incy, cudaStream_t stream);
+int kblas_csymv_async(char uplo, int n, cuFloatComplex alpha, const cuFloatComplex *dA,
+                      int lda, const cuFloatComplex *dx, int incx, cuFloatComplex beta,
+                      cuFloatComplex *dy, int incy, cudaStream_t stream);
+int kblas_zsymv_async(char uplo, int n, cuDoubleComplex alpha, const cuDoubleComplex *dA,
+                      int lda, const cuDoubleComplex *dx, int incx, cuDoubleComplex beta,
+                      cuDoubleComplex *dy, int incy, cudaStream_t stream);
+
+/* ------------------------------------------------------------------ */
+/* Submatrix ("new interface").  dA points at the    */
+/* ORIGINAL matrix; (offset_r, offset_c) locate the m x n submatrix.   */
+/* Replaces blockmv.offset.gemv_offset (offset.py:83-143) with         */
+/* OffsetRequest(parent, row_off, col_off, sub_m, sub_n)               */
+/* (offset.py:37-51).  Loads realign to the 16-byte granule at or      */
+/* below the submatrix start and mask the lead rows.                   */
+/* ------------------------------------------------------------------ */
+int kblas_sgemv_offset(char trans, int m, int n, float alpha, const float *dA, int lda,
+                       const float *dx, int incx, float beta, float *dy, int incy,
+                       int offset_r, int offset_c);
+int kblas_dgemv_offset(char trans, int m, int n, double alpha, const double *dA, int lda,
+                       const double *dx, int incx, double beta, double *dy, int incy,
+                       int offset_r, int offset_c);
+int kblas_cgemv_offset(char trans, int m, int n, cuFloatComplex alpha,
+                       const cuFloatComplex *dA, int lda, const cuFloatComplex *dx, int incx,
+                       cuFloatComplex beta, cuFloatComplex *dy, int incy, int offset_r,
+                       int offset_c);
+int kblas_zgemv_offset(char trans, int m, int n, cuDoubleComplex alpha,
+                       const cuDoubleComplex *dA, int lda, const cuDoubleComplex *dx,
+                       int incx, cuDoubleComplex beta, cuDoubleComplex *dy, int incy,
+                       int offset_r, int offset_c);
+int kblas_sgemv_offset_async(char trans, int m, int n, float alpha, const float *dA, int lda,
+                             const float *dx, int incx, float beta, float *dy, int incy,
+                             int offset_r, int offset_c, cudaStream_t stream);
+int kblas_dgemv_offset_async(char trans, int m, int n, double alpha, const double *dA,
+                             int lda, const double *dx, int incx, double beta, double *dy,
+                             int incy, int offset_r, int offset_c, cudaStream_t stream);
+int kblas_cgemv_offset_async(char trans, int m, int n, cuFloatComplex alpha,
+                             const cuFloatComplex *dA, int lda, const cuFloatComplex *dx,
+                             int incx, cuFloatComplex beta, cuFloatComplex *dy, int incy,
+                             int offset_r, int offset_c, cudaStream_t stream);
+int kblas_zgemv_offset_async(char trans, int m, int n, cuDoubleComplex alpha,
+                             const cuDoubleComplex *dA, int lda, const cuDoubleComplex *dx,
+                             int incx, cuDoubleComplex beta, cuDoubleComplex *dy, int incy,
+                             int offset_r, int offset_c, cudaStream_t stream);
+
+/* Diagonal submatrix of a triangle-stored matrix: n x n block at      */
+/* (offset, offset).  Replaces blockmv.offset.symv_hemv_offset         */
+/* (offset.py:146-208).                                                */
+int kblas_ssymv_offset(char uplo, int n, float alpha, const float *dA, int lda,
+                       const float *dx, int incx, float beta, float *dy, int incy,
+                       int offset);
+int kblas_dsymv_offset(char uplo, int n, double alpha, const double *dA, int lda,
+                       const double *dx, int incx, double beta, double *dy, int incy,
+                       int offset);
+int kblas_chemv_offset(char uplo, int n, cuFloatComplex alpha, const cuFloatComplex *dA,
+                       int lda, const cuFloatComplex *dx, int incx, cuFloatComplex beta,
+                       cuFloatComplex *dy, int incy, int offset);
+int kblas_zhemv_offset(char uplo, int n, cuDoubleComplex alpha, const cuDoubleComplex *dA,
+                       int lda, const cuDoubleComplex *dx, int incx, cuDoubleComplex beta,
+                       cuDoubleComplex *dy, int incy, int offset);
+int kblas_csymv_offset(char uplo, int n, cuFloatComplex alpha, const cuFloatComplex *dA,
+                       int lda, const cuFloatComplex *dx, int incx, cuFloatComplex beta,
+                       cuFloatComplex *dy, int incy, int offset);
+int kblas_zsymv_offset(char uplo, int n, cuDoubleComplex alpha, const cuDoubleComplex *dA,
+                       int lda, const cuDoubleComplex *dx, int incx, cuDoubleComplex beta,
+                       cuDoubleComplex *dy, int incy, int offset);
+int kblas_ssymv_offset_async(char uplo, int n, float alpha, const float *dA, int lda,
+                             const float *dx, int incx, float beta, float *dy, int incy,
+                             int offset, cudaStream_t stream);
+int kblas_dsymv_offset_async(char uplo, int n, double alpha, const double *dA, int lda,
+                             const double *dx, int incx, double beta, double *dy, int incy,
+                             int offset, cudaStream_t stream);
+int kblas_chemv_offset_async(char uplo, int n, cuFloatComplex alpha,
+                             const cuFloatComplex *dA, int lda, const cuFloatComplex *dx,
+                             int incx, cuFloatComplex beta, cuFloatComplex *dy, int incy,
+                             int offset, cudaStream_t stream);
+int kblas_zhemv_offset_async(char uplo, int n, cuDoubleComplex alpha,
+                             const cuDoubleComplex *dA, int lda, const cuDoubleComplex *dx,
+                             int incx, cuDoubleComplex beta, cuDoubleComplex *dy, int incy,
+                             int offset, cudaStream_t stream);
+int kblas_csymv_offset_async(char uplo, int n, cuFloatComplex alpha,
+                             const cuFloatComplex *dA, int lda, const cuFloatComplex *dx,
+                             int incx, cuFloatComplex beta, cuFloatComplex *dy, int incy,
+                             int offset, cudaStream_t stream);
+int kblas_zsymv_offset_async(char uplo, int n, cuDoubleComplex alpha,
+                             const cuDoubleComplex *dA, int lda, const cuDoubleComplex *dx,
+                             int incx, cuDoubleComplex beta, cuDoubleComplex *dy, int incy,
+                             int offset, cudaStream_t stream);
+
+/* ------------------------------------------------------------------ */
+/* Multi-GPU, 1D block-column-cyclic layout (PAPER.md:458-476;          */
+/* blockmv.multidevice, multidevice.py:72-284).  Block column j (width */
+/* nb) of the global m x n matrix lives on GPU j mod ngpus, packed      */
+/* contiguously into that GPU's local panel dA[g] (ld = lda, common).  */
+/* dx[g] holds a full replica of x on GPU g.  dy[0] is the root: it    */
+/* holds y on input and the result on output; dy[g] for g > 0 must be  */
+/* full-length device buffers on GPU g and receive that GPU's partial. */
+/* device_ids may be NULL (GPU g = CUDA device g); several logical     */
+/* GPUs may share one device.                                          */
+/* The sum of partials is done by a root kernel that reads each        */
+/* partial in device order over NVLink peer memory (or after a peer     */
+/* copy when peer access is unavailable), fused with beta * y:         */
+/* deterministic, matching multidevice.py:161,176,276,282-283.          */
+/* Replaces gemv_mgpu (multidevice.py:119-180) and symv_hemv_mgpu      */
+/* (multidevice.py:183-284); for SYMV/HEMV nb is the distribution      */
+/* block width (must equal the kernel block size in the reference,     */
+/* multidevice.py:205-208; here any nb >= 1 is accepted).              */
+/* ------------------------------------------------------------------ */
+int kblas_sgemv_mgpu(char trans, int m, int n, float alpha, float *const *dA, int lda,
+                     float *const *dx, int incx, float beta, float *const *dy, int incy,
+                     int ngpus, int nb, const int *device_ids);
+int kblas_dgemv_mgpu(char trans, int m, int n, double alpha, double *const *dA, int lda,
+                     double *const *dx, int incx, double beta, double *const *dy, int incy,
+                     int ngpus, int nb, const int *device_ids);
+int kblas_cgemv_mgpu(char trans, int m, int n, cuFloatComplex alpha,
+                     cuFloatComplex *const *dA, int lda, cuFloatComplex *const *dx, int incx,
+                     cuFloatComplex beta, cuFloatComplex *const *dy, int incy, int ngpus,
+                     int nb, const int *device_ids);
+int kblas_zgemv_mgpu(char trans, int m, int n, cuDoubleComplex alpha,
+                     cuDoubleComplex *const *dA, int lda, cuDoubleComplex *const *dx,
+                     int incx, cuDoubleComplex beta, cuDoubleComplex *const *dy, int incy,
+                     int ngpus, int nb, const int *device_ids);
+int kblas_ssymv_mgpu(char uplo, int n, float alpha, float *const *dA, int lda,
+                     float *const *dx, int incx, float beta, float *const *dy, int incy,
+                     int ngpus, int nb, const int *device_ids);
+int kblas_dsymv_mgpu(char uplo, int n, double alpha, double *const *dA, int lda,
+                     double *const *dx, int incx, double beta, double *const *dy, int incy,
+                     int ngpus, int nb, const int *device_ids);
+int kblas_chemv_mgpu(char uplo, int n, cuFloatComplex alpha, cuFloatComplex *const *dA,
+                     int lda, cuFloatComplex *const *dx, int incx, cuFloatComplex beta,
+                     cuFloatComplex *const *dy, int incy, int ngpus, int nb,
+                     const int *device_ids);
+int kblas_zhemv_mgpu(char uplo, int n, cuDoubleComplex alpha, cuDoubleComplex *const *dA,
+                     int lda, cuDoubleComplex *const *dx, int incx, cuDoubleComplex beta,
+                     cuDoubleComplex *const *dy, int incy, int ngpus, int nb,
+                     const int *device_ids);
+int kblas_csymv_mgpu(char uplo, int n, cuFloatComplex alpha, cuFloatComplex *const *dA,
+                     int lda, cuFloatComplex *const *dx, int incx, cuFloatComplex beta,
+                     cuFloatComplex *const *dy, int incy, int ngpus, int nb,
+                     const int *device_ids);
+int kblas_zsymv_mgpu(char uplo, int n, cuDoubleComplex alpha, cuDoubleComplex *const *dA,
+                     int lda, cuDoubleComplex *const *dx, int incx, cuDoubleComplex beta,
+                     cuDoubleComplex *const *dy, int incy, int ngpus, int nb,
+                     const int *device_ids);
+
+/* Per-device partial only (no cross-device reduction, no beta): the    */
+/* building block for one-process-per-GPU deployments, where the       */
+/* caller combines partials with an NCCL reduce.  Computes on the      */
+/* current device: dy_partial = alpha * (local contribution of GPU g). */
+/* prec: 's','d','c','z'; op: 'n','t','c' (gemv) or 'l','u' (symv,     */
+/* hemv when hermitian != 0).  alpha points to a host scalar of the    */
+/* precision's type.                                                   */
+int kblas_mv_mgpu_partial_async(char prec, char kind, char op, int m, int n,
+                                const void *alpha, const void *dA_local, int lda,
+                                const void *dx, void *dy_partial, int ngpus, int gpu,
+                                int nb, int hermitian, cudaStream_t stream);
+
+/* ------------------------------------------------------------------ */
+/* mgpu helpers: column count held by one GPU under */
+/* the cyclic layout (multidevice.py:38-43), and the local ld (rows    */
+/* padded to 32 elements, multidevice.py:46-52,85).                    */
+/* ------------------------------------------------------------------ */
+int kblas_mgpu_local_cols(int n, int nb, int ngpus, int gpu);
+int kblas_mgpu_local_ld(int m);
+/* Copy the global host matrix into (pre-allocated) local panels, and   */
+/* back (blockmv.distribute / gather, multidevice.py:72-110).  esize is */
+/* the element size in bytes.                                          */
+int kblas_setmatrix_mgpu_1d(int m, int n, size_t esize, const void *hA, int ldha,
+                            void *const *dA, int ldda, int ngpus, int nb,
+                            const int *device_ids);
+int kblas_getmatrix_mgpu_1d(int m, int n, size_t esize, void *const *dA, int ldda,
+                            void *hA, int ldha, int ngpus, int nb, const int *device_ids);
+
+/* Single-GPU host<->device panel copies (cuBLAS-style set/getmatrix):  */
+/* rows x cols column-major, element size esize, pitched by ldh / ldd.  */
+/* Used by the Python API to upload only the referenced part of a host  */
+/* operand (e.g. the stored triangle, block column by block column).   */
+int kblas_setmatrix_async(int rows, int cols, size_t esize, const void *hA, int ldha, void *dA,
+                          int ldda, cudaStream_t stream);
+int kblas_getmatrix_async(int rows, int cols, size_t esize, const void *dA, int ldda, void *hA,
+                          int ldha, cudaStream_t stream);
+
+/* ------------------------------------------------------------------ */
+/* Instrumentation (bench/test harness).                               */
+/* ------------------------------------------------------------------ */
+/* Number of kernels this library has launched since load.             */
+unsigned long long kblas_launch_count(void);
+/* When enabled, the library brackets every main (matrix-streaming)    */
+/* kernel with CUDA events on its launch stream.  kblas_timing_read     */
+/* synchronises those events and returns the summed milliseconds and   */
+/* the number of timed launches, then clears the record.               */
+int kblas_timing_enable(int enable);
+int kblas_timing_read(double *total_ms, int *launches);
+/* Description of the last plan chosen for a call on this thread      */
+/* (kernel family, grid, items, workspace bytes) as a NUL-terminated   */
+/* string; for reports and tests.                                      */
+const char *kblas_last_plan(void);
+/* Library version string. */
+const char *kblas_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* KBLAS_B200_H */

@@ -1,0 +1,174 @@
+"""ctypes binding of the C ABI declared in include/kblas_b200.h.
+
+The shared library is the only compute path: if it is missing or cannot be
+loaded this module raises, it never falls back to a CPU implementation.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from ctypes import POINTER, c_char, c_double, c_float, c_int, c_size_t, c_ulonglong, c_void_p
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libkblas_b200.so")
+HEADER = os.path.join(os.path.dirname(HERE), "include", "kblas_b200.h")
+
+
+class c_complex64(ctypes.Structure):
+    _fields_ = [("re", c_float), ("im", c_float)]
+
+
+class c_complex128(ctypes.Structure):
+    _fields_ = [("re", c_double), ("im", c_double)]
+
+
+SCALAR_CTYPE = {"s": c_float, "d": c_double, "c": c_complex64, "z": c_complex128}
+
+
+def scalar(tag: str, value):
+    """Host scalar of precision `tag` for a by-value C argument."""
+    ct = SCALAR_CTYPE[tag]
+    if tag in "cz":
+        v = complex(value)
+        return ct(v.real, v.imag)
+    if isinstance(value, complex):
+        if value.imag != 0:
+            raise ValueError(f"complex scalar {value!r} for real precision {tag!r}")
+        value = value.real
+    return ct(float(value))
+
+
+_lock = threading.Lock()
+_lib = None
+
+_GEMV = ["trans", "m", "n", "alpha", "A", "lda", "x", "incx", "beta", "y", "incy"]
+_SYMV = ["uplo", "n", "alpha", "A", "lda", "x", "incx", "beta", "y", "incy"]
+SYMV_NAMES = {"s": ["ssymv"], "d": ["dsymv"], "c": ["chemv", "csymv"], "z": ["zhemv", "zsymv"]}
+
+
+def _argtypes(kind, tag, extra=()):
+    s = SCALAR_CTYPE[tag]
+    if kind == "gemv":
+        base = [c_char, c_int, c_int, s, c_void_p, c_int, c_void_p, c_int, s, c_void_p, c_int]
+    else:
+        base = [c_char, c_int, s, c_void_p, c_int, c_void_p, c_int, s, c_void_p, c_int]
+    return base + list(extra)
+
+
+def _mgpu_argtypes(kind, tag):
+    s = SCALAR_CTYPE[tag]
+    pp = POINTER(c_void_p)
+    if kind == "gemv":
+        return [c_char, c_int, c_int, s, pp, c_int, pp, c_int, s, pp, c_int, c_int, c_int, POINTER(c_int)]
+    return [c_char, c_int, s, pp, c_int, pp, c_int, s, pp, c_int, c_int, c_int, POINTER(c_int)]
+
+
+def load():
+    """Load (once) and return the library with all prototypes set."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with `python -m paper_1410_1726_b200._build` "
+                "(there is no CPU fallback)"
+            )
+        lib = ctypes.CDLL(LIB_PATH)
+        for tag in "sdcz":
+            for suffix, extra in (
+                ("", ()),
+                ("_async", (c_void_p,)),
+                ("_offset", (c_int, c_int)),
+                ("_offset_async", (c_int, c_int, c_void_p)),
+            ):
+                f = getattr(lib, f"kblas_{tag}gemv{suffix}")
+                f.argtypes = _argtypes("gemv", tag, extra)
+                f.restype = c_int
+            getattr(lib, f"kblas_{tag}gemv_mgpu").argtypes = _mgpu_argtypes("gemv", tag)
+            getattr(lib, f"kblas_{tag}gemv_mgpu").restype = c_int
+            for name in SYMV_NAMES[tag]:
+                for suffix, extra in (
+                    ("", ()),
+                    ("_async", (c_void_p,)),
+                    ("_offset", (c_int,)),
+                    ("_offset_async", (c_int, c_void_p)),
+                ):
+                    f = getattr(lib, f"kblas_{name}{suffix}")
+                    f.argtypes = _argtypes("symv", tag, extra)
+                    f.restype = c_int
+                getattr(lib, f"kblas_{name}_mgpu").argtypes = _mgpu_argtypes("symv", tag)
+                getattr(lib, f"kblas_{name}_mgpu").restype = c_int
+        lib.kblas_mv_mgpu_partial_async.argtypes = [
+            c_char, c_char, c_char, c_int, c_int, c_void_p, c_void_p, c_int, c_void_p, c_void_p,
+            c_int, c_int, c_int, c_int, c_void_p,
+        ]
+        lib.kblas_mv_mgpu_partial_async.restype = c_int
+        lib.kblas_mgpu_local_cols.argtypes = [c_int, c_int, c_int, c_int]
+        lib.kblas_mgpu_local_cols.restype = c_int
+        lib.kblas_mgpu_local_ld.argtypes = [c_int]
+        lib.kblas_mgpu_local_ld.restype = c_int
+        for name in ("kblas_setmatrix_mgpu_1d", "kblas_getmatrix_mgpu_1d"):
+            getattr(lib, name).restype = c_int
+        lib.kblas_setmatrix_mgpu_1d.argtypes = [
+            c_int, c_int, c_size_t, c_void_p, c_int, POINTER(c_void_p), c_int, c_int, c_int, POINTER(c_int)]
+        lib.kblas_getmatrix_mgpu_1d.argtypes = [
+            c_int, c_int, c_size_t, POINTER(c_void_p), c_int, c_void_p, c_int, c_int, c_int, POINTER(c_int)]
+        for name in ("kblas_setmatrix_async", "kblas_getmatrix_async"):
+            getattr(lib, name).argtypes = [c_int, c_int, c_size_t, c_void_p, c_int, c_void_p, c_int, c_void_p]
+            getattr(lib, name).restype = c_int
+        lib.kblas_launch_count.restype = c_ulonglong
+        lib.kblas_launch_count.argtypes = []
+        lib.kblas_timing_enable.argtypes = [c_int]
+        lib.kblas_timing_enable.restype = c_int
+        lib.kblas_timing_read.argtypes = [POINTER(c_double), POINTER(c_int)]
+        lib.kblas_timing_read.restype = c_int
+        lib.kblas_last_plan.restype = ctypes.c_char_p
+        lib.kblas_last_plan.argtypes = []
+        lib.kblas_version.restype = ctypes.c_char_p
+        lib.kblas_version.argtypes = []
+        _lib = lib
+        return lib
+
+
+def header_symbols() -> list[str]:
+    """Every kblas_* function declared in include/kblas_b200.h."""
+    import re
+
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(kblas_\w+)\s*\(", text)))
+
+
+class KblasError(RuntimeError):
+    pass
+
+
+def check(rc: int, what: str, argnames=None):
+    if rc == 0:
+        return
+    if rc < 0:
+        k = -rc
+        name = argnames[k - 1] if argnames and 0 < k <= len(argnames) else f"#{k}"
+        raise ValueError(f"{what}: invalid argument {k} ({name})")
+    raise KblasError(f"{what}: CUDA error {rc}")
+
+
+def launch_count() -> int:
+    return int(load().kblas_launch_count())
+
+
+def last_plan() -> str:
+    return load().kblas_last_plan().decode()
+
+
+def timing_enable(on: bool):
+    load().kblas_timing_enable(1 if on else 0)
+
+
+def timing_read() -> tuple[float, int]:
+    ms, n = c_double(0.0), c_int(0)
+    check(load().kblas_timing_read(ctypes.byref(ms), ctypes.byref(n)), "kblas_timing_read")
+    return ms.value, n.value

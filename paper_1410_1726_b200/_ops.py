@@ -1,0 +1,132 @@
+"""Operand marshalling between the Python API and the C ABI.
+
+Shared by kernels.py, offset.py and multidevice.py: moves host operands to
+HBM when needed, builds fresh output vectors (the reference never mutates
+its inputs, SURVEY.md §8b "Ownership"), and calls the `_async` entry
+points on the current torch stream.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from .core import MatrixView, Precision, _is_torch
+
+SYMV_FN = {("s", False): "ssymv", ("d", False): "dsymv", ("c", True): "chemv", ("z", True): "zhemv",
+           ("c", False): "csymv", ("z", False): "zsymv"}
+
+
+def require_cuda():
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1410_1726_b200 needs a CUDA device (sm_100a); none is visible")
+
+
+def device_for(*objs) -> torch.device:
+    require_cuda()
+    for o in objs:
+        d = o.data if isinstance(o, MatrixView) else o
+        if _is_torch(d) and d.is_cuda:
+            return d.device
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream_handle(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def vector_in(v, length: int, prec: Precision, name: str, device) -> torch.Tensor:
+    """1-D operand of the precision's dtype on `device` (kernels.py:395-399)."""
+    if _is_torch(v):
+        if v.dim() != 1 or v.numel() != length:
+            raise ValueError(f"{name} must be a vector of length {length}")
+        return v.to(device=device, dtype=prec.torch_dtype).contiguous()
+    arr = np.asarray(v, dtype=prec.dtype)
+    if arr.ndim != 1 or arr.size != length:
+        raise ValueError(f"{name} must be a vector of length {length}")
+    t = torch.from_numpy(np.ascontiguousarray(arr))
+    return t.to(device, non_blocking=t.is_pinned())
+
+
+def output_like(y_in, y_dev: torch.Tensor, beta_zero: bool, inplace: bool) -> torch.Tensor:
+    """Buffer the kernel updates in place.  beta == 0 never reads y."""
+    if inplace:
+        if not (_is_torch(y_in) and y_in.is_cuda and y_in.is_contiguous() and y_dev.data_ptr() == y_in.data_ptr()):
+            raise ValueError("inplace=True needs y to be a contiguous CUDA tensor of the operand dtype")
+        return y_in
+    if beta_zero:
+        return torch.empty_like(y_dev)
+    if _is_torch(y_in) and y_dev.data_ptr() == y_in.data_ptr():
+        return y_dev.clone()
+    return y_dev  # already a private copy
+
+
+def result_like(y_in, y_out: torch.Tensor):
+    """numpy in -> numpy out (one D2H read); torch in -> torch out (stays in HBM)."""
+    if _is_torch(y_in):
+        return y_out
+    return y_out.cpu().numpy()
+
+
+def matrix_in(view: MatrixView, device, lower_tri: str | None = None):
+    """(device pointer of element (0, 0) of the view, lda, keepalive).
+
+    A CUDA view is used in place.  Host data is copied column-wise: the
+    view's columns (all ld rows, so the stride is kept) and, for a stored
+    triangle, only the rows at or below ('l') / above ('u') each 256-column
+    block's first column."""
+    esize = view.precision.element_bytes
+    if view.on_device:
+        return view.data.data_ptr() + view.linear_index(0, 0) * esize, view.ld, view.data
+    data = view.data
+    host = data.numpy() if _is_torch(data) else data
+    ld, c0, nc = view.ld, view.col_offset, view.cols
+    src = np.ascontiguousarray(host[c0 * ld: (c0 + nc) * ld])
+    dev = torch.empty(nc * ld, dtype=view.precision.torch_dtype, device=device)
+    lib = _lib.load()
+    st = stream_handle(device)
+    hptr, dptr = src.ctypes.data, dev.data_ptr()
+    r0 = view.row_offset
+    with torch.cuda.device(device):
+        if lower_tri is None:
+            blocks = [(0, nc, 0, ld)]
+        else:
+            # only the stored triangle, 256-column blocks (SYMV/HEMV)
+            blocks = []
+            for b0 in range(0, nc, 256):
+                b1 = min(nc, b0 + 256)
+                lo, hi = (r0 + b0, r0 + view.rows) if lower_tri == "l" else (r0, r0 + b1)
+                blocks.append((b0, b1, lo, hi))
+        for b0, b1, lo, hi in blocks:
+            off = (b0 * ld + lo) * esize
+            _lib.check(lib.kblas_setmatrix_async(hi - lo, b1 - b0, esize, hptr + off, ld, dptr + off, ld, st),
+                       "kblas_setmatrix_async")
+        if not np.shares_memory(src, host):
+            # a private staging copy must outlive the async copies
+            torch.cuda.current_stream(device).synchronize()
+    return dev.data_ptr() + view.row_offset * esize, ld, dev
+
+
+def call_gemv(prec: Precision, trans: str, m: int, n: int, alpha, a_ptr: int, lda: int,
+              x: torch.Tensor, beta, y: torch.Tensor, device, off_r: int = 0, off_c: int = 0):
+    lib = _lib.load()
+    f = getattr(lib, f"kblas_{prec.tag}gemv_offset_async")
+    with torch.cuda.device(device):
+        rc = f(trans.encode(), m, n, _lib.scalar(prec.tag, alpha), a_ptr, lda, x.data_ptr(), 1,
+               _lib.scalar(prec.tag, beta), y.data_ptr(), 1, off_r, off_c, stream_handle(device))
+    _lib.check(rc, f"kblas_{prec.tag}gemv_offset",
+               ["trans", "m", "n", "alpha", "A", "lda", "x", "incx", "beta", "y", "incy", "offset_r", "offset_c"])
+
+
+def call_symv(prec: Precision, hermitian: bool, uplo: str, d: int, alpha, a_ptr: int, lda: int,
+              x: torch.Tensor, beta, y: torch.Tensor, device, offset: int = 0):
+    """offset: the (offset, offset) diagonal position of the d x d operand from a_ptr."""
+    lib = _lib.load()
+    name = SYMV_FN[(prec.tag, bool(hermitian))]
+    f = getattr(lib, f"kblas_{name}_offset_async")
+    with torch.cuda.device(device):
+        rc = f(uplo.encode(), d, _lib.scalar(prec.tag, alpha), a_ptr, lda, x.data_ptr(), 1,
+               _lib.scalar(prec.tag, beta), y.data_ptr(), 1, offset, stream_handle(device))
+    _lib.check(rc, f"kblas_{name}_offset",
+               ["uplo", "n", "alpha", "A", "lda", "x", "incx", "beta", "y", "incy", "offset"])

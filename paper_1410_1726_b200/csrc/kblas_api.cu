@@ -1,0 +1,724 @@
+// kblas_api.cu — C ABI (include/kblas_b200.h) over the sm_100a kernels.
+//
+// Planning per call: pick the load path (256-bit vectors when the column
+// stride is 32-byte aligned, else one element per lane), realign the
+// submatrix start down to the 32-byte granule (offset realignment,
+// PAPER.md:826-863 / offset.py:66-71), size the stream-K grid to
+// #SM x occupancy, and launch main kernel + fixed-order epilogue on the
+// caller's stream.  Workspace for cross-CTA partials is cached per
+// (device, stream) and grows only; tile tables for SYMV/HEMV are cached per
+// shape.  No allocation happens on the steady-state path.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/kblas_b200.h"
+#include "kblas_kernels.cuh"
+
+using namespace kb;
+
+namespace {
+
+std::atomic<unsigned long long> g_launches{0};
+thread_local std::string g_last_plan;
+
+// ------------------------------------------------------------- timing hook
+std::mutex g_tmu;
+bool g_timing = false;
+struct EvPair { cudaEvent_t a, b; int dev; };
+std::vector<EvPair> g_events;
+
+struct TimedScope {
+  bool on = false;
+  EvPair ev{};
+  cudaStream_t s;
+  explicit TimedScope(cudaStream_t st) : s(st) {
+    std::lock_guard<std::mutex> lk(g_tmu);
+    if (!g_timing) return;
+    cudaGetDevice(&ev.dev);
+    if (cudaEventCreate(&ev.a) != cudaSuccess || cudaEventCreate(&ev.b) != cudaSuccess) return;
+    on = true;
+    cudaEventRecord(ev.a, s);
+  }
+  ~TimedScope() {
+    if (!on) return;
+    cudaEventRecord(ev.b, s);
+    std::lock_guard<std::mutex> lk(g_tmu);
+    g_events.push_back(ev);
+  }
+};
+
+// ------------------------------------------------------ device properties
+std::mutex g_mu;
+std::map<int, int> g_sms;
+std::map<const void *, int> g_occ;
+
+int dev_sms() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto it = g_sms.find(dev);
+  if (it != g_sms.end()) return it->second;
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (sms <= 0) sms = 1;
+  g_sms[dev] = sms;
+  return sms;
+}
+
+int occupancy(const void *fn, int threads) {
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_occ.find(fn);
+    if (it != g_occ.end()) return it->second;
+  }
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, 0) != cudaSuccess || occ < 1)
+    occ = 1;
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_occ[fn] = occ;
+  return occ;
+}
+
+// --------------------------------------------------------------- workspace
+struct WsBuf { void *ptr = nullptr; size_t bytes = 0; };
+std::map<std::pair<int, cudaStream_t>, WsBuf> g_ws;
+
+cudaError_t workspace(size_t bytes, cudaStream_t st, void **out) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_mu);
+  WsBuf &b = g_ws[{dev, st}];
+  if (b.bytes < bytes) {
+    if (b.ptr) {
+      cudaStreamSynchronize(st);
+      cudaFree(b.ptr);
+      b.ptr = nullptr;
+      b.bytes = 0;
+    }
+    size_t want = bytes + bytes / 4 + 4096;
+    cudaError_t e = cudaMalloc(&b.ptr, want);
+    if (e != cudaSuccess) { b.ptr = nullptr; return e; }
+    b.bytes = want;
+  }
+  *out = b.ptr;
+  return cudaSuccess;
+}
+
+inline long long cdiv(long long a, long long b) { return (a + b - 1) / b; }
+inline size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
+
+// ------------------------------------------------------------ scalar utils
+template <class T> bool is_zero(T v);
+template <> bool is_zero(float v) { return v == 0.f; }
+template <> bool is_zero(double v) { return v == 0.0; }
+template <> bool is_zero(float2 v) { return v.x == 0.f && v.y == 0.f; }
+template <> bool is_zero(double2 v) { return v.x == 0.0 && v.y == 0.0; }
+template <class T> bool is_one(T v);
+template <> bool is_one(float v) { return v == 1.f; }
+template <> bool is_one(double v) { return v == 1.0; }
+template <> bool is_one(float2 v) { return v.x == 1.f && v.y == 0.f; }
+template <> bool is_one(double2 v) { return v.x == 1.0 && v.y == 0.0; }
+template <class T> constexpr bool is_cplx() { return Elem<T>::cplx; }
+template <class T> const char *tname();
+template <> const char *tname<float>() { return "s"; }
+template <> const char *tname<double>() { return "d"; }
+template <> const char *tname<float2>() { return "c"; }
+template <> const char *tname<double2>() { return "z"; }
+
+inline int launched(int n = 1) { g_launches += n; return 0; }
+
+// ---------------------------------------------------------- load path
+// vec: 256-bit loads; needs lda*esize % 32 == 0.  The submatrix start is
+// realigned down to its 32-byte granule and the lead rows are masked.
+template <class T> struct Path { const T *base; int lead; bool vec; };
+
+template <class T>
+int make_path(const T *A, long long lda, Path<T> *out) {
+  const uintptr_t addr = reinterpret_cast<uintptr_t>(A);
+  if (addr % alignof(T) != 0) return -1;
+  if ((lda * (long long)sizeof(T)) % 32 == 0) {
+    const int lead = (int)((addr % 32) / sizeof(T));
+    *out = Path<T>{A - lead, lead, true};
+  } else {
+    *out = Path<T>{A, 0, false};
+  }
+  return 0;
+}
+
+// ------------------------------------------------------------- configs
+// (NW warps, CW columns per warp, R vectors per lane per column)
+template <class T> struct Cfg {
+  static constexpr int V = 32 / sizeof(T);
+  // gemv N / T
+  static constexpr int G_NW = 8, G_CW = 8, G_R = 1, G_RS = V;
+  // symv / hemv: W = S_NW * S_CW columns per tile (the t1 partial traffic
+  // is 2/W of the triangle); z halves CW to stay within 128 registers
+  static constexpr int S_NW = 16, S_CW = sizeof(T) == 16 ? 4 : 8, S_R = 1, S_RS = V;
+};
+
+// ============================================================= GEMV-N
+template <class T, int V, int NW, int CW, int R>
+cudaError_t run_gemv_n(const Path<T> &pa, long long lda, int m, int n, const T *x, ColMap cm, T *y,
+                       T alpha, T beta, bool beta_zero, cudaStream_t st) {
+  constexpr int RB = 32 * V * R, CSTEP = NW * CW;
+  auto kfn = gemv_n_kernel<T, V, NW, CW, R>;
+  const long long nrb = cdiv((long long)pa.lead + m, RB);
+  const long long KS = cdiv(n, CSTEP);
+  const long long total = nrb * KS;
+  const long long P = std::min<long long>(total, (long long)dev_sms() * occupancy((const void *)kfn, NW * 32));
+  const long long per = std::max<long long>(1, total / P);
+  const long long maxslots = std::min<long long>(P, cdiv(KS, per) + 1);
+  void *ws = nullptr;
+  cudaError_t e = workspace(align256((size_t)maxslots * m * sizeof(T)), st, &ws);
+  if (e != cudaSuccess) return e;
+  GemvParams p{pa.base, lda, m, n, pa.lead, x, ws, (long long)m, total, (int)P, (int)KS, cm};
+  {
+    TimedScope ts(st);
+    kfn<<<(unsigned)P, NW * 32, 0, st>>>(p);
+  }
+  gemv_n_epilogue<T><<<(unsigned)cdiv(m, 256), 256, 0, st>>>(y, (const T *)ws, m, m, pa.lead, RB, (int)KS,
+                                                              total, (int)P, alpha, beta, beta_zero);
+  launched(2);
+  char buf[256];
+  snprintf(buf, sizeof buf, "gemv_n %s %s lead=%d m=%d n=%d RB=%d KS=%lld items=%lld P=%lld slots=%lld",
+           tname<T>(), V > 1 ? "v256" : "scalar", pa.lead, m, n, RB, KS, total, P, maxslots);
+  g_last_plan = buf;
+  return cudaGetLastError();
+}
+
+// ============================================================= GEMV-T/C
+template <class T, int V, int NW, int CW, int R, bool CONJ>
+cudaError_t run_gemv_t(const Path<T> &pa, long long lda, int m, int n, long long nglob, const T *x,
+                       ColMap cm, T *y, T alpha, T beta, bool beta_zero, cudaStream_t st) {
+  constexpr int H = 32 * V * R, CBW = NW * CW;
+  auto kfn = gemv_t_kernel<T, V, NW, CW, R, CONJ>;
+  const long long ncb = cdiv(n, CBW);
+  const long long KS = cdiv((long long)pa.lead + m, H);
+  const long long total = ncb * KS;
+  const long long P = std::min<long long>(total, (long long)dev_sms() * occupancy((const void *)kfn, NW * 32));
+  const long long per = std::max<long long>(1, total / P);
+  const long long maxslots = std::min<long long>(P, cdiv(KS, per) + 1);
+  void *ws = nullptr;
+  cudaError_t e = workspace(align256((size_t)maxslots * ncb * CBW * sizeof(T)), st, &ws);
+  if (e != cudaSuccess) return e;
+  const long long ws_ld = ncb * CBW;
+  GemvParams p{pa.base, lda, m, n, pa.lead, x, ws, ws_ld, total, (int)P, (int)KS, cm};
+  {
+    TimedScope ts(st);
+    kfn<<<(unsigned)P, NW * 32, 0, st>>>(p);
+  }
+  gemv_t_epilogue<T><<<(unsigned)cdiv(nglob, 256), 256, 0, st>>>(y, (const T *)ws, ws_ld, nglob, CBW,
+                                                                  (int)KS, total, (int)P, cm, alpha, beta,
+                                                                  beta_zero);
+  launched(2);
+  char buf[256];
+  snprintf(buf, sizeof buf, "gemv_t %s %s%s lead=%d m=%d n=%d H=%d KS=%lld items=%lld P=%lld slots=%lld",
+           tname<T>(), V > 1 ? "v256" : "scalar", CONJ ? " conj" : "", pa.lead, m, n, H, KS, total, P,
+           maxslots);
+  g_last_plan = buf;
+  return cudaGetLastError();
+}
+
+// ============================================================= SYMV/HEMV
+struct TileTable {
+  SymTile *dev = nullptr;
+  int ntiles = 0;
+  long long total = 0;
+  long long maxslots = 0;
+};
+std::map<std::vector<long long>, TileTable> g_tiles;
+
+// Tiles for the local panel of GPU g under the block-cyclic layout (G=1,
+// nb=d for a single GPU): every owned block column is cut into W-wide tiles.
+cudaError_t tile_table(int d, int lead, bool lower, int W, int H, ColMap cm, int ncols_local, long long P,
+                       TileTable *out) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::vector<long long> key{dev, d, lead, lower, W, H, cm.G, cm.g, cm.nb, ncols_local, P};
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_tiles.find(key);
+    if (it != g_tiles.end()) { *out = it->second; return cudaSuccess; }
+  }
+  std::vector<SymTile> tiles;
+  long long prefix = 0;
+  for (long long l0 = 0; l0 < ncols_local; ) {
+    // local block containing l0 and its global extent
+    const long long b = l0 / cm.nb;
+    const long long J = cm.g + b * cm.G;
+    const long long gblk0 = J * cm.nb;
+    const long long gblk1 = std::min<long long>(d, gblk0 + cm.nb);
+    const long long lblk1 = b * cm.nb + (gblk1 - gblk0);
+    for (long long s = l0; s < lblk1; s += W) {
+      SymTile t{};
+      t.lcol0 = (int)s;
+      t.gcol0 = (int)(gblk0 + (s - b * cm.nb));
+      t.ncols = (int)std::min<long long>(W, lblk1 - s);
+      t.row0 = lower ? t.gcol0 : 0;
+      t.row1 = lower ? d : std::min(d, t.gcol0 + t.ncols);
+      const long long c0 = ((long long)t.row0 + lead) / H;
+      const long long c1 = cdiv((long long)t.row1 + lead, H);
+      t.chunk0 = (int)c0;
+      t.prefix = prefix;
+      prefix += c1 - c0;
+      tiles.push_back(t);
+    }
+    l0 = (b + 1) * cm.nb;
+  }
+  TileTable tt;
+  tt.ntiles = (int)tiles.size();
+  tt.total = prefix;
+  const long long Pe = std::min<long long>(P, std::max<long long>(prefix, 1));
+  tt.maxslots = 1;
+  for (size_t k = 0; k < tiles.size(); ++k) {
+    const long long a = tiles[k].prefix;
+    const long long bnext = (k + 1 < tiles.size()) ? tiles[k + 1].prefix : prefix;
+    if (bnext > a)
+      tt.maxslots = std::max<long long>(tt.maxslots, sk_owner(bnext - 1, prefix, Pe) - sk_owner(a, prefix, Pe) + 1);
+  }
+  if (!tiles.empty()) {
+    cudaError_t e = cudaMalloc(&tt.dev, tiles.size() * sizeof(SymTile));
+    if (e != cudaSuccess) return e;
+    e = cudaMemcpy(tt.dev, tiles.data(), tiles.size() * sizeof(SymTile), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return e;
+  }
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_tiles[key] = tt;
+  *out = tt;
+  return cudaSuccess;
+}
+
+template <class T, int V, int NW, int CW, int R, bool LOWER, bool HERM>
+cudaError_t run_symv(const Path<T> &pa, long long lda, int d, const T *x, ColMap cm, int ncols_local, T *y,
+                     T alpha, T beta, bool beta_zero, cudaStream_t st) {
+  constexpr int H = 32 * V * R, W = NW * CW;
+  auto kfn = symv_kernel<T, V, NW, CW, R, LOWER, HERM>;
+  const long long Pmax = (long long)dev_sms() * occupancy((const void *)kfn, NW * 32);
+  TileTable tt;
+  cudaError_t e = tile_table(d, pa.lead, LOWER, W, H, cm, ncols_local, Pmax, &tt);
+  if (e != cudaSuccess) return e;
+  if (tt.ntiles == 0 || tt.total == 0) {  // idle GPU: partial is zero
+    scal_kernel<T><<<(unsigned)cdiv(d, 256), 256, 0, st>>>(y, d, zero<T>(), 1);
+    launched();
+    return cudaGetLastError();
+  }
+  const long long P = std::min<long long>(tt.total, Pmax);
+  const size_t b1 = align256((size_t)tt.ntiles * d * sizeof(T));
+  const size_t b2 = align256((size_t)tt.maxslots * d * sizeof(T));
+  void *ws = nullptr;
+  e = workspace(b1 + b2, st, &ws);
+  if (e != cudaSuccess) return e;
+  SymParams p{pa.base, lda, d, pa.lead, x, ws, (long long)d, (char *)ws + b1, (long long)d,
+              tt.dev, tt.ntiles, tt.total, (int)P};
+  {
+    TimedScope ts(st);
+    kfn<<<(unsigned)P, NW * 32, 0, st>>>(p);
+  }
+  symv_epilogue<T, LOWER><<<(unsigned)cdiv(d, 256), 256, 0, st>>>(y, p, alpha, beta, beta_zero);
+  launched(2);
+  char buf[256];
+  snprintf(buf, sizeof buf, "symv %s %s %s%s lead=%d d=%d W=%d H=%d tiles=%d items=%lld P=%lld slots=%lld",
+           tname<T>(), V > 1 ? "v256" : "scalar", LOWER ? "L" : "U", HERM ? " herm" : "", pa.lead, d, W, H,
+           tt.ntiles, tt.total, P, tt.maxslots);
+  g_last_plan = buf;
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------ dispatch
+template <class T>
+cudaError_t dispatch_gemv(char trans, const Path<T> &pa, long long lda, int m, int n, long long nglob,
+                          const T *x, ColMap cm, T *y, T alpha, T beta, bool beta_zero, cudaStream_t st) {
+  using C = Cfg<T>;
+  if (trans == 'n') {
+    if (pa.vec) return run_gemv_n<T, C::V, C::G_NW, C::G_CW, C::G_R>(pa, lda, m, n, x, cm, y, alpha, beta, beta_zero, st);
+    return run_gemv_n<T, 1, C::G_NW, C::G_CW, C::G_RS>(pa, lda, m, n, x, cm, y, alpha, beta, beta_zero, st);
+  }
+  if (trans == 'c' && is_cplx<T>()) {
+    if (pa.vec) return run_gemv_t<T, C::V, C::G_NW, C::G_CW, C::G_R, true>(pa, lda, m, n, nglob, x, cm, y, alpha, beta, beta_zero, st);
+    return run_gemv_t<T, 1, C::G_NW, C::G_CW, C::G_RS, true>(pa, lda, m, n, nglob, x, cm, y, alpha, beta, beta_zero, st);
+  }
+  if (pa.vec) return run_gemv_t<T, C::V, C::G_NW, C::G_CW, C::G_R, false>(pa, lda, m, n, nglob, x, cm, y, alpha, beta, beta_zero, st);
+  return run_gemv_t<T, 1, C::G_NW, C::G_CW, C::G_RS, false>(pa, lda, m, n, nglob, x, cm, y, alpha, beta, beta_zero, st);
+}
+
+template <class T, bool HERM>
+cudaError_t dispatch_symv_h(bool lower, const Path<T> &pa, long long lda, int d, const T *x, ColMap cm,
+                            int ncols_local, T *y, T alpha, T beta, bool beta_zero, cudaStream_t st) {
+  using C = Cfg<T>;
+  if (lower) {
+    if (pa.vec) return run_symv<T, C::V, C::S_NW, C::S_CW, C::S_R, true, HERM>(pa, lda, d, x, cm, ncols_local, y, alpha, beta, beta_zero, st);
+    return run_symv<T, 1, C::S_NW, C::S_CW, C::S_RS, true, HERM>(pa, lda, d, x, cm, ncols_local, y, alpha, beta, beta_zero, st);
+  }
+  if (pa.vec) return run_symv<T, C::V, C::S_NW, C::S_CW, C::S_R, false, HERM>(pa, lda, d, x, cm, ncols_local, y, alpha, beta, beta_zero, st);
+  return run_symv<T, 1, C::S_NW, C::S_CW, C::S_RS, false, HERM>(pa, lda, d, x, cm, ncols_local, y, alpha, beta, beta_zero, st);
+}
+
+template <class T>
+cudaError_t dispatch_symv(bool lower, bool herm, const Path<T> &pa, long long lda, int d, const T *x, ColMap cm,
+                          int ncols_local, T *y, T alpha, T beta, bool beta_zero, cudaStream_t st) {
+  if constexpr (is_cplx<T>()) {
+    if (herm) return dispatch_symv_h<T, true>(lower, pa, lda, d, x, cm, ncols_local, y, alpha, beta, beta_zero, st);
+  }
+  return dispatch_symv_h<T, false>(lower, pa, lda, d, x, cm, ncols_local, y, alpha, beta, beta_zero, st);
+}
+
+inline int code(cudaError_t e) { return e == cudaSuccess ? 0 : (int)e; }
+
+template <class T>
+int scal_only(T *y, long long len, T beta, cudaStream_t st) {
+  scal_kernel<T><<<(unsigned)cdiv(len, 256), 256, 0, st>>>(y, len, beta, is_zero(beta) ? 1 : 0);
+  launched();
+  g_last_plan = std::string("scal ") + tname<T>();
+  return code(cudaGetLastError());
+}
+
+// ------------------------------------------------ BLAS-level entry points
+template <class T>
+int gemv_entry(char trans, int m, int n, T alpha, const T *dA, int lda, const T *dx, int incx, T beta, T *dy,
+               int incy, int offset_r, int offset_c, cudaStream_t st) {
+  char t = (char)(trans | 0x20);
+  if (t != 'n' && t != 't' && t != 'c') return -1;
+  if (m < 0) return -2;
+  if (n < 0) return -3;
+  if (offset_r < 0 || offset_c < 0) return -12;
+  if ((long long)lda < std::max(1LL, (long long)offset_r + m)) return -6;
+  if (incx != 1) return -8;
+  if (incy != 1) return -11;
+  if (t == 'c' && !is_cplx<T>()) t = 't';  // kernels.py:422-423
+  const long long ylen = (t == 'n') ? m : n;
+  if (m == 0 || n == 0) {
+    if (ylen == 0 || is_one(beta)) return 0;
+    return scal_only(dy, ylen, beta, st);
+  }
+  if (is_zero(alpha) && is_one(beta)) return 0;  // quick return (kernels.py:427-428)
+  if (is_zero(alpha)) return scal_only(dy, ylen, beta, st);  // kernels.py:431-432
+  const T *A = dA + (long long)offset_c * lda + offset_r;
+  Path<T> pa;
+  if (make_path(A, lda, &pa) != 0) return -5;
+  ColMap cm{1, 0, 1};
+  return code(dispatch_gemv<T>(t, pa, lda, m, n, n, dx, cm, dy, alpha, beta, is_zero(beta), st));
+}
+
+template <class T>
+int symv_entry(char uplo, bool herm, int n, T alpha, const T *dA, int lda, const T *dx, int incx, T beta, T *dy,
+               int incy, int offset, cudaStream_t st) {
+  const char u = (char)(uplo | 0x20);
+  if (u != 'l' && u != 'u') return -1;
+  if (n < 0) return -2;
+  if (offset < 0) return -11;
+  if ((long long)lda < std::max(1LL, (long long)offset + n)) return -5;
+  if (incx != 1) return -7;
+  if (incy != 1) return -10;
+  if (n == 0) return 0;
+  if (is_zero(alpha) && is_one(beta)) return 0;
+  if (is_zero(alpha)) return scal_only(dy, n, beta, st);
+  const T *A = dA + (long long)offset * lda + offset;
+  Path<T> pa;
+  if (make_path(A, lda, &pa) != 0) return -4;
+  ColMap cm{1, 0, n};
+  return code(dispatch_symv<T>(u == 'l', herm, pa, lda, n, dx, cm, n, dy, alpha, beta, is_zero(beta), st));
+}
+
+// ------------------------------------------------------------------ mgpu
+long long local_cols(long long n, long long nb, long long G, long long g) {
+  long long total = 0;
+  const long long nblk = cdiv(n, nb);
+  for (long long j = g; j < nblk; j += G) total += std::min(n, (j + 1) * nb) - j * nb;
+  return total;
+}
+
+struct DevGuard {
+  int prev = 0;
+  DevGuard() { cudaGetDevice(&prev); }
+  ~DevGuard() { cudaSetDevice(prev); }
+};
+
+// partial of one GPU: y_part = alpha * (local contribution), beta ignored
+template <class T>
+int partial_entry(bool is_gemv, char op, bool herm, int m, int n, T alpha, const T *dA, int lda, const T *dx,
+                  T *dpart, int G, int g, int nb, cudaStream_t st) {
+  const long long lc = local_cols(n, nb, G, g);
+  const long long plen = is_gemv ? ((op == 'n') ? m : n) : n;
+  if (lc == 0 || is_zero(alpha)) return scal_only(dpart, plen, zero<T>(), st);
+  Path<T> pa;
+  if (make_path(dA, lda, &pa) != 0) return -5;
+  ColMap cm{G, g, nb};
+  if (is_gemv) {
+    char t = op;
+    if (t == 'c' && !is_cplx<T>()) t = 't';
+    return code(dispatch_gemv<T>(t, pa, lda, m, (int)lc, n, dx, cm, dpart, alpha, zero<T>(), true, st));
+  }
+  return code(dispatch_symv<T>(op == 'l', herm, pa, lda, n, dx, cm, (int)lc, dpart, alpha, zero<T>(), true, st));
+}
+
+template <class T>
+int mgpu_entry(bool is_gemv, char op, bool herm, int m, int n, T alpha, T *const *dA, int lda, T *const *dx,
+               T beta, T *const *dy, int ngpus, int nb, const int *device_ids) {
+  if (ngpus < 1 || ngpus > kMaxGpus) return -13;
+  if (nb < 1) return -14;
+  DevGuard guard;
+  auto devof = [&](int g) { return device_ids ? device_ids[g] : g; };
+  const long long ylen = is_gemv ? ((op == 'n') ? m : n) : n;
+  const int root = devof(0);
+  cudaError_t e;
+  if (ylen == 0) return 0;
+  if (is_zero(alpha) && is_one(beta)) return 0;
+  if (is_zero(alpha) || (is_gemv && (m == 0 || n == 0))) {
+    cudaSetDevice(root);
+    int rc = scal_only(dy[0], ylen, beta, 0);
+    if (rc) return rc;
+    return code(cudaStreamSynchronize(0));
+  }
+  // root's own partial lives in a workspace slot (dy[0] holds the input y)
+  cudaSetDevice(root);
+  void *rootbuf = nullptr;
+  // separate from the kernel workspace: allocate once per device
+  static std::mutex mu;
+  static std::map<int, WsBuf> rootbufs;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    WsBuf &b = rootbufs[root];
+    const size_t need = (size_t)ylen * sizeof(T) * (ngpus + 1);
+    if (b.bytes < need) {
+      if (b.ptr) { cudaDeviceSynchronize(); cudaFree(b.ptr); }
+      b.ptr = nullptr; b.bytes = 0;
+      if ((e = cudaMalloc(&b.ptr, need)) != cudaSuccess) return code(e);
+      b.bytes = need;
+    }
+    rootbuf = b.ptr;
+  }
+  T *root_part = static_cast<T *>(rootbuf);
+  std::vector<cudaEvent_t> done(ngpus, nullptr);
+  for (int g = 0; g < ngpus; ++g) {
+    const int dev = devof(g);
+    if ((e = cudaSetDevice(dev)) != cudaSuccess) return code(e);
+    T *out = (g == 0) ? root_part : dy[g];
+    int rc = partial_entry<T>(is_gemv, op, herm, m, n, alpha, dA[g], lda, dx[g], out, ngpus, g, nb, 0);
+    if (rc) return rc;
+    cudaEventCreateWithFlags(&done[g], cudaEventDisableTiming);
+    cudaEventRecord(done[g], 0);
+  }
+  cudaSetDevice(root);
+  PartList<T> parts{};
+  for (int g = 0; g < ngpus; ++g) {
+    const int dev = devof(g);
+    cudaStreamWaitEvent(0, done[g], 0);
+    if (g == 0 || dev == root) {
+      parts.p[g] = (g == 0) ? root_part : dy[g];
+      continue;
+    }
+    int can = 0;
+    cudaDeviceCanAccessPeer(&can, root, dev);
+    if (can) {
+      cudaError_t pe = cudaDeviceEnablePeerAccess(dev, 0);
+      if (pe == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+      else if (pe != cudaSuccess) { cudaGetLastError(); can = 0; }
+    }
+    if (can) {
+      parts.p[g] = dy[g];  // NVLink peer load inside the combine kernel
+    } else {
+      T *slot = root_part + (size_t)ylen * g;
+      if ((e = cudaMemcpyPeerAsync(slot, root, dy[g], dev, ylen * sizeof(T), 0)) != cudaSuccess) return code(e);
+      parts.p[g] = slot;
+    }
+  }
+  mgpu_combine_kernel<T><<<(unsigned)cdiv(ylen, 256), 256>>>(dy[0], parts, ngpus, ylen, beta, is_zero(beta) ? 1 : 0);
+  launched();
+  e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaStreamSynchronize(0);
+  for (auto ev : done) if (ev) cudaEventDestroy(ev);
+  return code(e);
+}
+
+}  // namespace
+
+// ====================================================================
+// extern "C" surface
+// ====================================================================
+extern "C" {
+
+#define KB_GEMV(P, T)                                                                                        \
+  int kblas_##P##gemv(char trans, int m, int n, T alpha, const T *dA, int lda, const T *dx, int incx, T beta,   \
+                      T *dy, int incy) {                                                                       \
+    return gemv_entry<T>(trans, m, n, alpha, dA, lda, dx, incx, beta, dy, incy, 0, 0, 0);                      \
+  }                                                                                                            \
+  int kblas_##P##gemv_async(char trans, int m, int n, T alpha, const T *dA, int lda, const T *dx, int incx,    \
+                            T beta, T *dy, int incy, cudaStream_t s) {                                         \
+    return gemv_entry<T>(trans, m, n, alpha, dA, lda, dx, incx, beta, dy, incy, 0, 0, s);                      \
+  }                                                                                                            \
+  int kblas_##P##gemv_offset(char trans, int m, int n, T alpha, const T *dA, int lda, const T *dx, int incx,   \
+                             T beta, T *dy, int incy, int offset_r, int offset_c) {                            \
+    return gemv_entry<T>(trans, m, n, alpha, dA, lda, dx, incx, beta, dy, incy, offset_r, offset_c, 0);        \
+  }                                                                                                            \
+  int kblas_##P##gemv_offset_async(char trans, int m, int n, T alpha, const T *dA, int lda, const T *dx,       \
+                                   int incx, T beta, T *dy, int incy, int offset_r, int offset_c,             \
+                                   cudaStream_t s) {                                                           \
+    return gemv_entry<T>(trans, m, n, alpha, dA, lda, dx, incx, beta, dy, incy, offset_r, offset_c, s);        \
+  }                                                                                                            \
+  int kblas_##P##gemv_mgpu(char trans, int m, int n, T alpha, T *const *dA, int lda, T *const *dx, int incx,   \
+                           T beta, T *const *dy, int incy, int ngpus, int nb, const int *device_ids) {         \
+    char t = (char)(trans | 0x20);                                                                             \
+    if (t != 'n' && t != 't' && t != 'c') return -1;                                                           \
+    if (m < 0) return -2;                                                                                      \
+    if (n < 0) return -3;                                                                                      \
+    if (lda < std::max(1, m)) return -6;                                                                       \
+    if (incx != 1) return -8;                                                                                  \
+    if (incy != 1) return -11;                                                                                 \
+    return mgpu_entry<T>(true, t, false, m, n, alpha, dA, lda, dx, beta, dy, ngpus, nb, device_ids);          \
+  }
+
+#define KB_SYMV(NAME, T, HERM)                                                                                \
+  int kblas_##NAME(char uplo, int n, T alpha, const T *dA, int lda, const T *dx, int incx, T beta, T *dy,      \
+                   int incy) {                                                                                 \
+    return symv_entry<T>(uplo, HERM, n, alpha, dA, lda, dx, incx, beta, dy, incy, 0, 0);                       \
+  }                                                                                                            \
+  int kblas_##NAME##_async(char uplo, int n, T alpha, const T *dA, int lda, const T *dx, int incx, T beta,     \
+                           T *dy, int incy, cudaStream_t s) {                                                  \
+    return symv_entry<T>(uplo, HERM, n, alpha, dA, lda, dx, incx, beta, dy, incy, 0, s);                       \
+  }                                                                                                            \
+  int kblas_##NAME##_offset(char uplo, int n, T alpha, const T *dA, int lda, const T *dx, int incx, T beta,    \
+                            T *dy, int incy, int offset) {                                                     \
+    return symv_entry<T>(uplo, HERM, n, alpha, dA, lda, dx, incx, beta, dy, incy, offset, 0);                  \
+  }                                                                                                            \
+  int kblas_##NAME##_offset_async(char uplo, int n, T alpha, const T *dA, int lda, const T *dx, int incx,      \
+                                  T beta, T *dy, int incy, int offset, cudaStream_t s) {                       \
+    return symv_entry<T>(uplo, HERM, n, alpha, dA, lda, dx, incx, beta, dy, incy, offset, s);                  \
+  }                                                                                                            \
+  int kblas_##NAME##_mgpu(char uplo, int n, T alpha, T *const *dA, int lda, T *const *dx, int incx, T beta,    \
+                          T *const *dy, int incy, int ngpus, int nb, const int *device_ids) {                  \
+    const char u = (char)(uplo | 0x20);                                                                        \
+    if (u != 'l' && u != 'u') return -1;                                                                       \
+    if (n < 0) return -2;                                                                                      \
+    if (lda < std::max(1, n)) return -5;                                                                       \
+    if (incx != 1) return -7;                                                                                  \
+    if (incy != 1) return -10;                                                                                 \
+    return mgpu_entry<T>(false, u, HERM, n, n, alpha, dA, lda, dx, beta, dy, ngpus, nb, device_ids);          \
+  }
+
+KB_GEMV(s, float)
+KB_GEMV(d, double)
+KB_GEMV(c, cuFloatComplex)
+KB_GEMV(z, cuDoubleComplex)
+KB_SYMV(ssymv, float, false)
+KB_SYMV(dsymv, double, false)
+KB_SYMV(chemv, cuFloatComplex, true)
+KB_SYMV(zhemv, cuDoubleComplex, true)
+KB_SYMV(csymv, cuFloatComplex, false)
+KB_SYMV(zsymv, cuDoubleComplex, false)
+
+int kblas_mv_mgpu_partial_async(char prec, char kind, char op, int m, int n, const void *alpha,
+                                const void *dA_local, int lda, const void *dx, void *dy_partial, int ngpus,
+                                int gpu, int nb, int hermitian, cudaStream_t stream) {
+  const bool is_gemv = (kind | 0x20) == 'g';
+  const char o = (char)(op | 0x20);
+  if (ngpus < 1 || gpu < 0 || gpu >= ngpus || nb < 1 || m < 0 || n < 0) return -1;
+  switch (prec | 0x20) {
+    case 's': return partial_entry<float>(is_gemv, o, false, m, n, *(const float *)alpha, (const float *)dA_local, lda, (const float *)dx, (float *)dy_partial, ngpus, gpu, nb, stream);
+    case 'd': return partial_entry<double>(is_gemv, o, false, m, n, *(const double *)alpha, (const double *)dA_local, lda, (const double *)dx, (double *)dy_partial, ngpus, gpu, nb, stream);
+    case 'c': return partial_entry<float2>(is_gemv, o, hermitian != 0, m, n, *(const float2 *)alpha, (const float2 *)dA_local, lda, (const float2 *)dx, (float2 *)dy_partial, ngpus, gpu, nb, stream);
+    case 'z': return partial_entry<double2>(is_gemv, o, hermitian != 0, m, n, *(const double2 *)alpha, (const double2 *)dA_local, lda, (const double2 *)dx, (double2 *)dy_partial, ngpus, gpu, nb, stream);
+  }
+  return -1;
+}
+
+int kblas_mgpu_local_cols(int n, int nb, int ngpus, int gpu) {
+  if (n < 0 || nb < 1 || ngpus < 1 || gpu < 0 || gpu >= ngpus) return -1;
+  return (int)local_cols(n, nb, ngpus, gpu);
+}
+
+int kblas_mgpu_local_ld(int m) { return (int)(cdiv(std::max(m, 1), 32) * 32); }
+
+static int copy_mgpu(bool to_dev, int m, int n, size_t esize, const void *hA_c, void *hA, int ldha,
+                     void *const *dA, int ldda, int ngpus, int nb, const int *device_ids) {
+  if (m < 0 || n < 0 || ngpus < 1 || nb < 1 || ldha < std::max(1, m) || ldda < std::max(1, m)) return -1;
+  DevGuard guard;
+  const long long nblk = cdiv(n, nb);
+  for (long long j = 0; j < nblk; ++j) {
+    const int g = (int)(j % ngpus);
+    const long long b = j / ngpus;
+    const long long c0 = j * nb, w = std::min<long long>(n, c0 + nb) - c0;
+    cudaSetDevice(device_ids ? device_ids[g] : g);
+    char *dp = static_cast<char *>(dA[g]) + (size_t)(b * nb) * ldda * esize;
+    cudaError_t e;
+    if (to_dev)
+      e = cudaMemcpy2D(dp, (size_t)ldda * esize, static_cast<const char *>(hA_c) + (size_t)c0 * ldha * esize,
+                       (size_t)ldha * esize, (size_t)m * esize, (size_t)w, cudaMemcpyHostToDevice);
+    else
+      e = cudaMemcpy2D(static_cast<char *>(hA) + (size_t)c0 * ldha * esize, (size_t)ldha * esize, dp,
+                       (size_t)ldda * esize, (size_t)m * esize, (size_t)w, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return (int)e;
+  }
+  return 0;
+}
+
+int kblas_setmatrix_mgpu_1d(int m, int n, size_t esize, const void *hA, int ldha, void *const *dA, int ldda,
+                            int ngpus, int nb, const int *device_ids) {
+  return copy_mgpu(true, m, n, esize, hA, nullptr, ldha, dA, ldda, ngpus, nb, device_ids);
+}
+
+int kblas_getmatrix_mgpu_1d(int m, int n, size_t esize, void *const *dA, int ldda, void *hA, int ldha, int ngpus,
+                            int nb, const int *device_ids) {
+  return copy_mgpu(false, m, n, esize, nullptr, hA, ldha, dA, ldda, ngpus, nb, device_ids);
+}
+
+int kblas_setmatrix_async(int rows, int cols, size_t esize, const void *hA, int ldha, void *dA, int ldda,
+                          cudaStream_t stream) {
+  if (rows < 0 || cols < 0 || ldha < std::max(1, rows) || ldda < std::max(1, rows)) return -1;
+  if (rows == 0 || cols == 0) return 0;
+  return code(cudaMemcpy2DAsync(dA, (size_t)ldda * esize, hA, (size_t)ldha * esize, (size_t)rows * esize,
+                                (size_t)cols, cudaMemcpyHostToDevice, stream));
+}
+
+int kblas_getmatrix_async(int rows, int cols, size_t esize, const void *dA, int ldda, void *hA, int ldha,
+                          cudaStream_t stream) {
+  if (rows < 0 || cols < 0 || ldha < std::max(1, rows) || ldda < std::max(1, rows)) return -1;
+  if (rows == 0 || cols == 0) return 0;
+  return code(cudaMemcpy2DAsync(hA, (size_t)ldha * esize, dA, (size_t)ldda * esize, (size_t)rows * esize,
+                                (size_t)cols, cudaMemcpyDeviceToHost, stream));
+}
+
+unsigned long long kblas_launch_count(void) { return g_launches.load(); }
+
+int kblas_timing_enable(int enable) {
+  std::lock_guard<std::mutex> lk(g_tmu);
+  g_timing = enable != 0;
+  return 0;
+}
+
+int kblas_timing_read(double *total_ms, int *launches) {
+  std::vector<EvPair> evs;
+  {
+    std::lock_guard<std::mutex> lk(g_tmu);
+    evs.swap(g_events);
+  }
+  DevGuard guard;
+  double tot = 0.0;
+  int rc = 0;
+  for (auto &ev : evs) {
+    cudaSetDevice(ev.dev);
+    float ms = 0.f;
+    cudaError_t e = cudaEventSynchronize(ev.b);
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, ev.a, ev.b);
+    if (e != cudaSuccess) rc = (int)e;
+    tot += ms;
+    cudaEventDestroy(ev.a);
+    cudaEventDestroy(ev.b);
+  }
+  if (total_ms) *total_ms = tot;
+  if (launches) *launches = (int)evs.size();
+  return rc;
+}
+
+const char *kblas_last_plan(void) { return g_last_plan.c_str(); }
+
+const char *kblas_version(void) { return "kblas-b200 0.1.0 (sm_100a)"; }
+
+}  // extern "C"

@@ -1,0 +1,193 @@
+// kblas_device.cuh — element arithmetic, 256-bit streaming loads and the
+// stream-K work split shared by every matrix-vector kernel.
+//
+// Element types: float (s), double (d), float2 (c), double2 (z).  Complex
+// numbers are interleaved (re, im) pairs as in the reference
+// (core.py:1-8); cuFloatComplex / cuDoubleComplex are the same layouts.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace kb {
+
+// ---------------------------------------------------------------------------
+// element arithmetic
+// ---------------------------------------------------------------------------
+template <class T> struct Elem;
+template <> struct Elem<float>   { using R = float;  static constexpr bool cplx = false; };
+template <> struct Elem<double>  { using R = double; static constexpr bool cplx = false; };
+template <> struct Elem<float2>  { using R = float;  static constexpr bool cplx = true; };
+template <> struct Elem<double2> { using R = double; static constexpr bool cplx = true; };
+
+template <class T> __host__ __device__ __forceinline__ T zero();
+template <> __host__ __device__ __forceinline__ float zero<float>() { return 0.f; }
+template <> __host__ __device__ __forceinline__ double zero<double>() { return 0.0; }
+template <> __host__ __device__ __forceinline__ float2 zero<float2>() { return make_float2(0.f, 0.f); }
+template <> __host__ __device__ __forceinline__ double2 zero<double2>() { return make_double2(0.0, 0.0); }
+
+// c + a * b
+__device__ __forceinline__ float fma_(float a, float b, float c) { return fmaf(a, b, c); }
+__device__ __forceinline__ double fma_(double a, double b, double c) { return fma(a, b, c); }
+__device__ __forceinline__ float2 fma_(float2 a, float2 b, float2 c) {
+  c.x = fmaf(a.x, b.x, c.x); c.x = fmaf(-a.y, b.y, c.x);
+  c.y = fmaf(a.x, b.y, c.y); c.y = fmaf(a.y, b.x, c.y);
+  return c;
+}
+__device__ __forceinline__ double2 fma_(double2 a, double2 b, double2 c) {
+  c.x = fma(a.x, b.x, c.x); c.x = fma(-a.y, b.y, c.x);
+  c.y = fma(a.x, b.y, c.y); c.y = fma(a.y, b.x, c.y);
+  return c;
+}
+// c + conj(a) * b  (identical to fma_ for real types)
+__device__ __forceinline__ float fmac_(float a, float b, float c) { return fmaf(a, b, c); }
+__device__ __forceinline__ double fmac_(double a, double b, double c) { return fma(a, b, c); }
+__device__ __forceinline__ float2 fmac_(float2 a, float2 b, float2 c) {
+  c.x = fmaf(a.x, b.x, c.x); c.x = fmaf(a.y, b.y, c.x);
+  c.y = fmaf(a.x, b.y, c.y); c.y = fmaf(-a.y, b.x, c.y);
+  return c;
+}
+__device__ __forceinline__ double2 fmac_(double2 a, double2 b, double2 c) {
+  c.x = fma(a.x, b.x, c.x); c.x = fma(a.y, b.y, c.x);
+  c.y = fma(a.x, b.y, c.y); c.y = fma(-a.y, b.x, c.y);
+  return c;
+}
+template <bool CONJ, class T> __device__ __forceinline__ T fmax_(T a, T b, T c) {
+  if constexpr (CONJ) return fmac_(a, b, c); else return fma_(a, b, c);
+}
+
+__device__ __forceinline__ float add_(float a, float b) { return a + b; }
+__device__ __forceinline__ double add_(double a, double b) { return a + b; }
+__device__ __forceinline__ float2 add_(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 add_(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+
+__device__ __forceinline__ float mul_(float a, float b) { return a * b; }
+__device__ __forceinline__ double mul_(double a, double b) { return a * b; }
+__device__ __forceinline__ float2 mul_(float2 a, float2 b) {
+  return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 mul_(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+
+// zero the imaginary part (Hermitian diagonal, kernels.py:353-354)
+__device__ __forceinline__ float realify(float a) { return a; }
+__device__ __forceinline__ double realify(double a) { return a; }
+__device__ __forceinline__ float2 realify(float2 a) { a.y = 0.f; return a; }
+__device__ __forceinline__ double2 realify(double2 a) { a.y = 0.0; return a; }
+
+template <class T> __device__ __forceinline__ T sel(bool p, T a) { return p ? a : zero<T>(); }
+
+__device__ __forceinline__ float shfl_xor_(float v, int m) { return __shfl_xor_sync(0xffffffffu, v, m); }
+__device__ __forceinline__ double shfl_xor_(double v, int m) { return __shfl_xor_sync(0xffffffffu, v, m); }
+__device__ __forceinline__ float2 shfl_xor_(float2 v, int m) {
+  v.x = __shfl_xor_sync(0xffffffffu, v.x, m); v.y = __shfl_xor_sync(0xffffffffu, v.y, m); return v;
+}
+__device__ __forceinline__ double2 shfl_xor_(double2 v, int m) {
+  v.x = __shfl_xor_sync(0xffffffffu, v.x, m); v.y = __shfl_xor_sync(0xffffffffu, v.y, m); return v;
+}
+template <class T> __device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) v = add_(v, shfl_xor_(v, m));
+  return v;
+}
+
+// ---------------------------------------------------------------------------
+// streaming loads.  The matrix is read exactly once, so loads bypass L1
+// allocation and are marked evict-first in L2 (the 126 MB L2 is kept for
+// the vectors and the partial-sum workspace).  sm_100 has 256-bit global
+// loads (SASS LDG.E.ENL2.256): one instruction moves 32 bytes per lane, a
+// warp 1 KiB of a column.
+// ---------------------------------------------------------------------------
+struct U8 { uint32_t r[8]; };
+__device__ __forceinline__ U8 ld_stream_v8(const void *p) {
+  U8 u;
+  asm("ld.global.nc.L1::no_allocate.L2::evict_first.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=r"(u.r[0]), "=r"(u.r[1]), "=r"(u.r[2]), "=r"(u.r[3]),
+        "=r"(u.r[4]), "=r"(u.r[5]), "=r"(u.r[6]), "=r"(u.r[7])
+      : "l"(p));
+  return u;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ float ld_stream(const float *p, uint64_t pol) {
+  float v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ld_stream(const double *p, uint64_t pol) {
+  double v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ float2 ld_stream(const float2 *p, uint64_t pol) {
+  float2 v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f32 {%0,%1}, [%2], %3;"
+      : "=f"(v.x), "=f"(v.y) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double2 ld_stream(const double2 *p, uint64_t pol) {
+  double2 v;
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+      : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+  return v;
+}
+
+// V consecutive elements starting at p.  V * sizeof(T) == 32 uses one
+// 256-bit load (p must be 32-byte aligned); V == 1 loads one element.
+template <class T, int V> struct Pack { T v[V]; };
+template <class T, int V>
+__device__ __forceinline__ Pack<T, V> ld_pack(const T *p, uint64_t pol) {
+  Pack<T, V> r;
+  if constexpr (V * sizeof(T) == 32) {
+    union { U8 u; T t[V]; } cv;
+    cv.u = ld_stream_v8(p);
+#pragma unroll
+    for (int v = 0; v < V; ++v) r.v[v] = cv.t[v];
+  } else {
+    static_assert(V == 1, "scalar path loads one element");
+    r.v[0] = ld_stream(p, pol);
+  }
+  return r;
+}
+template <class T, int V> __device__ __forceinline__ Pack<T, V> zero_pack() {
+  Pack<T, V> r;
+#pragma unroll
+  for (int v = 0; v < V; ++v) r.v[v] = zero<T>();
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// stream-K split: `total` equal work items over P CTAs; CTA c owns
+// [sk_start(c), sk_start(c+1)).  sk_owner(i) is the CTA owning item i.
+// Partial sums that straddle CTAs are written to per-CTA workspace slots
+// and summed in slot order by the epilogue kernel (deterministic).
+// ---------------------------------------------------------------------------
+__host__ __device__ __forceinline__ long long sk_start(long long c, long long total, long long P) {
+  return c * total / P;
+}
+__host__ __device__ __forceinline__ int sk_owner(long long i, long long total, long long P) {
+  return (int)(((i + 1) * P - 1) / total);
+}
+
+// 1D block-column-cyclic column map (multidevice.py:33-35, 72-93): local
+// column p of GPU g is global column (g + (p / nb) * G) * nb + p % nb.
+struct ColMap {
+  int G, g, nb;
+};
+__host__ __device__ __forceinline__ long long map_col(const ColMap &cm, long long p) {
+  if (cm.G == 1) return p;
+  long long b = p / cm.nb;
+  return (cm.g + b * cm.G) * cm.nb + (p - b * cm.nb);
+}
+// inverse: global column c -> local column, or -1 if not owned by cm.g
+__host__ __device__ __forceinline__ long long unmap_col(const ColMap &cm, long long c) {
+  if (cm.G == 1) return c;
+  long long b = c / cm.nb;
+  if (b % cm.G != cm.g) return -1;
+  return (b / cm.G) * cm.nb + (c - b * cm.nb);
+}
+
+}  // namespace kb

@@ -1,0 +1,479 @@
+// kblas_kernels.cuh — sm_100a matrix-vector kernels.
+//
+// Three streaming kernels, one per product shape, each followed by a tiny
+// fixed-order epilogue that sums cross-CTA partials and applies alpha/beta:
+//
+//   gemv_n_kernel  y = A x        (reference: _gemv_accumulate transposed=False,
+//                                  kernels.py:149-201 via run_gemv_n 209-221)
+//   gemv_t_kernel  y = A^T x / A^H x  (run_gemv_t, kernels.py:224-236)
+//   symv_kernel    y = A x from one stored triangle; every element is read
+//                  once and used twice: t1 = A_blk x_col -> rows, and
+//                  t2 = A_blk^T|H x_row -> columns (_symv_offdiag_accumulate
+//                  kernels.py:239-284 and _diag_accumulate 316-359 fused;
+//                  diagonal tiles are masked in registers, never mirrored
+//                  through memory)
+//
+// Work distribution is stream-K: the matrix is cut into equal "items"
+// (one 32*V*R-row chunk of CW columns per warp, NW warps per CTA) and CTA c
+// walks the contiguous item range [c*total/P, (c+1)*total/P).  Every CTA
+// streams the same number of bytes, so a grid of P = #SM x occupancy CTAs
+// has no wave tail (the paper's TB_R oscillation, PAPER.md:311-332,
+// 1259-1292, does not arise).
+//
+// Lanes read column segments with 256-bit loads (32 contiguous bytes per
+// lane, 1 KiB per warp per column); the warp's CW column loads are all
+// issued before any FMA so CW x 32 B per lane are in flight.
+#pragma once
+#include "kblas_device.cuh"
+
+namespace kb {
+
+struct GemvParams {
+  const void *A;    // 32-byte aligned base: physical row 0 of local column 0
+  long long lda;
+  int m, n;         // logical rows, local columns
+  int lead;         // physical row of logical row 0 (offset realignment)
+  const void *x;    // N: indexed by global column; T: indexed by logical row
+  void *ws;         // partial slots ws[slot * ws_ld + idx]
+  long long ws_ld;
+  long long total;  // work items
+  int P;            // CTAs
+  int KS;           // N: column steps per row block; T: row chunks per column block
+  ColMap cm;
+};
+
+// ---------------------------------------------------------------------------
+// GEMV-N.  Item = (row block of RB = 32*V*R rows) x (NW*CW columns); items
+// are ordered row-block-major so a CTA accumulates one row block across many
+// columns in registers, reduces across its warps through shared memory and
+// writes one partial slot per row block it touched.
+// ---------------------------------------------------------------------------
+template <class T, int V, int NW, int CW, int R>
+__global__ void __launch_bounds__(NW * 32) gemv_n_kernel(const GemvParams p) {
+  constexpr int NT = NW * 32;
+  constexpr int RB = 32 * V * R;
+  constexpr int CSTEP = NW * CW;
+  __shared__ T red[NW][RB];
+  const T *__restrict__ A = static_cast<const T *>(p.A);
+  const T *__restrict__ x = static_cast<const T *>(p.x);
+  T *__restrict__ ws = static_cast<T *>(p.ws);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t pol = policy_evict_first();
+  long long it = sk_start(blockIdx.x, p.total, p.P);
+  const long long end = sk_start(blockIdx.x + 1, p.total, p.P);
+  const long long plimit = (long long)p.lead + p.m;
+
+  while (it < end) {
+    const long long rb = it / p.KS;
+    const long long rb_first = rb * p.KS;
+    const long long stop = min(end, rb_first + p.KS);
+    const long long p0 = rb * RB;
+    T acc[R][V];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int v = 0; v < V; ++v) acc[r][v] = zero<T>();
+
+    for (long long q = it; q < stop; ++q) {
+      const int cbase = (int)(q - rb_first) * CSTEP + warp * CW;
+      Pack<T, V> a[CW][R];
+      T xv[CW];
+#pragma unroll
+      for (int j = 0; j < CW; ++j) {
+        const int col = cbase + j;
+        const bool cok = col < p.n;
+        xv[j] = cok ? __ldg(x + map_col(p.cm, col)) : zero<T>();
+        const T *colp = A + (long long)col * p.lda + p0 + lane * V;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const long long ps = p0 + r * 32 * V + lane * V;
+          a[j][r] = (cok && ps < plimit) ? ld_pack<T, V>(colp + r * 32 * V, pol) : zero_pack<T, V>();
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < CW; ++j)
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+          for (int v = 0; v < V; ++v) acc[r][v] = fma_(a[j][r].v[v], xv[j], acc[r][v]);
+    }
+
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int v = 0; v < V; ++v) red[warp][r * 32 * V + lane * V + v] = acc[r][v];
+    __syncthreads();
+    const long long slot = (long long)blockIdx.x - sk_owner(rb_first, p.total, p.P);
+    for (int t = threadIdx.x; t < RB; t += NT) {
+      T s = red[0][t];
+#pragma unroll
+      for (int w = 1; w < NW; ++w) s = add_(s, red[w][t]);
+      const long long i = p0 + t - p.lead;
+      if (i >= 0 && i < p.m) ws[slot * p.ws_ld + i] = s;
+    }
+    __syncthreads();
+    it = stop;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// GEMV-T / GEMV-C.  Item = (column block of NW*CW columns) x (row chunk of
+// H = 32*V*R rows), column-block-major.  Each lane keeps a partial dot
+// product per column in registers across the whole chunk range and reduces
+// across the warp once per column block (no shared memory, no barrier).
+// Rows outside the logical range are masked with selects, so padding or a
+// parent's neighbouring rows (possibly NaN) never enter a sum.
+// ---------------------------------------------------------------------------
+template <class T, int V, int NW, int CW, int R, bool CONJ>
+__global__ void __launch_bounds__(NW * 32) gemv_t_kernel(const GemvParams p) {
+  constexpr int H = 32 * V * R;
+  constexpr int CBW = NW * CW;
+  const T *__restrict__ A = static_cast<const T *>(p.A);
+  const T *__restrict__ x = static_cast<const T *>(p.x);
+  T *__restrict__ ws = static_cast<T *>(p.ws);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t pol = policy_evict_first();
+  long long it = sk_start(blockIdx.x, p.total, p.P);
+  const long long end = sk_start(blockIdx.x + 1, p.total, p.P);
+  const long long plimit = (long long)p.lead + p.m;
+
+  while (it < end) {
+    const long long cb = it / p.KS;
+    const long long cb_first = cb * p.KS;
+    const long long stop = min(end, cb_first + p.KS);
+    const int col0 = (int)cb * CBW + warp * CW;
+    const T *Aw = A + (long long)col0 * p.lda;
+    T t2[CW];
+#pragma unroll
+    for (int j = 0; j < CW; ++j) t2[j] = zero<T>();
+
+    for (long long q = it; q < stop; ++q) {
+      const long long p0 = (q - cb_first) * H;
+      T xr[R][V];
+      bool ok[R][V];
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          const long long i = p0 + r * 32 * V + lane * V + v - p.lead;
+          ok[r][v] = (i >= 0) && (i < p.m);
+          xr[r][v] = ok[r][v] ? __ldg(x + i) : zero<T>();
+        }
+      Pack<T, V> a[CW][R];
+#pragma unroll
+      for (int j = 0; j < CW; ++j) {
+        const bool cok = col0 + j < p.n;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const long long ps = p0 + r * 32 * V + lane * V;
+          a[j][r] = (cok && ps < plimit) ? ld_pack<T, V>(Aw + (long long)j * p.lda + ps, pol)
+                                         : zero_pack<T, V>();
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < CW; ++j)
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+          for (int v = 0; v < V; ++v) t2[j] = fmax_<CONJ>(sel(ok[r][v], a[j][r].v[v]), xr[r][v], t2[j]);
+    }
+
+    const long long slot = (long long)blockIdx.x - sk_owner(cb_first, p.total, p.P);
+#pragma unroll
+    for (int j = 0; j < CW; ++j) {
+      const T s = warp_sum(t2[j]);
+      if (lane == 0 && col0 + j < p.n) ws[slot * p.ws_ld + col0 + j] = s;
+    }
+    it = stop;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// SYMV / HEMV from one stored triangle.
+//
+// A tile is W = NW*CW consecutive columns [gcol0, gcol0+ncols) together with
+// every stored row of those columns: rows [gcol0, d) for 'l', [0, gcol0+ncols)
+// for 'u'.  The tile's rows are walked in H-row chunks; each stored element
+// a(i,c) is loaded once (256-bit) and used twice:
+//   t1[i] += a(i,c) x[c]            for i >= c ('l') / i <= c ('u')
+//   t2[c] += op(a(i,c)) x[i]        for i >  c ('l') / i <  c ('u')
+// with op = conj for HEMV, identity for SYMV (and complex symmetric), and
+// the Hermitian diagonal forced real (kernels.py:353-354).  Only chunks that
+// intersect the diagonal band evaluate the triangle masks; elements outside
+// the stored triangle are replaced by zero with a select, so the
+// unreferenced triangle may hold anything (NaN included).
+//
+// t1 for a chunk is complete after a shared-memory reduction over the warps
+// and is written to ws1[tile][row] (each (tile, row) exactly once).  t2
+// stays in registers for the tile and is written to ws2[slot][column] once
+// per (tile, CTA).  The epilogue sums ws1 over the tiles covering each row
+// and ws2 over the slots of the row's own tile, in fixed order.
+//
+// Tiles come from a host-built table so the same kernel serves the
+// single-GPU path, diagonal submatrices (offset API) and the local
+// block-column panels of the mgpu layout.
+// ---------------------------------------------------------------------------
+struct SymTile {
+  int gcol0;        // first global column of the tile
+  int lcol0;        // first local column (pointer offset in the panel)
+  int ncols;        // columns in the tile (<= W)
+  int row0, row1;   // stored logical rows [row0, row1)
+  int chunk0;       // first physical H-row chunk
+  long long prefix; // items before this tile
+};
+
+struct SymParams {
+  const void *A;
+  long long lda;
+  int d;
+  int lead;
+  const void *x;
+  void *ws1;
+  long long ws1_ld;
+  void *ws2;
+  long long ws2_ld;
+  const SymTile *tiles;
+  int ntiles;
+  long long total;
+  int P;
+};
+
+template <class T, int V, int NW, int CW, int R, bool LOWER, bool HERM>
+__global__ void __launch_bounds__(NW * 32, 1) symv_kernel(const SymParams p) {
+  constexpr int NT = NW * 32;
+  constexpr int H = 32 * V * R;
+  constexpr int W = NW * CW;
+  __shared__ T red[2][NW][H];
+  __shared__ T xs[W];
+  const T *__restrict__ A = static_cast<const T *>(p.A);
+  const T *__restrict__ x = static_cast<const T *>(p.x);
+  T *__restrict__ ws1 = static_cast<T *>(p.ws1);
+  T *__restrict__ ws2 = static_cast<T *>(p.ws2);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t pol = policy_evict_first();
+  long long it = sk_start(blockIdx.x, p.total, p.P);
+  const long long end = sk_start(blockIdx.x + 1, p.total, p.P);
+  if (it >= end) return;
+
+  // tile holding item `it`: the last tile whose prefix <= it
+  int k;
+  {
+    int lo = 0, hi = p.ntiles - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (p.tiles[mid].prefix <= it) lo = mid; else hi = mid - 1;
+    }
+    k = lo;
+  }
+  int buf = 0;
+  const int cl = warp * CW;
+
+  while (it < end) {
+    const SymTile tl = p.tiles[k];
+    const long long tnext = (k + 1 < p.ntiles) ? p.tiles[k + 1].prefix : p.total;
+    const long long stop = min(end, tnext);
+    __syncthreads();
+    for (int t = threadIdx.x; t < W; t += NT) xs[t] = t < tl.ncols ? __ldg(x + tl.gcol0 + t) : zero<T>();
+    __syncthreads();
+    const T *xc = xs + cl;  // x of this warp's columns (shared-memory broadcast)
+
+    T t2[CW];
+#pragma unroll
+    for (int j = 0; j < CW; ++j) t2[j] = zero<T>();
+    const T *Aw = A + (long long)(tl.lcol0 + cl) * p.lda;
+    const long long vlo = (long long)tl.row0 + p.lead;  // physical stored range
+    const long long vhi = (long long)tl.row1 + p.lead;
+
+    for (long long q = it; q < stop; ++q) {
+      const long long p0 = (long long)(tl.chunk0 + (q - tl.prefix)) * H;
+      T xr[R][V];
+      bool ok[R][V];
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          const long long ps = p0 + r * 32 * V + lane * V + v;
+          ok[r][v] = (ps >= vlo) && (ps < vhi);
+          xr[r][v] = ok[r][v] ? __ldg(x + (ps - p.lead)) : zero<T>();
+        }
+      Pack<T, V> a[CW][R];
+#pragma unroll
+      for (int j = 0; j < CW; ++j) {
+        const bool cok = cl + j < tl.ncols;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const long long vs = p0 + r * 32 * V + lane * V;
+          a[j][r] = (cok && vs < vhi && vs + V > vlo)
+                        ? ld_pack<T, V>(Aw + (long long)j * p.lda + vs, pol)
+                        : zero_pack<T, V>();
+        }
+      }
+      T acc[R][V];
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int v = 0; v < V; ++v) acc[r][v] = zero<T>();
+
+      const long long g0 = p0 - p.lead;  // logical row of the chunk's first physical row
+      const bool diag = (g0 < (long long)tl.gcol0 + tl.ncols) && (g0 + H > tl.gcol0);
+      if (!diag) {
+#pragma unroll
+        for (int j = 0; j < CW; ++j)
+#pragma unroll
+          for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+              const T e = sel(ok[r][v], a[j][r].v[v]);
+              acc[r][v] = fma_(e, xc[j], acc[r][v]);
+              t2[j] = fmax_<HERM>(e, xr[r][v], t2[j]);
+            }
+      } else {
+#pragma unroll
+        for (int j = 0; j < CW; ++j) {
+          const long long c = (long long)tl.gcol0 + cl + j;
+#pragma unroll
+          for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+              const long long i = g0 + r * 32 * V + lane * V + v;
+              const bool in1 = ok[r][v] && (LOWER ? i >= c : i <= c);
+              const bool in2 = ok[r][v] && (LOWER ? i > c : i < c);
+              T e1 = sel(in1, a[j][r].v[v]);
+              if (HERM && i == c) e1 = realify(e1);
+              acc[r][v] = fma_(e1, xc[j], acc[r][v]);
+              t2[j] = fmax_<HERM>(sel(in2, a[j][r].v[v]), xr[r][v], t2[j]);
+            }
+        }
+      }
+
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int v = 0; v < V; ++v) red[buf][warp][r * 32 * V + lane * V + v] = acc[r][v];
+      __syncthreads();
+      for (int t = threadIdx.x; t < H; t += NT) {
+        const long long ps = p0 + t;
+        if (ps >= vlo && ps < vhi) {
+          T s = red[buf][0][t];
+#pragma unroll
+          for (int w = 1; w < NW; ++w) s = add_(s, red[buf][w][t]);
+          ws1[(long long)k * p.ws1_ld + (ps - p.lead)] = s;
+        }
+      }
+      buf ^= 1;
+    }
+
+    const long long slot = (long long)blockIdx.x - sk_owner(tl.prefix, p.total, p.P);
+#pragma unroll
+    for (int j = 0; j < CW; ++j) {
+      const T s = warp_sum(t2[j]);
+      if (lane == 0 && cl + j < tl.ncols) ws2[slot * p.ws2_ld + tl.gcol0 + cl + j] = s;
+    }
+    it = stop;
+    ++k;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Epilogues: fixed-order sum of partial slots, then y = alpha*sum + beta*y.
+// beta_zero: y is written without being read (kernels.py:136-137).
+// ---------------------------------------------------------------------------
+template <class T>
+__device__ __forceinline__ void store_axpby(T *y, long long i, T alpha, T s, T beta, int beta_zero) {
+  T r = mul_(alpha, s);
+  if (!beta_zero) r = fma_(beta, y[i], r);
+  y[i] = r;
+}
+
+template <class T>
+__global__ void gemv_n_epilogue(T *y, const T *__restrict__ ws, long long ws_ld, int m, int lead,
+                                int RB, int KS, long long total, int P, T alpha, T beta,
+                                int beta_zero) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  const long long rb = (i + lead) / RB;
+  const int first = sk_owner(rb * KS, total, P);
+  const int last = sk_owner(rb * KS + KS - 1, total, P);
+  T s = ws[i];
+  for (int sl = 1; sl <= last - first; ++sl) s = add_(s, ws[sl * ws_ld + i]);
+  store_axpby(y, i, alpha, s, beta, beta_zero);
+}
+
+// y indexed by global column c in [0, nglob); columns not owned by this GPU
+// (mgpu partial mode) are written as zero.
+template <class T>
+__global__ void gemv_t_epilogue(T *y, const T *__restrict__ ws, long long ws_ld, long long nglob,
+                                int CBW, int KS, long long total, int P, ColMap cm, T alpha, T beta,
+                                int beta_zero) {
+  const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nglob) return;
+  const long long l = unmap_col(cm, c);
+  if (l < 0) { y[c] = zero<T>(); return; }
+  const long long cb = l / CBW;
+  const int first = sk_owner(cb * KS, total, P);
+  const int last = sk_owner(cb * KS + KS - 1, total, P);
+  T s = ws[l];
+  for (int sl = 1; sl <= last - first; ++sl) s = add_(s, ws[sl * ws_ld + l]);
+  store_axpby(y, c, alpha, s, beta, beta_zero);
+}
+
+template <class T, bool LOWER>
+__global__ void symv_epilogue(T *y, const SymParams p, T alpha, T beta, int beta_zero) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= p.d) return;
+  const T *__restrict__ ws1 = static_cast<const T *>(p.ws1);
+  const T *__restrict__ ws2 = static_cast<const T *>(p.ws2);
+  // nle = number of tiles with gcol0 <= i (tiles sorted by gcol0)
+  int lo = 0, hi = p.ntiles;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (p.tiles[mid].gcol0 <= i) lo = mid + 1; else hi = mid;
+  }
+  const int nle = lo;
+  T s = zero<T>();
+  // t1: tiles whose stored rows include i
+  if (LOWER) {
+    for (int k = 0; k < nle; ++k) s = add_(s, ws1[(long long)k * p.ws1_ld + i]);
+  } else {
+    int k0 = nle;
+    while (k0 > 0 && p.tiles[k0 - 1].gcol0 + p.tiles[k0 - 1].ncols > i) --k0;
+    for (int k = k0; k < p.ntiles; ++k) s = add_(s, ws1[(long long)k * p.ws1_ld + i]);
+  }
+  // t2: the tile owning column i (if any on this GPU)
+  if (nle > 0) {
+    const SymTile tl = p.tiles[nle - 1];
+    if (i < (long long)tl.gcol0 + tl.ncols) {
+      const long long tnext = (nle < p.ntiles) ? p.tiles[nle].prefix : p.total;
+      if (tnext > tl.prefix) {
+        const int first = sk_owner(tl.prefix, p.total, p.P);
+        const int last = sk_owner(tnext - 1, p.total, p.P);
+        for (int sl = 0; sl <= last - first; ++sl) s = add_(s, ws2[sl * p.ws2_ld + i]);
+      }
+    }
+  }
+  store_axpby(y, i, alpha, s, beta, beta_zero);
+}
+
+// y <- beta * y (beta == 0: zero fill); run_scal semantics (kernels.py:127-146)
+template <class T>
+__global__ void scal_kernel(T *y, long long n, T beta, int beta_zero) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  y[i] = beta_zero ? zero<T>() : mul_(beta, y[i]);
+}
+
+// mgpu root combine: y = beta*y + sum_g part[g] in device order
+// (multidevice.py:161,176,276 then 282-283).  part[g] may be a peer
+// pointer on another GPU (NVLink load) or a local copy.
+constexpr int kMaxGpus = 16;
+template <class T> struct PartList { const T *p[kMaxGpus]; };
+template <class T>
+__global__ void mgpu_combine_kernel(T *y, PartList<T> parts, int G, long long n, T beta, int beta_zero) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  T s = parts.p[0][i];
+  for (int g = 1; g < G; ++g) s = add_(s, parts.p[g][i]);
+  y[i] = beta_zero ? s : fma_(beta, y[i], s);
+}
+
+}  // namespace kb

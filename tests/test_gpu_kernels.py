@@ -1,0 +1,370 @@
+"""GPU behaviour and parity tests modelled on the reference's own tests
+(test_kernels.py, test_offset.py, test_acceptance.py c1/c5/c8), run
+through the drop-in API and the C ABI against the CPU oracle."""
+
+import ctypes
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1410_1726_b200 as kb
+from paper_1410_1726_b200 import _lib
+from oracle import naive, streamed
+
+pytestmark = pytest.mark.gpu
+
+DT = {"s": torch.float32, "d": torch.float64, "c": torch.complex64, "z": torch.complex128}
+
+
+def dev_matrix(rng, m, n, tag, ld=None, fill=naive.fill):
+    """(MatrixView on the GPU, host 2-D copy) with leading dimension ld."""
+    ld = ld or m
+    host = np.zeros(ld * n, dtype=naive.DTYPES[tag])
+    win = naive.window(host, ld, m, n)
+    win[:, :] = fill(rng, (m, n), tag)
+    v = kb.MatrixView(torch.from_numpy(host).cuda(), m, n, ld, kb.precision(tag))
+    return v, np.array(win)
+
+
+def dvec(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def check(got, want, tag, alpha, dense_abs, x, beta, y, factor=1.0):
+    got = got.cpu().numpy() if isinstance(got, torch.Tensor) else got
+    bound = factor * naive.run_bound(tag, alpha, dense_abs, x, beta, y)
+    err = naive.max_abs_error(got, want)
+    assert err <= bound, (err, bound)
+
+
+class TestGemv:
+    @pytest.mark.parametrize("tag", "sdcz")
+    @pytest.mark.parametrize("trans", "ntc")
+    def test_matches_oracle_shapes(self, tag, trans):
+        """test_kernels.py:42-55 shapes plus wave-edge and ragged sizes."""
+        rng = np.random.default_rng(11)
+        for m, n in [(1, 1), (7, 5), (32, 32), (65, 33), (100, 300), (1000, 37), (37, 1000), (2049, 1537)]:
+            v, a = dev_matrix(rng, m, n, tag, ld=-(-m // 32) * 32)
+            xl, yl = (n, m) if trans == "n" else (m, n)
+            x, y = naive.fill(rng, xl, tag), naive.fill(rng, yl, tag)
+            got = kb.gemv(trans, 0.7, v, dvec(x), -0.3, dvec(y)).y_out
+            want = naive.naive_gemv(trans, 0.7, a, x, -0.3, y)
+            dense = np.abs(a) if trans == "n" else np.abs(a).T
+            check(got, want, tag, 0.7, dense, x, -0.3, y)
+
+    @pytest.mark.parametrize("tag", "sdcz")
+    def test_every_lead_and_unaligned_ld(self, tag):
+        """Submatrix starts at every offset inside the 32-byte granule
+        (realigned 256-bit path) and odd ld (one-element path)."""
+        rng = np.random.default_rng(12)
+        for ld in (515, 520):
+            v, a = dev_matrix(rng, 500, 300, tag, ld=ld)
+            for ro in range(0, 9):
+                for trans in "nt":
+                    sub = v.submatrix(ro, 3, 480 - ro, 290)
+                    sa = a[ro:480, 3:293]
+                    xl, yl = (290, 480 - ro) if trans == "n" else (480 - ro, 290)
+                    x, y = naive.fill(rng, xl, tag), naive.fill(rng, yl, tag)
+                    got = kb.gemv(trans, 1.3, sub, dvec(x), 0.5, dvec(y)).y_out
+                    want = naive.naive_gemv(trans, 1.3, sa, x, 0.5, y)
+                    dense = np.abs(sa) if trans == "n" else np.abs(sa).T
+                    check(got, want, tag, 1.3, dense, x, 0.5, y)
+
+    def test_deterministic(self):
+        """Bit-identical repeated calls (test_kernels.py:57-65): no atomics."""
+        rng = np.random.default_rng(3)
+        for tag in "sz":
+            v, _ = dev_matrix(rng, 3000, 2000, tag)
+            for trans in "nt":
+                xl, yl = (2000, 3000) if trans == "n" else (3000, 2000)
+                x, y = dvec(naive.fill(rng, xl, tag)), dvec(naive.fill(rng, yl, tag))
+                r1 = kb.gemv(trans, 1.3, v, x, 0.4, y).y_out
+                r2 = kb.gemv(trans, 1.3, v, x, 0.4, y).y_out
+                assert torch.equal(r1, r2)
+
+    def test_beta_zero_kills_nan(self):
+        rng = np.random.default_rng(6)
+        v, a = dev_matrix(rng, 64, 64, "d")
+        x = naive.fill(rng, 64, "d")
+        for trans in "nt":
+            got = kb.gemv(trans, 1.0, v, dvec(x), 0.0, torch.full((64,), float("nan"), device="cuda")).y_out
+            assert torch.isfinite(got).all()
+            check(got, naive.naive_gemv(trans, 1.0, a, x, 0.0, np.zeros(64)), "d", 1.0, np.abs(a), x, 0.0,
+                  np.zeros(64))
+
+    def test_quick_return_and_alpha_zero(self):
+        rng = np.random.default_rng(7)
+        v, a = dev_matrix(rng, 32, 32, "d")
+        x, y = naive.fill(rng, 32, "d"), naive.fill(rng, 32, "d")
+        n0 = _lib.launch_count()
+        rep = kb.gemv("n", 0.0, v, dvec(x), 1.0, dvec(y))
+        assert np.array_equal(rep.y_out.cpu().numpy(), y)
+        assert rep.transactions == 0 and rep.tb_count == 0 and rep.flops == 0
+        assert _lib.launch_count() == n0
+        # alpha == 0: beta * y only, A never read (poison it)
+        v.data.fill_(float("nan"))
+        rep = kb.gemv("n", 0.0, v, dvec(x), 0.5, dvec(y))
+        assert np.allclose(rep.y_out.cpu().numpy(), 0.5 * y)
+        assert rep.matrix_transactions == 0 and rep.scal_invocations == 1
+
+    def test_conjugate_on_real_is_transpose_bit_exact(self):
+        rng = np.random.default_rng(13)
+        v, _ = dev_matrix(rng, 40, 30, "d")
+        x, y = dvec(naive.fill(rng, 40, "d")), dvec(naive.fill(rng, 30, "d"))
+        assert torch.equal(kb.gemv("c", 1.0, v, x, 0.0, y).y_out, kb.gemv("t", 1.0, v, x, 0.0, y).y_out)
+
+    def test_inputs_not_mutated_and_types(self):
+        rng = np.random.default_rng(14)
+        v, a = dev_matrix(rng, 50, 40, "z")
+        x, y = naive.fill(rng, 40, "z"), naive.fill(rng, 50, "z")
+        xt, yt = dvec(x), dvec(y)
+        before = v.data.clone()
+        rep = kb.gemv("n", 1 + 2j, v, xt, 0.5 - 1j, yt)
+        assert torch.equal(v.data, before) and np.array_equal(yt.cpu().numpy(), y)
+        assert isinstance(rep.y_out, torch.Tensor) and rep.y_out.dtype == torch.complex128
+        rep2 = kb.gemv("n", 1 + 2j, v, x, 0.5 - 1j, y)
+        assert isinstance(rep2.y_out, np.ndarray)
+        assert np.array_equal(rep2.y_out, rep.y_out.cpu().numpy())
+
+    def test_inplace(self):
+        rng = np.random.default_rng(15)
+        v, a = dev_matrix(rng, 300, 200, "d")
+        x, y = naive.fill(rng, 200, "d"), naive.fill(rng, 300, "d")
+        yt = dvec(y)
+        rep = kb.gemv("n", 2.0, v, dvec(x), 1.5, yt, inplace=True)
+        assert rep.y_out.data_ptr() == yt.data_ptr()
+        check(yt, naive.naive_gemv("n", 2.0, a, x, 1.5, y), "d", 2.0, np.abs(a), x, 1.5, y)
+
+    def test_errors(self):
+        rng = np.random.default_rng(16)
+        v, _ = dev_matrix(rng, 8, 8, "d")
+        with pytest.raises(ValueError):
+            kb.gemv("q", 1.0, v, np.zeros(8), 0.0, np.zeros(8))
+        with pytest.raises(ValueError):
+            kb.gemv("n", 1.0, v, np.zeros(7), 0.0, np.zeros(8))
+
+
+class TestSymv:
+    @pytest.mark.parametrize("tag", "sdcz")
+    @pytest.mark.parametrize("uplo", "lu")
+    def test_matches_oracle_sizes(self, tag, uplo):
+        """test_kernels.py:166-179 sizes plus tile-edge sizes."""
+        rng = np.random.default_rng(21)
+        for d in (1, 5, 32, 33, 100, 127, 128, 129, 257, 1000, 2047):
+            for herm in ([True, False] if tag in "cz" else [False]):
+                v, a = dev_matrix(rng, d, d, tag, ld=-(-d // 32) * 32)
+                x, y = naive.fill(rng, d, tag), naive.fill(rng, d, tag)
+                hv = kb.HermitianView(v, uplo)
+                got = kb.symv_hemv(uplo, 1.1, hv, dvec(x), -0.2, dvec(y), hermitian=herm).y_out
+                want = naive.naive_symv_hemv(1.1, a, uplo, x, -0.2, y, hermitian=herm)
+                dense = np.abs(naive.dense_from_triangle(a, uplo, herm))
+                check(got, want, tag, 1.1, dense, x, -0.2, y)
+
+    @pytest.mark.parametrize("tag", "sdcz")
+    @pytest.mark.parametrize("uplo", "lu")
+    def test_unreferenced_triangle_poisoned(self, tag, uplo):
+        """The other triangle holds NaN: result must be finite and correct
+        (the executable form of the reference's triangle guard,
+        core.py:155-188, test_kernels.py:213-221)."""
+        rng = np.random.default_rng(25)
+        for d, ro in ((300, 0), (517, 3), (1024, 1)):
+            ld = d + 8
+            host = np.full(ld * d, np.nan, dtype=naive.DTYPES[tag])
+            win = naive.window(host, ld, d, d)
+            vals = naive.fill(rng, (d - ro, d - ro), tag)
+            tri = np.tril(vals) if uplo == "l" else np.triu(vals)
+            mask = np.tril(np.ones((d - ro,) * 2, bool)) if uplo == "l" else np.triu(np.ones((d - ro,) * 2, bool))
+            sub = win[ro:, ro:]
+            sub[mask] = tri[mask]
+            v = kb.MatrixView(torch.from_numpy(host).cuda(), d, d, ld, kb.precision(tag)).submatrix(
+                ro, ro, d - ro, d - ro)
+            x, y = naive.fill(rng, d - ro, tag), naive.fill(rng, d - ro, tag)
+            got = kb.symv_hemv(uplo, 0.9, kb.HermitianView(v, uplo), dvec(x), 0.0, dvec(y)).y_out
+            assert torch.isfinite(got).all()
+            herm = tag in "cz"
+            want = naive.naive_symv_hemv(0.9, tri, uplo, x, 0.0, y, hermitian=herm)
+            check(got, want, tag, 0.9, np.abs(naive.dense_from_triangle(tri, uplo, herm)), x, 0.0, y)
+
+    def test_hemv_ignores_imaginary_diagonal(self):
+        rng = np.random.default_rng(26)
+        d = 200
+        v, a = dev_matrix(rng, d, d, "c")
+        idx = np.arange(d)
+        a[idx, idx] = a[idx, idx].real + 5j
+        v.array().copy_(torch.from_numpy(a).cuda())
+        x, y = naive.fill(rng, d, "c"), naive.fill(rng, d, "c")
+        got = kb.hemv("l", 1.0, kb.HermitianView(v, "l"), dvec(x), 0.0, dvec(y)).y_out
+        want = naive.naive_symv_hemv(1.0, a, "l", x, 0.0, y, hermitian=True)
+        check(got, want, "c", 1.0, np.abs(naive.dense_from_triangle(a, "l", True)), x, 0.0, y)
+
+    def test_deterministic_and_no_scal(self):
+        rng = np.random.default_rng(22)
+        v, _ = dev_matrix(rng, 3000, 3000, "d")
+        hv = kb.HermitianView(v, "l")
+        x, y = dvec(naive.fill(rng, 3000, "d")), dvec(naive.fill(rng, 3000, "d"))
+        r1 = kb.symv_hemv("l", 1.0, hv, x, 3.0, y)
+        r2 = kb.symv_hemv("l", 1.0, hv, x, 3.0, y)
+        assert torch.equal(r1.y_out, r2.y_out)
+        assert r1.scal_invocations == 0 and r1.atomic_adds == 0
+        assert r1.flops == 2 * 3000 * 3000 + 2 * 3000
+
+    def test_beta_zero_kills_nan(self):
+        rng = np.random.default_rng(23)
+        v, _ = dev_matrix(rng, 64, 64, "d")
+        got = kb.symv_hemv("u", 1.0, kb.HermitianView(v, "u"), dvec(naive.fill(rng, 64, "d")), 0.0,
+                           torch.full((64,), float("nan"), device="cuda")).y_out
+        assert torch.isfinite(got).all()
+
+    def test_rejections(self):
+        rng = np.random.default_rng(27)
+        vc, _ = dev_matrix(rng, 32, 32, "c")
+        vd, _ = dev_matrix(rng, 32, 32, "d")
+        x = np.zeros(32)
+        with pytest.raises(ValueError):
+            kb.symv("l", 1.0, kb.HermitianView(vc, "l"), x, 0.0, x)
+        with pytest.raises(ValueError):
+            kb.hemv("l", 1.0, kb.HermitianView(vd, "l"), x, 0.0, x)
+        with pytest.raises(ValueError):
+            kb.symv_hemv("u", 1.0, kb.HermitianView(vd, "l"), x, 0.0, x)
+        with pytest.raises(ValueError):
+            kb.symv_hemv("l", 1.0, kb.HermitianView(vd, "l"), x, 0.0, x, hermitian=True)
+
+
+class TestOffset:
+    @pytest.mark.parametrize("tag", "sdcz")
+    def test_paper_offsets_match_standard_bit_exact(self, tag):
+        """The offset API on (i, j) of a parent == the standard API on the
+        submatrix view (same realigned plan: bit-identical), and both match
+        the oracle.  Offsets from BASELINE config 4 plus an aligned control."""
+        rng = np.random.default_rng(31)
+        parent_n = 2048
+        v, a = dev_matrix(rng, parent_n, parent_n, tag)
+        for (i, j) in ((1, 1), (7, 3), (13, 13), (16, 16)):
+            sm, sn = parent_n - i, parent_n - j
+            for trans in "nt":
+                xl, yl = (sn, sm) if trans == "n" else (sm, sn)
+                x, y = dvec(naive.fill(rng, xl, tag)), dvec(naive.fill(rng, yl, tag))
+                off = kb.gemv_offset(trans, 1.0, kb.OffsetRequest(v, i, j, sm, sn), x, 0.5, y).y_out
+                std = kb.gemv(trans, 1.0, v.submatrix(i, j, sm, sn), x, 0.5, y).y_out
+                assert torch.equal(off, std)
+                sa = a[i:, j:]
+                want = naive.naive_gemv(trans, 1.0, sa, x.cpu().numpy(), 0.5, y.cpu().numpy())
+                dense = np.abs(sa) if trans == "n" else np.abs(sa).T
+                check(off, want, tag, 1.0, dense, x.cpu().numpy(), 0.5, y.cpu().numpy())
+            for uplo in "lu":
+                d = parent_n - i
+                x, y = dvec(naive.fill(rng, d, tag)), dvec(naive.fill(rng, d, tag))
+                hv = kb.HermitianView(v, uplo)
+                off = kb.symv_hemv_offset(uplo, 1.0, hv, i, d, x, 0.5, y).y_out
+                std = kb.symv_hemv(uplo, 1.0, kb.HermitianView(v.submatrix(i, i, d, d), uplo), x, 0.5, y).y_out
+                assert torch.equal(off, std)
+                sa = a[i:, i:]
+                herm = tag in "cz"
+                want = naive.naive_symv_hemv(1.0, sa, uplo, x.cpu().numpy(), 0.5, y.cpu().numpy())
+                check(off, want, tag, 1.0, np.abs(naive.dense_from_triangle(sa, uplo, herm)), x.cpu().numpy(),
+                      0.5, y.cpu().numpy())
+
+    def test_unaligned_parent_ld_warns(self):
+        v = kb.alloc_matrix(100, 100, kb.precision("d"), ld=101)
+        req = kb.OffsetRequest(v, 3, 0, 32, 32)
+        with pytest.warns(UserWarning, match="not segment-aligned"):
+            kb.gemv_offset("n", 1.0, req, np.zeros(32), 0.0, np.zeros(32))
+
+    def test_offset_counts_true_submatrix(self):
+        rng = np.random.default_rng(47)
+        v, _ = dev_matrix(rng, 256, 256, "d")
+        rep = kb.symv_hemv_offset("l", 1.0, kb.HermitianView(v, "l"), 13, 100, np.zeros(100), 1.0,
+                                  np.zeros(100))
+        assert rep.flops == 2 * 100 * 100 + 2 * 100
+        rep = kb.gemv_offset("n", 1.0, kb.OffsetRequest(v, 5, 9, 40, 40), np.zeros(40), 0.0, np.zeros(40))
+        assert rep.scal_invocations == 1
+
+
+class TestCAbi:
+    """Direct C-ABI calls (the boundary a C/ctypes binding would use)."""
+
+    @pytest.mark.parametrize("tag", "sdcz")
+    def test_sync_and_async_entry_points(self, tag):
+        lib = _lib.load()
+        rng = np.random.default_rng(41)
+        m, n = 777, 555
+        v, a = dev_matrix(rng, m, n, tag, ld=800)
+        x, y = naive.fill(rng, n, tag), naive.fill(rng, m, tag)
+        xt = dvec(x)
+        for suffix in ("", "_async"):
+            yt = dvec(y)
+            f = getattr(lib, f"kblas_{tag}gemv{suffix}")
+            args = [b"N", m, n, _lib.scalar(tag, 0.25), v.data.data_ptr(), 800, xt.data_ptr(), 1,
+                    _lib.scalar(tag, 2.0), yt.data_ptr(), 1]
+            if suffix:
+                args.append(torch.cuda.current_stream().cuda_stream)
+            assert f(*args) == 0
+            torch.cuda.synchronize()
+            check(yt, naive.naive_gemv("n", 0.25, a, x, 2.0, y), tag, 0.25, np.abs(a), x, 2.0, y)
+
+    def test_symv_mgpu_c_entry_single_device(self):
+        """kblas_dsymv_mgpu with every logical GPU mapped to device 0."""
+        lib = _lib.load()
+        rng = np.random.default_rng(42)
+        d, nb, G = 1000, 64, 3
+        v, a = dev_matrix(rng, d, d, "d")
+        dist = kb.distribute(v, nb, G)
+        x, y = naive.fill(rng, d, "d"), naive.fill(rng, d, "d")
+        xs = [dvec(x) for _ in range(G)]
+        ys = [dvec(y)] + [torch.empty(d, dtype=torch.float64, device="cuda") for _ in range(G - 1)]
+        arr = ctypes.c_void_p * G
+        pa = arr(*[dist.local_views[g].data.data_ptr() for g in range(G)])
+        px = arr(*[t.data_ptr() for t in xs])
+        py = arr(*[t.data_ptr() for t in ys])
+        ids = (ctypes.c_int * G)(*([0] * G))
+        ld = dist.local_views[0].ld
+        rc = lib.kblas_dsymv_mgpu(b"L", d, _lib.scalar("d", 0.5), pa, ld, px, 1, _lib.scalar("d", -1.0), py, 1,
+                                  G, nb, ids)
+        assert rc == 0
+        want = naive.naive_symv_hemv(0.5, a, "l", x, -1.0, y)
+        check(ys[0], want, "d", 0.5, np.abs(naive.dense_from_triangle(a, "l", False)), x, -1.0, y)
+
+
+class TestLarge:
+    """Sizes the numpy oracle cannot hold comfortably: the streamed C oracle
+    (all host threads) and size-independent properties."""
+
+    def test_dsymv_16384_vs_streamed_oracle(self):
+        d = 16384
+        g = torch.Generator(device="cuda").manual_seed(5)
+        A = torch.rand(d, d, device="cuda", dtype=torch.float64, generator=g) * 2 - 1
+        v = kb.view_of(A.T)  # column-major view of a row-major tensor
+        x = torch.rand(d, device="cuda", dtype=torch.float64, generator=g) * 2 - 1
+        y = torch.rand(d, device="cuda", dtype=torch.float64, generator=g) * 2 - 1
+        for uplo in "lu":
+            got = kb.symv_hemv(uplo, 1.0, kb.HermitianView(v, uplo), x, 0.5, y).y_out.cpu().numpy()
+            a_host = v.array().cpu().numpy()
+            xh, yh = x.cpu().numpy(), y.cpu().numpy()
+            want = streamed.symv(uplo, 1.0, a_host, xh, 0.5, yh)
+            norm = streamed.symv_norm_inf(uplo, a_host)
+            bound = 50 * np.finfo(np.float64).eps * (norm * np.max(np.abs(xh)) + 0.5 * np.max(np.abs(yh)))
+            assert naive.max_abs_error(got, want) <= bound
+
+    def test_symv_equals_gemv_on_mirrored_matrix_32768(self):
+        """DSYMV L at BASELINE config 2 size vs DGEMV on the explicitly mirrored
+        matrix (two independent kernels), plus linearity in x."""
+        d = 32768
+        g = torch.Generator(device="cuda").manual_seed(6)
+        A = torch.rand(d, d, device="cuda", dtype=torch.float64, generator=g) * 2 - 1
+        L = torch.tril(A)
+        del A
+        full = L + torch.tril(L, -1).T  # symmetric, row-major == column-major
+        x1 = torch.rand(d, device="cuda", dtype=torch.float64, generator=g) * 2 - 1
+        x2 = torch.rand(d, device="cuda", dtype=torch.float64, generator=g) * 2 - 1
+        y0 = torch.zeros(d, device="cuda", dtype=torch.float64)
+        lv = kb.view_of(L.T.contiguous().T)
+        del L
+        hv = kb.HermitianView(lv, "l")
+        s1 = kb.symv_hemv("l", 1.0, hv, x1, 0.0, y0).y_out
+        g1 = kb.gemv("n", 1.0, kb.view_of(full.T), x1, 0.0, y0).y_out
+        bound = 50 * np.finfo(np.float64).eps * d * 1.0
+        assert (s1 - g1).abs().max().item() <= bound
+        s2 = kb.symv_hemv("l", 1.0, hv, x2, 0.0, y0).y_out
+        s12 = kb.symv_hemv("l", 1.0, hv, x1 + x2, 0.0, y0).y_out
+        assert (s12 - (s1 + s2)).abs().max().item() <= 2 * bound

@@ -1,0 +1,128 @@
+"""mgpu API on the GPU (test_multidevice.py model).  Logical GPUs map onto
+the physical devices present (all onto cuda:0 on a 1-GPU box)."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1410_1726_b200 as kb
+from oracle import blocked, naive
+
+pytestmark = pytest.mark.gpu
+
+
+def dev_matrix(rng, m, n, tag):
+    ld = -(-m // 32) * 32
+    host = np.zeros(ld * n, dtype=naive.DTYPES[tag])
+    win = naive.window(host, ld, m, n)
+    win[:, :] = naive.fill(rng, (m, n), tag)
+    return kb.MatrixView(torch.from_numpy(host).cuda(), m, n, ld, kb.precision(tag)), np.array(win)
+
+
+@pytest.mark.parametrize("devices", range(1, 9))
+def test_distribute_gather_round_trip(devices):
+    rng = np.random.default_rng(60 + devices)
+    m, n = int(rng.integers(30, 200)), int(rng.integers(30, 200))
+    v, a = dev_matrix(rng, m, n, "z")
+    dist = kb.distribute(v, 32, devices)
+    back = kb.gather(dist)
+    assert torch.equal(back.array(), v.array())
+    for g in range(devices):
+        if dist.local_views[g] is None:
+            assert not kb.owned_block_cols(n, 32, devices, g)
+
+
+@pytest.mark.parametrize("devices", [1, 2, 3, 4, 8])
+@pytest.mark.parametrize("trans", "ntc")
+def test_gemv_mgpu_matches_single(devices, trans):
+    rng = np.random.default_rng(70)
+    tag = "z" if trans == "c" else "d"
+    for d in (64, 100, 256, 1000):
+        v, a = dev_matrix(rng, d, d, tag)
+        x, y = naive.fill(rng, d, tag), naive.fill(rng, d, tag)
+        merged, per = kb.gemv_mgpu(trans, 1.2, kb.distribute(v, 32, devices), x, -0.5, y)
+        single = kb.gemv(trans, 1.2, v, x, -0.5, y).y_out
+        bound = naive.tolerance_bound(np.abs(a), x, tag) + 50 * naive.EPS[tag] * (np.max(np.abs(y)) + 1)
+        assert naive.max_abs_error(merged.y_out, single) <= bound
+        assert len(per) == devices
+        assert merged.flops == sum(r.flops for r in per)
+
+
+@pytest.mark.parametrize("devices", [1, 2, 4, 8])
+@pytest.mark.parametrize("tag,uplo", [("d", "l"), ("d", "u"), ("c", "l"), ("z", "u"), ("s", "u")])
+def test_symv_hemv_mgpu_matches_oracle(devices, tag, uplo):
+    rng = np.random.default_rng(80)
+    for d, nb in ((64, 32), (100, 32), (512, 64), (1500, 128)):
+        v, a = dev_matrix(rng, d, d, tag)
+        x, y = naive.fill(rng, d, tag), naive.fill(rng, d, tag)
+        merged, per = kb.symv_hemv_mgpu(uplo, 0.9, kb.distribute(v, nb, devices), x, 0.7, y, kb.KernelConfig(nb, 2))
+        want = naive.naive_symv_hemv(0.9, a, uplo, x, 0.7, y)
+        sim = blocked.symv_hemv_mgpu(uplo, 0.9, a, x, 0.7, y, devices, nb)
+        dense = np.abs(naive.dense_from_triangle(a, uplo, tag in "cz"))
+        bound = naive.run_bound(tag, 0.9, dense, x, 0.7, y)
+        assert naive.max_abs_error(merged.y_out, want) <= bound
+        assert naive.max_abs_error(merged.y_out, sim) <= 2 * bound
+        assert len(per) == devices
+
+
+def test_transposed_segments_bit_identical_g1_g4():
+    """test_multidevice.py:114-124: disjoint T segments, G=1 == G=4 bit-for-bit."""
+    rng = np.random.default_rng(73)
+    v, _ = dev_matrix(rng, 96, 96, "d")
+    x = naive.fill(rng, 96, "d")
+    y = np.zeros(96)
+    one, _ = kb.gemv_mgpu("t", 1.0, kb.distribute(v, 32, 1), x, 0.0, y)
+    four, _ = kb.gemv_mgpu("t", 1.0, kb.distribute(v, 32, 4), x, 0.0, y)
+    assert np.array_equal(one.y_out, four.y_out)
+
+
+def test_deterministic_reduction():
+    rng = np.random.default_rng(72)
+    v, _ = dev_matrix(rng, 1500, 1500, "s")
+    x, y = naive.fill(rng, 1500, "s"), naive.fill(rng, 1500, "s")
+    dist = kb.distribute(v, 32, 3)
+    r1, _ = kb.gemv_mgpu("n", 1.0, dist, x, 0.3, y)
+    r2, _ = kb.gemv_mgpu("n", 1.0, dist, x, 0.3, y)
+    assert np.array_equal(r1.y_out, r2.y_out)
+
+
+def test_symv_mgpu_validation():
+    rng = np.random.default_rng(81)
+    v, _ = dev_matrix(rng, 128, 128, "d")
+    with pytest.raises(ValueError, match="block width"):
+        kb.symv_hemv_mgpu("l", 1.0, kb.distribute(v, 64, 2), np.zeros(128), 0.0, np.zeros(128), kb.KernelConfig(32, 2))
+    r, _ = dev_matrix(rng, 96, 64, "d")
+    with pytest.raises(ValueError, match="square"):
+        kb.symv_hemv_mgpu("l", 1.0, kb.distribute(r, 32, 2), np.zeros(64), 0.0, np.zeros(64), kb.KernelConfig(32, 2))
+
+
+class TestCommandQueue:
+    def test_results_unavailable_before_sync(self):
+        rng = np.random.default_rng(90)
+        v, a = dev_matrix(rng, 64, 64, "d")
+        x, y = naive.fill(rng, 64, "d"), naive.fill(rng, 64, "d")
+        q = kb.CommandQueue("stream-0")
+        h = kb.gemv_mgpu_async("n", 1.0, kb.distribute(v, 32, 2), x, 0.0, y, kb.KernelConfig(32, 2), q)
+        with pytest.raises(RuntimeError):
+            h.result()
+        q.synchronize()
+        merged, per = h.result()
+        assert np.allclose(merged.y_out, naive.naive_gemv("n", 1.0, a, x, 0.0, y))
+
+    def test_in_order_execution(self):
+        order = []
+        q = kb.CommandQueue()
+        q.submit(lambda: order.append("first"))
+        q.submit(lambda: order.append("second"))
+        q.synchronize()
+        assert order == ["first", "second"]
+
+    def test_symv_async(self):
+        rng = np.random.default_rng(91)
+        v, a = dev_matrix(rng, 96, 96, "d")
+        x, y = naive.fill(rng, 96, "d"), naive.fill(rng, 96, "d")
+        q = kb.CommandQueue()
+        h = kb.symv_hemv_mgpu_async("l", 1.0, kb.distribute(v, 32, 3), x, 1.0, y, kb.KernelConfig(32, 2), q)
+        q.synchronize()
+        merged, _ = h.result()
+        assert np.allclose(merged.y_out, naive.naive_symv_hemv(1.0, a, "l", x, 1.0, y))

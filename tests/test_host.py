@@ -1,0 +1,210 @@
+"""Host-side logic of the drop-in (no GPU needed): argument types and
+validation mirrored from the reference, layout/partition arithmetic, the
+algorithmic byte/flop counts, and the C-ABI library surface."""
+
+import ctypes
+
+import numpy as np
+import pytest
+
+from paper_1410_1726_b200 import _lib, roofline
+from paper_1410_1726_b200.core import HermitianView, MatrixView, precision, view_of
+from paper_1410_1726_b200.multidevice import (
+    local_col_count,
+    owned_block_cols,
+    required_local_elements,
+)
+from paper_1410_1726_b200.offset import OffsetRequest, effective_dims, realigned_frame
+from paper_1410_1726_b200.partition import KernelConfig, sk_owner, sk_start, tb_share
+
+
+class TestPrecision:
+    def test_tags(self):
+        assert precision("D").element_bytes == 8
+        assert precision("z").flops_per_mul == 6 and precision("z").flops_per_add == 2
+        with pytest.raises(ValueError):
+            precision("q")
+
+    def test_eps_of_real_component(self):
+        assert precision("c").eps == np.finfo(np.float32).eps
+        assert precision("z").eps == np.finfo(np.float64).eps
+
+
+class TestViews:
+    def test_matrix_view_validation(self):
+        prec = precision("d")
+        buf = np.zeros(100, dtype=np.float64)
+        with pytest.raises(ValueError):
+            MatrixView(buf, 0, 3, 10, prec)
+        with pytest.raises(ValueError):
+            MatrixView(buf, 10, 3, 9, prec)  # ld too small
+        with pytest.raises(ValueError):
+            MatrixView(buf, 10, 11, 10, prec)  # buffer too small
+        with pytest.raises(ValueError):
+            MatrixView(buf.astype(np.float32), 10, 3, 10, prec)  # dtype
+
+    def test_linear_index_and_submatrix(self):
+        prec = precision("s")
+        buf = np.arange(64, dtype=np.float32)
+        v = MatrixView(buf, 8, 8, 8, prec)
+        sub = v.submatrix(2, 3, 4, 5)
+        assert sub.linear_index(0, 0) == 3 * 8 + 2
+        assert sub.array()[1, 2] == buf[(3 + 2) * 8 + 2 + 1]
+        assert v.decode_linear(sub.linear_index(1, 2)) == (3, 5)
+        with pytest.raises(ValueError):
+            v.submatrix(5, 0, 4, 1)
+
+    def test_view_of_fortran_array(self):
+        a = np.asfortranarray(np.arange(12, dtype=np.float64).reshape(3, 4))
+        v = view_of(a)
+        assert v.rows == 3 and v.cols == 4 and np.array_equal(v.array(), a)
+
+    def test_hermitian_view(self):
+        v = MatrixView(np.zeros(16), 4, 4, 4, precision("d"))
+        hv = HermitianView(v, "L")
+        assert hv.uplo == "l" and hv.dim == 4
+        with pytest.raises(ValueError):
+            HermitianView(v, "x")
+        with pytest.raises(ValueError):
+            HermitianView(MatrixView(np.zeros(16), 4, 3, 4, precision("d")), "l")
+
+
+class TestPartition:
+    def test_kernel_config_validation(self):
+        KernelConfig(32, 4, 2)
+        for bad in ((31, 1), (0, 1), (32, 0), (32, 3)):
+            with pytest.raises(ValueError):
+                KernelConfig(*bad)
+        with pytest.raises(ValueError):
+            KernelConfig(32, 2, 0)
+
+    def test_tb_share_covers(self):
+        for total in range(0, 60):
+            for coop in range(1, 9):
+                cover = []
+                for s in range(coop):
+                    w, st = tb_share(total, coop, s)
+                    cover.extend(range(st, st + w))
+                assert cover == list(range(total))
+
+    def test_stream_k_split(self):
+        """Every item owned by exactly one CTA; shares differ by at most one."""
+        for total in (1, 7, 148, 1000, 2049):
+            for P in (1, 3, 148, 296):
+                if P > total:
+                    continue
+                sizes = [sk_start(c + 1, total, P) - sk_start(c, total, P) for c in range(P)]
+                assert sum(sizes) == total and max(sizes) - min(sizes) <= 1
+                for i in range(0, total, max(1, total // 50)):
+                    c = sk_owner(i, total, P)
+                    assert sk_start(c, total, P) <= i < sk_start(c + 1, total, P)
+
+
+class TestOffsetGeometry:
+    def test_effective_dims(self):
+        assert effective_dims(1000, 1000, 100, 70, 32) == (128, 96)
+        assert effective_dims(100, 100, 97, 99, 32) == (100, 100)
+        with pytest.raises(ValueError):
+            effective_dims(50, 50, 51, 10, 32)
+
+    def test_offset_request_validation(self):
+        parent = MatrixView(np.zeros(64 * 64), 64, 64, 64, precision("d"))
+        with pytest.raises(ValueError):
+            OffsetRequest(parent, -1, 0, 8, 8)
+        with pytest.raises(ValueError):
+            OffsetRequest(parent, 60, 0, 8, 8)
+
+    def test_realignment_padding_below_one_granule(self):
+        for eb in (4, 8, 16):
+            per = 32 // eb
+            for off in range(0, 40):
+                start, frame, lead = realigned_frame(off, 100, eb)
+                assert start % per == 0 and 0 <= lead < per and frame == lead + 100
+
+
+class TestLayout:
+    def test_cyclic_ownership(self):
+        assert owned_block_cols(7 * 32, 32, 3, 0) == [0, 3, 6]
+        assert owned_block_cols(7 * 32, 32, 3, 1) == [1, 4]
+
+    def test_local_counts(self):
+        assert local_col_count(100, 32, 2, 0) == 64
+        assert local_col_count(100, 32, 2, 1) == 36
+        assert required_local_elements(100, 100, 32, 2, 0) == 128 * 64
+        assert required_local_elements(100, 100, 32, 4, 3) == 128 * 4
+
+
+class TestRoofline:
+    def test_baseline_bytes(self):
+        """The algorithmic divisors quoted in BASELINE.md §2."""
+        d = precision("d")
+        z = precision("z")
+        assert roofline.byte_count(d, "gemv", 4096) == 134_316_032
+        assert roofline.flop_count(d, "gemv", 4096) == 33_562_624
+        assert roofline.byte_count(d, "symv", 32768) == 4_295_884_800
+        assert roofline.flop_count(d, "symv", 32768) == 2_147_549_184
+        assert roofline.byte_count(d, "symv", 100_000) == 40_002_800_000
+        assert roofline.byte_count(z, "symv", 100_000) == 80_005_600_000
+
+    def test_rectangular_forms_reduce_to_square(self):
+        for tag in "sdcz":
+            p = precision(tag)
+            assert roofline.gemv_bytes(p, 300, 300) == roofline.byte_count(p, "gemv", 300)
+            assert roofline.symv_bytes(p, 300) == roofline.byte_count(p, "symv", 300)
+            assert roofline.gemv_flops(p, 300, 300) == roofline.flop_count(p, "gemv", 300)
+            assert roofline.symv_flops(p, 300) == roofline.flop_count(p, "symv", 300)
+
+
+class TestCAbi:
+    def test_library_exports_every_header_symbol(self):
+        lib = _lib.load()
+        syms = _lib.header_symbols()
+        assert len(syms) >= 60
+        missing = [s for s in syms if not hasattr(lib, s)]
+        assert missing == []
+
+    def test_version_and_host_helpers(self):
+        lib = _lib.load()
+        assert b"sm_100a" in lib.kblas_version()
+        assert lib.kblas_mgpu_local_cols(100, 32, 2, 1) == 36
+        assert lib.kblas_mgpu_local_cols(100, 32, 4, 3) == 4
+        assert lib.kblas_mgpu_local_ld(100) == 128
+        assert lib.kblas_mgpu_local_cols(100, 0, 2, 1) == -1
+
+    def test_argument_errors_are_blas_style(self):
+        """xerbla numbering, checked before any device work."""
+        lib = _lib.load()
+        one = _lib.scalar("d", 1.0)
+        assert lib.kblas_dgemv(b"x", 4, 4, one, None, 4, None, 1, one, None, 1) == -1
+        assert lib.kblas_dgemv(b"n", -1, 4, one, None, 4, None, 1, one, None, 1) == -2
+        assert lib.kblas_dgemv(b"n", 4, -1, one, None, 4, None, 1, one, None, 1) == -3
+        assert lib.kblas_dgemv(b"n", 4, 4, one, None, 3, None, 1, one, None, 1) == -6
+        assert lib.kblas_dgemv(b"n", 4, 4, one, None, 4, None, 2, one, None, 1) == -8
+        assert lib.kblas_dgemv(b"n", 4, 4, one, None, 4, None, 1, one, None, 2) == -11
+        assert lib.kblas_dsymv(b"q", 4, one, None, 4, None, 1, one, None, 1) == -1
+        assert lib.kblas_dsymv(b"l", 4, one, None, 3, None, 1, one, None, 1) == -5
+        assert lib.kblas_dsymv(b"l", 4, one, None, 4, None, 3, one, None, 1) == -7
+        # quick returns: nothing to do, nothing launched
+        before = lib.kblas_launch_count()
+        assert lib.kblas_dgemv(b"n", 0, 0, one, None, 1, None, 1, one, None, 1) == 0
+        zero = _lib.scalar("d", 0.0)
+        assert lib.kblas_dsymv(b"l", 8, zero, None, 8, None, 1, one, None, 1) == 0
+        assert lib.kblas_launch_count() == before
+
+    def test_compute_without_gpu_fails_loudly(self):
+        """On a host without a GPU a compute call returns a CUDA error code
+        (no silent CPU path)."""
+        import torch
+
+        if torch.cuda.is_available():
+            pytest.skip("GPU present")
+        lib = _lib.load()
+        one = _lib.scalar("d", 1.0)
+        buf = (ctypes.c_double * 64)()
+        rc = lib.kblas_dgemv(b"n", 8, 8, one, ctypes.addressof(buf), 8, ctypes.addressof(buf), 1, one,
+                             ctypes.addressof(buf), 1)
+        assert rc > 0
+        from paper_1410_1726_b200 import gemv
+
+        with pytest.raises(RuntimeError):
+            gemv("n", 1.0, MatrixView(np.zeros(64), 8, 8, 8, precision("d")), np.zeros(8), 0.0, np.zeros(8))
