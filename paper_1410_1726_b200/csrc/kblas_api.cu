@@ -17,6 +17,7 @@
 #include <mutex>
 #include <string>
 #include <tuple>
+#include <utility>
 #include <vector>
 
 #include "../../include/kblas_b200.h"
@@ -135,6 +136,24 @@ template <> const char *tname<double2>() { return "z"; }
 
 inline int launched(int n = 1) { g_launches += n; return 0; }
 
+// Launch an epilogue with programmatic stream serialization: it may start
+// while the preceding streaming kernel drains and waits in
+// griddepcontrol.wait for that grid's completion (hides launch latency).
+template <class... KArgs, class... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, cudaStream_t st, Args &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 // ---------------------------------------------------------- load path
 // vec: 256-bit loads; needs lda*esize % 32 == 0.  The submatrix start is
 // realigned down to its 32-byte granule and the lead rows are masked.
@@ -157,8 +176,8 @@ int make_path(const T *A, long long lda, Path<T> *out) {
 // (NW warps, CW columns per warp, R vectors per lane per column)
 template <class T> struct Cfg {
   static constexpr int V = 32 / sizeof(T);
-  // gemv N / T
-  static constexpr int G_NW = 8, G_CW = 8, G_R = 1, G_RS = V;
+  // gemv N / T (register double-buffered: 2 x CW x R loads in flight per lane)
+  static constexpr int G_NW = 8, G_CW = 4, G_R = 1, G_RS = V;
   // symv / hemv: W = S_NW * S_CW columns per tile (the t1 partial traffic
   // is 2/W of the triangle); z halves CW to stay within 128 registers
   static constexpr int S_NW = 16, S_CW = sizeof(T) == 16 ? 4 : 8, S_R = 1, S_RS = V;
@@ -168,10 +187,10 @@ template <class T> struct Cfg {
 template <class T, int V, int NW, int CW, int R>
 cudaError_t run_gemv_n(const Path<T> &pa, long long lda, int m, int n, const T *x, ColMap cm, T *y,
                        T alpha, T beta, bool beta_zero, cudaStream_t st) {
-  constexpr int RB = 32 * V * R, CSTEP = NW * CW;
+  constexpr int RB = NW * 32 * V * R;
   auto kfn = gemv_n_kernel<T, V, NW, CW, R>;
   const long long nrb = cdiv((long long)pa.lead + m, RB);
-  const long long KS = cdiv(n, CSTEP);
+  const long long KS = cdiv(n, CW);
   const long long total = nrb * KS;
   const long long P = std::min<long long>(total, (long long)dev_sms() * occupancy((const void *)kfn, NW * 32));
   const long long per = std::max<long long>(1, total / P);
@@ -184,8 +203,8 @@ cudaError_t run_gemv_n(const Path<T> &pa, long long lda, int m, int n, const T *
     TimedScope ts(st);
     kfn<<<(unsigned)P, NW * 32, 0, st>>>(p);
   }
-  gemv_n_epilogue<T><<<(unsigned)cdiv(m, 256), 256, 0, st>>>(y, (const T *)ws, m, m, pa.lead, RB, (int)KS,
-                                                              total, (int)P, alpha, beta, beta_zero);
+  launch_pdl(gemv_n_epilogue<T>, (unsigned)cdiv(m, 256), 256, st, y, (const T *)ws, (long long)m, m, pa.lead,
+             (int)RB, (int)KS, total, (int)P, alpha, beta, (int)beta_zero);
   launched(2);
   char buf[256];
   snprintf(buf, sizeof buf, "gemv_n %s %s lead=%d m=%d n=%d RB=%d KS=%lld items=%lld P=%lld slots=%lld",
@@ -215,9 +234,8 @@ cudaError_t run_gemv_t(const Path<T> &pa, long long lda, int m, int n, long long
     TimedScope ts(st);
     kfn<<<(unsigned)P, NW * 32, 0, st>>>(p);
   }
-  gemv_t_epilogue<T><<<(unsigned)cdiv(nglob, 256), 256, 0, st>>>(y, (const T *)ws, ws_ld, nglob, CBW,
-                                                                  (int)KS, total, (int)P, cm, alpha, beta,
-                                                                  beta_zero);
+  launch_pdl(gemv_t_epilogue<T>, (unsigned)cdiv(nglob, 256), 256, st, y, (const T *)ws, ws_ld, nglob, (int)CBW,
+             (int)KS, total, (int)P, cm, alpha, beta, (int)beta_zero);
   launched(2);
   char buf[256];
   snprintf(buf, sizeof buf, "gemv_t %s %s%s lead=%d m=%d n=%d H=%d KS=%lld items=%lld P=%lld slots=%lld",
@@ -322,7 +340,7 @@ cudaError_t run_symv(const Path<T> &pa, long long lda, int d, const T *x, ColMap
     TimedScope ts(st);
     kfn<<<(unsigned)P, NW * 32, 0, st>>>(p);
   }
-  symv_epilogue<T, LOWER><<<(unsigned)cdiv(d, 256), 256, 0, st>>>(y, p, alpha, beta, beta_zero);
+  launch_pdl(symv_epilogue<T, LOWER, 8>, (unsigned)cdiv(d, 32), 256, st, y, p, alpha, beta, (int)beta_zero);
   launched(2);
   char buf[256];
   snprintf(buf, sizeof buf, "symv %s %s %s%s lead=%d d=%d W=%d H=%d tiles=%d items=%lld P=%lld slots=%lld",
@@ -403,7 +421,7 @@ int gemv_entry(char trans, int m, int n, T alpha, const T *dA, int lda, const T 
   const T *A = dA + (long long)offset_c * lda + offset_r;
   Path<T> pa;
   if (make_path(A, lda, &pa) != 0) return -5;
-  ColMap cm{1, 0, 1};
+  ColMap cm{1, 0, 1 << 30};
   return code(dispatch_gemv<T>(t, pa, lda, m, n, n, dx, cm, dy, alpha, beta, is_zero(beta), st));
 }
 
@@ -423,7 +441,7 @@ int symv_entry(char uplo, bool herm, int n, T alpha, const T *dA, int lda, const
   const T *A = dA + (long long)offset * lda + offset;
   Path<T> pa;
   if (make_path(A, lda, &pa) != 0) return -4;
-  ColMap cm{1, 0, n};
+  ColMap cm{1, 0, 1 << 30};
   return code(dispatch_symv<T>(u == 'l', herm, pa, lda, n, dx, cm, n, dy, alpha, beta, is_zero(beta), st));
 }
 

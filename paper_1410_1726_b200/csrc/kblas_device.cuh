@@ -98,65 +98,57 @@ template <class T> __device__ __forceinline__ T warp_sum(T v) {
 // loads (SASS LDG.E.ENL2.256): one instruction moves 32 bytes per lane, a
 // warp 1 KiB of a column.
 // ---------------------------------------------------------------------------
-struct U8 { uint32_t r[8]; };
-__device__ __forceinline__ U8 ld_stream_v8(const void *p) {
-  U8 u;
-  asm("ld.global.nc.L1::no_allocate.L2::evict_first.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-      : "=r"(u.r[0]), "=r"(u.r[1]), "=r"(u.r[2]), "=r"(u.r[3]),
-        "=r"(u.r[4]), "=r"(u.r[5]), "=r"(u.r[6]), "=r"(u.r[7])
-      : "l"(p));
-  return u;
-}
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t pol;
   asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   return pol;
 }
-__device__ __forceinline__ float ld_stream(const float *p, uint64_t pol) {
-  float v;
-  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
-  return v;
-}
-__device__ __forceinline__ double ld_stream(const double *p, uint64_t pol) {
-  double v;
-  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
-  return v;
-}
-__device__ __forceinline__ float2 ld_stream(const float2 *p, uint64_t pol) {
-  float2 v;
-  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f32 {%0,%1}, [%2], %3;"
-      : "=f"(v.x), "=f"(v.y) : "l"(p), "l"(pol));
-  return v;
-}
-__device__ __forceinline__ double2 ld_stream(const double2 *p, uint64_t pol) {
-  double2 v;
-  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
-      : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
-  return v;
-}
-
-// V consecutive elements starting at p.  V * sizeof(T) == 32 uses one
-// 256-bit load (p must be 32-byte aligned); V == 1 loads one element.
-template <class T, int V> struct Pack { T v[V]; };
-template <class T, int V>
-__device__ __forceinline__ Pack<T, V> ld_pack(const T *p, uint64_t pol) {
-  Pack<T, V> r;
-  if constexpr (V * sizeof(T) == 32) {
-    union { U8 u; T t[V]; } cv;
-    cv.u = ld_stream_v8(p);
-#pragma unroll
-    for (int v = 0; v < V; ++v) r.v[v] = cv.t[v];
-  } else {
-    static_assert(V == 1, "scalar path loads one element");
-    r.v[0] = ld_stream(p, pol);
+// V consecutive elements starting at p, kept as raw 32-bit words so the
+// load writes straight into the registers the FMAs read (a predicated-off
+// load leaves the words zero).  V * sizeof(T) == 32 is one 256-bit load
+// (p 32-byte aligned); V == 1 loads one element (natural alignment).
+template <class T, int V> struct Pack {
+  static constexpr int W = V * (int)sizeof(T) / 4;
+  uint32_t w[W];
+  __device__ __forceinline__ T v(int k) const {
+    if constexpr (sizeof(T) == 4) {
+      return __uint_as_float(w[k]);
+    } else if constexpr (sizeof(T) == 16) {
+      return T{__hiloint2double((int)w[4 * k + 1], (int)w[4 * k]), __hiloint2double((int)w[4 * k + 3], (int)w[4 * k + 2])};
+    } else if constexpr (Elem<T>::cplx) {
+      return T{__uint_as_float(w[2 * k]), __uint_as_float(w[2 * k + 1])};
+    } else {
+      return __hiloint2double((int)w[2 * k + 1], (int)w[2 * k]);
+    }
   }
-  return r;
-}
-template <class T, int V> __device__ __forceinline__ Pack<T, V> zero_pack() {
-  Pack<T, V> r;
+};
+
+template <class T, int V>
+__device__ __forceinline__ void ld_pack(Pack<T, V> &a, const T *p, bool pred, uint64_t pol) {
+  constexpr int W = Pack<T, V>::W;
 #pragma unroll
-  for (int v = 0; v < V; ++v) r.v[v] = zero<T>();
-  return r;
+  for (int k = 0; k < W; ++k) a.w[k] = 0u;
+  const int pr = pred ? 1 : 0;
+  if constexpr (W == 8) {
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %9, 0;\n\t"
+        "@q ld.global.nc.L1::no_allocate.L2::evict_first.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n\t}"
+        : "+r"(a.w[0]), "+r"(a.w[1]), "+r"(a.w[2]), "+r"(a.w[3]), "+r"(a.w[4]), "+r"(a.w[5]), "+r"(a.w[6]), "+r"(a.w[7])
+        : "l"(p), "r"(pr));
+  } else if constexpr (W == 4) {
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %5, 0;\n\t"
+        "@q ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %6;\n\t}"
+        : "+r"(a.w[0]), "+r"(a.w[1]), "+r"(a.w[2]), "+r"(a.w[3])
+        : "l"(p), "r"(pr), "l"(pol));
+  } else if constexpr (W == 2) {
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %3, 0;\n\t"
+        "@q ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %4;\n\t}"
+        : "+r"(a.w[0]), "+r"(a.w[1]) : "l"(p), "r"(pr), "l"(pol));
+  } else {
+    static_assert(W == 1, "unsupported pack width");
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t"
+        "@q ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %3;\n\t}"
+        : "+r"(a.w[0]) : "l"(p), "r"(pr), "l"(pol));
+  }
 }
 
 // ---------------------------------------------------------------------------

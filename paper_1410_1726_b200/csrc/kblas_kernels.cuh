@@ -28,6 +28,16 @@
 
 namespace kb {
 
+// ---------------------------------------------------------------------------
+// Programmatic dependent launch: the epilogue grid is launched while the
+// streaming kernel runs (launch latency hidden) and blocks here until the
+// streaming grid has completed and its writes are visible.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 struct GemvParams {
   const void *A;    // 32-byte aligned base: physical row 0 of local column 0
   long long lda;
@@ -43,17 +53,21 @@ struct GemvParams {
 };
 
 // ---------------------------------------------------------------------------
-// GEMV-N.  Item = (row block of RB = 32*V*R rows) x (NW*CW columns); items
-// are ordered row-block-major so a CTA accumulates one row block across many
-// columns in registers, reduces across its warps through shared memory and
-// writes one partial slot per row block it touched.
+// GEMV-N.  The NW warps of a CTA are stacked along the rows: a CTA row block
+// is RB = NW*32*V*R rows, so every column visit reads RB*sizeof(T) contiguous
+// bytes (8 KiB for D) and each warp owns its own rows.  Item = (row block) x
+// (CW columns); items are row-block-major, so a CTA sweeps its row block
+// across a contiguous column range, keeps the partial row sums in
+// registers, and writes them once per row block it touched (no shared
+// memory, no barrier).  The next item's loads are issued before the current
+// item's FMAs (register double buffering, as the paper's Alg. 1 does with
+// its two half-block buffers).
 // ---------------------------------------------------------------------------
 template <class T, int V, int NW, int CW, int R>
 __global__ void __launch_bounds__(NW * 32) gemv_n_kernel(const GemvParams p) {
-  constexpr int NT = NW * 32;
-  constexpr int RB = 32 * V * R;
-  constexpr int CSTEP = NW * CW;
-  __shared__ T red[NW][RB];
+  griddep_launch_dependents();
+  constexpr int WR = 32 * V * R;  // rows per warp
+  constexpr int RB = NW * WR;     // rows per CTA row block
   const T *__restrict__ A = static_cast<const T *>(p.A);
   const T *__restrict__ x = static_cast<const T *>(p.x);
   T *__restrict__ ws = static_cast<T *>(p.ws);
@@ -67,51 +81,65 @@ __global__ void __launch_bounds__(NW * 32) gemv_n_kernel(const GemvParams p) {
     const long long rb = it / p.KS;
     const long long rb_first = rb * p.KS;
     const long long stop = min(end, rb_first + p.KS);
-    const long long p0 = rb * RB;
+    const long long pw = rb * RB + warp * WR;  // first physical row of this warp
+    bool rok[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) rok[r] = pw + r * 32 * V + lane * V < plimit;
     T acc[R][V];
 #pragma unroll
     for (int r = 0; r < R; ++r)
 #pragma unroll
       for (int v = 0; v < V; ++v) acc[r][v] = zero<T>();
 
-    for (long long q = it; q < stop; ++q) {
-      const int cbase = (int)(q - rb_first) * CSTEP + warp * CW;
-      Pack<T, V> a[CW][R];
-      T xv[CW];
+    auto load = [&](long long q, Pack<T, V> (&a)[CW][R], T (&xv)[CW]) {
+      const int c0 = (int)(q - rb_first) * CW;
+      // CW consecutive local columns map to consecutive global columns
+      // unless they straddle a distribution block (mgpu only)
+      const long long g0 = map_col(p.cm, c0);
+      const bool contiguous = p.cm.G == 1 || (c0 % p.cm.nb) + CW <= p.cm.nb;
 #pragma unroll
       for (int j = 0; j < CW; ++j) {
-        const int col = cbase + j;
+        const int col = c0 + j;
         const bool cok = col < p.n;
-        xv[j] = cok ? __ldg(x + map_col(p.cm, col)) : zero<T>();
-        const T *colp = A + (long long)col * p.lda + p0 + lane * V;
+        const long long gx = contiguous ? g0 + j : map_col(p.cm, col);
+        xv[j] = cok ? __ldg(x + gx) : zero<T>();
+        const T *colp = A + (long long)col * p.lda + pw + lane * V;
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const long long ps = p0 + r * 32 * V + lane * V;
-          a[j][r] = (cok && ps < plimit) ? ld_pack<T, V>(colp + r * 32 * V, pol) : zero_pack<T, V>();
-        }
+        for (int r = 0; r < R; ++r) ld_pack(a[j][r], colp + r * 32 * V, cok && rok[r], pol);
       }
+    };
+    Pack<T, V> a0[CW][R], a1[CW][R];
+    T x0[CW], x1[CW];
+    long long q = it;
+    load(q, a0, x0);
+    while (q < stop) {
+      const bool more = q + 1 < stop;
+      if (more) load(q + 1, a1, x1);
 #pragma unroll
       for (int j = 0; j < CW; ++j)
 #pragma unroll
         for (int r = 0; r < R; ++r)
 #pragma unroll
-          for (int v = 0; v < V; ++v) acc[r][v] = fma_(a[j][r].v[v], xv[j], acc[r][v]);
+          for (int v = 0; v < V; ++v) acc[r][v] = fma_(a0[j][r].v(v), x0[j], acc[r][v]);
+      if (!more) break;
+      if (q + 2 < stop) load(q + 2, a0, x0);
+#pragma unroll
+      for (int j = 0; j < CW; ++j)
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+          for (int v = 0; v < V; ++v) acc[r][v] = fma_(a1[j][r].v(v), x1[j], acc[r][v]);
+      q += 2;
     }
 
+    const long long slot = (long long)blockIdx.x - sk_owner(rb_first, p.total, p.P);
 #pragma unroll
     for (int r = 0; r < R; ++r)
 #pragma unroll
-      for (int v = 0; v < V; ++v) red[warp][r * 32 * V + lane * V + v] = acc[r][v];
-    __syncthreads();
-    const long long slot = (long long)blockIdx.x - sk_owner(rb_first, p.total, p.P);
-    for (int t = threadIdx.x; t < RB; t += NT) {
-      T s = red[0][t];
-#pragma unroll
-      for (int w = 1; w < NW; ++w) s = add_(s, red[w][t]);
-      const long long i = p0 + t - p.lead;
-      if (i >= 0 && i < p.m) ws[slot * p.ws_ld + i] = s;
-    }
-    __syncthreads();
+      for (int v = 0; v < V; ++v) {
+        const long long i = pw + r * 32 * V + lane * V + v - p.lead;
+        if (i >= 0 && i < p.m) ws[slot * p.ws_ld + i] = acc[r][v];
+      }
     it = stop;
   }
 }
@@ -126,6 +154,7 @@ __global__ void __launch_bounds__(NW * 32) gemv_n_kernel(const GemvParams p) {
 // ---------------------------------------------------------------------------
 template <class T, int V, int NW, int CW, int R, bool CONJ>
 __global__ void __launch_bounds__(NW * 32) gemv_t_kernel(const GemvParams p) {
+  griddep_launch_dependents();
   constexpr int H = 32 * V * R;
   constexpr int CBW = NW * CW;
   const T *__restrict__ A = static_cast<const T *>(p.A);
@@ -147,35 +176,54 @@ __global__ void __launch_bounds__(NW * 32) gemv_t_kernel(const GemvParams p) {
 #pragma unroll
     for (int j = 0; j < CW; ++j) t2[j] = zero<T>();
 
-    for (long long q = it; q < stop; ++q) {
+    // chunk loads: A (CW columns x R vectors) and the matching x rows;
+    // rows outside [0, m) are zeroed in x and masked in A with a select,
+    // so padding / a parent's neighbouring rows (possibly NaN) never enter
+    auto load = [&](long long q, Pack<T, V> (&a)[CW][R], T (&xr)[R][V]) {
       const long long p0 = (q - cb_first) * H;
-      T xr[R][V];
-      bool ok[R][V];
 #pragma unroll
       for (int r = 0; r < R; ++r)
 #pragma unroll
         for (int v = 0; v < V; ++v) {
           const long long i = p0 + r * 32 * V + lane * V + v - p.lead;
-          ok[r][v] = (i >= 0) && (i < p.m);
-          xr[r][v] = ok[r][v] ? __ldg(x + i) : zero<T>();
+          xr[r][v] = (i >= 0 && i < p.m) ? __ldg(x + i) : zero<T>();
         }
-      Pack<T, V> a[CW][R];
 #pragma unroll
       for (int j = 0; j < CW; ++j) {
         const bool cok = col0 + j < p.n;
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           const long long ps = p0 + r * 32 * V + lane * V;
-          a[j][r] = (cok && ps < plimit) ? ld_pack<T, V>(Aw + (long long)j * p.lda + ps, pol)
-                                         : zero_pack<T, V>();
+          ld_pack(a[j][r], Aw + (long long)j * p.lda + ps, cok && ps < plimit, pol);
         }
       }
+    };
+    auto fma_chunk = [&](long long q, const Pack<T, V> (&a)[CW][R], const T (&xr)[R][V]) {
+      const long long p0 = (q - cb_first) * H;
+      const bool interior = p0 >= p.lead && p0 + H <= plimit;
 #pragma unroll
       for (int j = 0; j < CW; ++j)
 #pragma unroll
         for (int r = 0; r < R; ++r)
 #pragma unroll
-          for (int v = 0; v < V; ++v) t2[j] = fmax_<CONJ>(sel(ok[r][v], a[j][r].v[v]), xr[r][v], t2[j]);
+          for (int v = 0; v < V; ++v) {
+            const long long i = p0 + r * 32 * V + lane * V + v - p.lead;
+            const bool ok = interior || (i >= 0 && i < p.m);
+            t2[j] = fmax_<CONJ>(sel(ok, a[j][r].v(v)), xr[r][v], t2[j]);
+          }
+    };
+    Pack<T, V> a0[CW][R], a1[CW][R];
+    T x0[R][V], x1[R][V];
+    long long q = it;
+    load(q, a0, x0);
+    while (q < stop) {
+      const bool more = q + 1 < stop;
+      if (more) load(q + 1, a1, x1);
+      fma_chunk(q, a0, x0);
+      if (!more) break;
+      if (q + 2 < stop) load(q + 2, a0, x0);
+      fma_chunk(q + 1, a1, x1);
+      q += 2;
     }
 
     const long long slot = (long long)blockIdx.x - sk_owner(cb_first, p.total, p.P);
@@ -240,6 +288,7 @@ struct SymParams {
 
 template <class T, int V, int NW, int CW, int R, bool LOWER, bool HERM>
 __global__ void __launch_bounds__(NW * 32, 1) symv_kernel(const SymParams p) {
+  griddep_launch_dependents();
   constexpr int NT = NW * 32;
   constexpr int H = 32 * V * R;
   constexpr int W = NW * CW;
@@ -303,9 +352,7 @@ __global__ void __launch_bounds__(NW * 32, 1) symv_kernel(const SymParams p) {
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           const long long vs = p0 + r * 32 * V + lane * V;
-          a[j][r] = (cok && vs < vhi && vs + V > vlo)
-                        ? ld_pack<T, V>(Aw + (long long)j * p.lda + vs, pol)
-                        : zero_pack<T, V>();
+          ld_pack(a[j][r], Aw + (long long)j * p.lda + vs, cok && vs < vhi && vs + V > vlo, pol);
         }
       }
       T acc[R][V];
@@ -323,7 +370,7 @@ __global__ void __launch_bounds__(NW * 32, 1) symv_kernel(const SymParams p) {
           for (int r = 0; r < R; ++r)
 #pragma unroll
             for (int v = 0; v < V; ++v) {
-              const T e = sel(ok[r][v], a[j][r].v[v]);
+              const T e = sel(ok[r][v], a[j][r].v(v));
               acc[r][v] = fma_(e, xc[j], acc[r][v]);
               t2[j] = fmax_<HERM>(e, xr[r][v], t2[j]);
             }
@@ -338,10 +385,10 @@ __global__ void __launch_bounds__(NW * 32, 1) symv_kernel(const SymParams p) {
               const long long i = g0 + r * 32 * V + lane * V + v;
               const bool in1 = ok[r][v] && (LOWER ? i >= c : i <= c);
               const bool in2 = ok[r][v] && (LOWER ? i > c : i < c);
-              T e1 = sel(in1, a[j][r].v[v]);
+              T e1 = sel(in1, a[j][r].v(v));
               if (HERM && i == c) e1 = realify(e1);
               acc[r][v] = fma_(e1, xc[j], acc[r][v]);
-              t2[j] = fmax_<HERM>(sel(in2, a[j][r].v[v]), xr[r][v], t2[j]);
+              t2[j] = fmax_<HERM>(sel(in2, a[j][r].v(v)), xr[r][v], t2[j]);
             }
         }
       }
@@ -389,6 +436,7 @@ template <class T>
 __global__ void gemv_n_epilogue(T *y, const T *__restrict__ ws, long long ws_ld, int m, int lead,
                                 int RB, int KS, long long total, int P, T alpha, T beta,
                                 int beta_zero) {
+  griddep_wait();
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= m) return;
   const long long rb = (i + lead) / RB;
@@ -405,6 +453,7 @@ template <class T>
 __global__ void gemv_t_epilogue(T *y, const T *__restrict__ ws, long long ws_ld, long long nglob,
                                 int CBW, int KS, long long total, int P, ColMap cm, T alpha, T beta,
                                 int beta_zero) {
+  griddep_wait();
   const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= nglob) return;
   const long long l = unmap_col(cm, c);
@@ -417,10 +466,18 @@ __global__ void gemv_t_epilogue(T *y, const T *__restrict__ ws, long long ws_ld,
   store_axpby(y, c, alpha, s, beta, beta_zero);
 }
 
-template <class T, bool LOWER>
-__global__ void symv_epilogue(T *y, const SymParams p, T alpha, T beta, int beta_zero) {
-  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= p.d) return;
+// One CTA per 32 rows (lane = row).  The t1 partials of a row are spread
+// over up to d/W tiles; the EW warps split that tile range into EW fixed
+// contiguous parts (a function of the row only, so the summation order is
+// fixed and results are bit-reproducible), then warp 0 adds the parts in
+// order plus the row's t2 slots.
+template <class T, bool LOWER, int EW>
+__global__ void __launch_bounds__(EW * 32) symv_epilogue(T *y, const SymParams p, T alpha, T beta, int beta_zero) {
+  griddep_wait();
+  __shared__ T part[EW][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long i = (long long)blockIdx.x * 32 + lane;
+  const bool valid = i < p.d;
   const T *__restrict__ ws1 = static_cast<const T *>(p.ws1);
   const T *__restrict__ ws2 = static_cast<const T *>(p.ws2);
   // nle = number of tiles with gcol0 <= i (tiles sorted by gcol0)
@@ -430,15 +487,32 @@ __global__ void symv_epilogue(T *y, const SymParams p, T alpha, T beta, int beta
     if (p.tiles[mid].gcol0 <= i) lo = mid + 1; else hi = mid;
   }
   const int nle = lo;
-  T s = zero<T>();
-  // t1: tiles whose stored rows include i
+  int kb, ke;
   if (LOWER) {
-    for (int k = 0; k < nle; ++k) s = add_(s, ws1[(long long)k * p.ws1_ld + i]);
+    kb = 0;
+    ke = nle;
   } else {
-    int k0 = nle;
-    while (k0 > 0 && p.tiles[k0 - 1].gcol0 + p.tiles[k0 - 1].ncols > i) --k0;
-    for (int k = k0; k < p.ntiles; ++k) s = add_(s, ws1[(long long)k * p.ws1_ld + i]);
+    kb = nle;
+    if (nle > 0 && p.tiles[nle - 1].gcol0 + p.tiles[nle - 1].ncols > i) kb = nle - 1;
+    ke = p.ntiles;
   }
+  const int len = valid ? ke - kb : 0;
+  const int k0 = kb + (int)((long long)len * warp / EW), k1 = kb + (int)((long long)len * (warp + 1) / EW);
+  T s0 = zero<T>(), s1 = zero<T>(), s2 = zero<T>(), s3 = zero<T>();
+  int k = k0;
+  for (; k + 4 <= k1; k += 4) {
+    s0 = add_(s0, ws1[(long long)k * p.ws1_ld + i]);
+    s1 = add_(s1, ws1[(long long)(k + 1) * p.ws1_ld + i]);
+    s2 = add_(s2, ws1[(long long)(k + 2) * p.ws1_ld + i]);
+    s3 = add_(s3, ws1[(long long)(k + 3) * p.ws1_ld + i]);
+  }
+  for (; k < k1; ++k) s0 = add_(s0, ws1[(long long)k * p.ws1_ld + i]);
+  part[warp][lane] = add_(add_(s0, s1), add_(s2, s3));
+  __syncthreads();
+  if (warp != 0 || !valid) return;
+  T s = part[0][lane];
+#pragma unroll
+  for (int w = 1; w < EW; ++w) s = add_(s, part[w][lane]);
   // t2: the tile owning column i (if any on this GPU)
   if (nle > 0) {
     const SymTile tl = p.tiles[nle - 1];
