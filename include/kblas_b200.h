@@ -300,6 +300,17 @@ unsigned long long kblas_launch_count(void);
 /* the number of timed launches, then clears the record.               */
 int kblas_timing_enable(int enable);
 int kblas_timing_read(double *total_ms, int *launches);
+/* Select the SYMV/HEMV streaming kernel: -1 (default) = per-precision */
+/* choice from the empirical tuning, 1 = TMA-fed warp-specialised      */
+/* pipeline whenever the operand allows it (column stride a multiple   */
+/* of 16 bytes), 0 = register-load kernel.  Returns the previous mode. */
+/* (Env KBLAS_NO_TMA=1 selects 0 at load.)                             */
+int kblas_set_tma(int mode);
+/* Tuning hook for the TMA SYMV/HEMV kernel shape (consumer warps, */
+/* columns per warp, rows per lane, pipeline stages); -1 = tuned      */
+/* per-precision default.  Used by scripts/tune_symv.py; returns the  */
+/* previous variant.                                                  */
+int kblas_set_symv_variant(int variant);
 /* Description of the last plan chosen for a call on this thread      */
 /* (kernel family, grid, items, workspace bytes) as a NUL-terminated   */
 /* string; for reports and tests.                                      */

@@ -125,6 +125,10 @@ def load():
         lib.kblas_timing_enable.restype = c_int
         lib.kblas_timing_read.argtypes = [POINTER(c_double), POINTER(c_int)]
         lib.kblas_timing_read.restype = c_int
+        lib.kblas_set_symv_variant.argtypes = [c_int]
+        lib.kblas_set_symv_variant.restype = c_int
+        lib.kblas_set_tma.argtypes = [c_int]
+        lib.kblas_set_tma.restype = c_int
         lib.kblas_last_plan.restype = ctypes.c_char_p
         lib.kblas_last_plan.argtypes = []
         lib.kblas_version.restype = ctypes.c_char_p
@@ -162,6 +166,13 @@ def launch_count() -> int:
 
 def last_plan() -> str:
     return load().kblas_last_plan().decode()
+
+
+def set_tma(mode) -> int:
+    """SYMV/HEMV kernel: True/1 TMA-fed pipeline, False/0 register-load
+    kernel, -1 tuned per-precision default.  Returns the previous mode."""
+    m = -1 if mode == -1 else (1 if mode else 0)
+    return int(load().kblas_set_tma(m))
 
 
 def timing_enable(on: bool):

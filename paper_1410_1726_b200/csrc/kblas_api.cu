@@ -12,6 +12,7 @@
 
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -20,8 +21,11 @@
 #include <utility>
 #include <vector>
 
+#include <cudaTypedefs.h>
+
 #include "../../include/kblas_b200.h"
 #include "kblas_kernels.cuh"
+#include "kblas_symv_tma.cuh"
 
 using namespace kb;
 
@@ -181,6 +185,7 @@ template <class T> struct Cfg {
   // symv / hemv: W = S_NW * S_CW columns per tile (the t1 partial traffic
   // is 2/W of the triangle); z halves CW to stay within 128 registers
   static constexpr int S_NW = 16, S_CW = sizeof(T) == 16 ? 4 : 8, S_R = 1, S_RS = V;
+
 };
 
 // ============================================================= GEMV-N
@@ -256,11 +261,13 @@ std::map<std::vector<long long>, TileTable> g_tiles;
 
 // Tiles for the local panel of GPU g under the block-cyclic layout (G=1,
 // nb=d for a single GPU): every owned block column is cut into W-wide tiles.
+// exact: chunks start at each tile's first stored row (TMA path); else on
+// the physical H-row grid (vector-load path, 32-byte granules).
 cudaError_t tile_table(int d, int lead, bool lower, int W, int H, ColMap cm, int ncols_local, long long P,
-                       TileTable *out) {
+                       TileTable *out, bool exact = false) {
   int dev = 0;
   cudaGetDevice(&dev);
-  std::vector<long long> key{dev, d, lead, lower, W, H, cm.G, cm.g, cm.nb, ncols_local, P};
+  std::vector<long long> key{dev, d, lead, lower, W, H, cm.G, cm.g, cm.nb, ncols_local, P, exact};
   {
     std::lock_guard<std::mutex> lk(g_mu);
     auto it = g_tiles.find(key);
@@ -282,8 +289,8 @@ cudaError_t tile_table(int d, int lead, bool lower, int W, int H, ColMap cm, int
       t.ncols = (int)std::min<long long>(W, lblk1 - s);
       t.row0 = lower ? t.gcol0 : 0;
       t.row1 = lower ? d : std::min(d, t.gcol0 + t.ncols);
-      const long long c0 = ((long long)t.row0 + lead) / H;
-      const long long c1 = cdiv((long long)t.row1 + lead, H);
+      const long long c0 = exact ? 0 : ((long long)t.row0 + lead) / H;
+      const long long c1 = exact ? cdiv((long long)t.row1 - t.row0, H) : cdiv((long long)t.row1 + lead, H);
       t.chunk0 = (int)c0;
       t.prefix = prefix;
       prefix += c1 - c0;
@@ -350,6 +357,111 @@ cudaError_t run_symv(const Path<T> &pa, long long lda, int d, const T *x, ColMap
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------- SYMV via TMA
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void *ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  });
+  return fn;
+}
+
+// SYMV/HEMV kernel choice: -1 auto (per-precision default from the
+// empirical tuning in profiles/r1_tune_symv_*.jsonl), 0 register-load
+// kernel, 1 TMA kernel.  KBLAS_NO_TMA=1 forces 0 at load.
+int g_use_tma = -2;
+int g_symv_variant = -1;  // -1: per-precision default variant
+int tma_mode() {
+  if (g_use_tma == -2) {
+    const char *e = getenv("KBLAS_NO_TMA");
+    g_use_tma = (e && e[0] == '1') ? 0 : -1;
+  }
+  return g_use_tma;
+}
+bool use_tma() { return tma_mode() != 0; }
+// tuned defaults: TMA for s and z (variants 0 / 1), registers for d and c
+template <class T> bool prefer_tma() { return sizeof(T) == 16 || sizeof(T) == 4; }
+template <class T> int default_variant() { return sizeof(T) == 16 ? 1 : 0; }
+
+// A00: element (0,0) of the d x d operand (any row alignment); needs a
+// 16-byte multiple column stride.
+template <class T>
+bool tma_ok(const T *A00, long long lda) {
+  const uintptr_t addr = reinterpret_cast<uintptr_t>(A00);
+  const int mode = tma_mode();
+  const bool want = mode == 1 || (mode == -1 && prefer_tma<T>());
+  return want && tensor_map_encoder() != nullptr && (lda * (long long)sizeof(T)) % 16 == 0 &&
+         addr % sizeof(T) == 0;
+}
+
+template <class T, int NC, int CW, int RS, int S, bool LOWER, bool HERM>
+cudaError_t run_symv_tma(const T *A00, long long lda, int d, const T *x, ColMap cm, int ncols_local, T *y,
+                         T alpha, T beta, bool beta_zero, cudaStream_t st) {
+  constexpr int HS = Stage<T, RS>::HS, W = NC * CW;
+  constexpr size_t smem = symv_tma_smem<T, NC, CW, RS, S>();
+  static_assert(smem <= 227 * 1024, "shared memory budget");
+  auto kfn = symv_tma_kernel<T, NC, CW, RS, S, LOWER, HERM>;
+  {
+    static std::once_flag once;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(once, [&] {
+      attr_err = cudaFuncSetAttribute((const void *)kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    });
+    if (attr_err != cudaSuccess) return attr_err;
+  }
+  const uintptr_t addr = reinterpret_cast<uintptr_t>(A00);
+  const int lead = (int)((addr % 16) / sizeof(T));
+  const T *base = A00 - lead;
+  const int unit = sizeof(T) == 16 ? 8 : (int)sizeof(T);
+  const int upe = (int)sizeof(T) / unit;
+  CUtensorMap map;
+  cuuint64_t dims[2] = {(cuuint64_t)(lead + d) * upe, (cuuint64_t)std::max(ncols_local, 1)};
+  cuuint64_t strides[1] = {(cuuint64_t)lda * sizeof(T)};
+  cuuint32_t box[2] = {(cuuint32_t)(HS * upe), (cuuint32_t)W};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult cr = tensor_map_encoder()(&map, unit == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
+                                     2, (void *)base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  const long long Pmax = dev_sms();
+  TileTable tt;
+  cudaError_t e = tile_table(d, lead, LOWER, W, HS, cm, ncols_local, Pmax, &tt);
+  if (e != cudaSuccess) return e;
+  if (tt.ntiles == 0 || tt.total == 0) {
+    scal_kernel<T><<<(unsigned)cdiv(d, 256), 256, 0, st>>>(y, d, zero<T>(), 1);
+    launched();
+    return cudaGetLastError();
+  }
+  const long long P = std::min<long long>(tt.total, Pmax);
+  const size_t b1 = align256((size_t)tt.ntiles * d * sizeof(T));
+  const size_t b2 = align256((size_t)tt.maxslots * d * sizeof(T));
+  void *ws = nullptr;
+  e = workspace(b1 + b2, st, &ws);
+  if (e != cudaSuccess) return e;
+  SymTmaParams tp;
+  tp.sp = SymParams{base, lda, d, lead, x, ws, (long long)d, (char *)ws + b1, (long long)d,
+                    tt.dev, tt.ntiles, tt.total, (int)P};
+  tp.unit_per_elem = upe;
+  {
+    TimedScope ts(st);
+    kfn<<<(unsigned)P, (NC + 2) * 32, smem, st>>>(map, tp);
+  }
+  launch_pdl(symv_epilogue<T, LOWER, 8>, (unsigned)cdiv(d, 32), 256, st, y, tp.sp, alpha, beta, (int)beta_zero);
+  launched(2);
+  char buf[256];
+  snprintf(buf, sizeof buf, "symv_tma %s %s%s lead=%d d=%d W=%d H=%d S=%d tiles=%d items=%lld P=%lld slots=%lld smem=%zu",
+           tname<T>(), LOWER ? "L" : "U", HERM ? " herm" : "", lead, d, W, HS, S, tt.ntiles, tt.total, P,
+           tt.maxslots, (size_t)smem);
+  g_last_plan = buf;
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------ dispatch
 template <class T>
 cudaError_t dispatch_gemv(char trans, const Path<T> &pa, long long lda, int m, int n, long long nglob,
@@ -371,6 +483,33 @@ template <class T, bool HERM>
 cudaError_t dispatch_symv_h(bool lower, const Path<T> &pa, long long lda, int d, const T *x, ColMap cm,
                             int ncols_local, T *y, T alpha, T beta, bool beta_zero, cudaStream_t st) {
   using C = Cfg<T>;
+  const T *A00 = pa.base + pa.lead;
+  if (tma_ok(A00, lda)) {
+#define KB_TMA(NC, CW, RS, S)                                                                                 \
+  return lower ? run_symv_tma<T, NC, CW, RS, S, true, HERM>(A00, lda, d, x, cm, ncols_local, y, alpha, beta,  \
+                                                             beta_zero, st)                                  \
+               : run_symv_tma<T, NC, CW, RS, S, false, HERM>(A00, lda, d, x, cm, ncols_local, y, alpha, beta, \
+                                                              beta_zero, st)
+    // tuning variants (kblas_set_symv_variant); 0 is the default
+    // (consumer warps, columns per warp, rows per lane, stages)
+    if constexpr (sizeof(T) == 16) {
+      switch (g_symv_variant < 0 ? default_variant<T>() : g_symv_variant) {
+        case 1: KB_TMA(8, 8, 2, 3);
+        case 2: KB_TMA(16, 8, 1, 3);
+        case 3: KB_TMA(8, 16, 1, 3);
+        default: KB_TMA(16, 4, 1, 5);
+      }
+    } else {
+      switch (g_symv_variant < 0 ? default_variant<T>() : g_symv_variant) {
+        case 1: KB_TMA(16, 8, 1, 5);
+        case 2: KB_TMA(8, 8, 4, 3);
+        case 3: KB_TMA(16, 8, 4, 1);
+        case 4: KB_TMA(8, 16, 2, 3);
+        default: KB_TMA(16, 8, 2, 3);
+      }
+    }
+#undef KB_TMA
+  }
   if (lower) {
     if (pa.vec) return run_symv<T, C::V, C::S_NW, C::S_CW, C::S_R, true, HERM>(pa, lda, d, x, cm, ncols_local, y, alpha, beta, beta_zero, st);
     return run_symv<T, 1, C::S_NW, C::S_CW, C::S_RS, true, HERM>(pa, lda, d, x, cm, ncols_local, y, alpha, beta, beta_zero, st);
@@ -736,6 +875,18 @@ int kblas_timing_read(double *total_ms, int *launches) {
 }
 
 const char *kblas_last_plan(void) { return g_last_plan.c_str(); }
+
+int kblas_set_symv_variant(int v) {
+  const int prev = g_symv_variant;
+  g_symv_variant = v;
+  return prev;
+}
+
+int kblas_set_tma(int mode) {
+  const int prev = tma_mode();
+  g_use_tma = mode < 0 ? -1 : (mode ? 1 : 0);
+  return prev;
+}
 
 const char *kblas_version(void) { return "kblas-b200 0.1.0 (sm_100a)"; }
 

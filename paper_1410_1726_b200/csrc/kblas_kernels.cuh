@@ -316,6 +316,7 @@ __global__ void __launch_bounds__(NW * 32, 1) symv_kernel(const SymParams p) {
   }
   int buf = 0;
   const int cl = warp * CW;
+  const uint64_t keep = policy_evict_last();
 
   while (it < end) {
     const SymTile tl = p.tiles[k];
@@ -404,7 +405,7 @@ __global__ void __launch_bounds__(NW * 32, 1) symv_kernel(const SymParams p) {
           T s = red[buf][0][t];
 #pragma unroll
           for (int w = 1; w < NW; ++w) s = add_(s, red[buf][w][t]);
-          ws1[(long long)k * p.ws1_ld + (ps - p.lead)] = s;
+          st_keep(ws1 + (long long)k * p.ws1_ld + (ps - p.lead), s, keep);
         }
       }
       buf ^= 1;

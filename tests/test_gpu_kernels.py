@@ -368,3 +368,50 @@ class TestLarge:
         s2 = kb.symv_hemv("l", 1.0, hv, x2, 0.0, y0).y_out
         s12 = kb.symv_hemv("l", 1.0, hv, x1 + x2, 0.0, y0).y_out
         assert (s12 - (s1 + s2)).abs().max().item() <= 2 * bound
+
+
+@pytest.fixture(params=["tma", "regs"])
+def symv_path(request):
+    """Run a test on both SYMV/HEMV streaming kernels: the TMA-fed
+    warp-specialised pipeline (default) and the register-load kernel."""
+    prev = _lib.set_tma(request.param == "tma")
+    yield request.param
+    _lib.set_tma(prev)
+
+
+class TestSymvBothPaths:
+    @pytest.mark.parametrize("tag", "sdcz")
+    @pytest.mark.parametrize("uplo", "lu")
+    def test_oracle_both_paths(self, symv_path, tag, uplo):
+        rng = np.random.default_rng(121)
+        for d in (1, 31, 64, 129, 700, 1537):
+            for ro in (0, 3):
+                host = np.full((d + ro + 8) * (d + ro), np.nan, dtype=naive.DTYPES[tag])
+                ld = d + ro + 8
+                win = naive.window(host, ld, d + ro, d + ro)
+                vals = naive.fill(rng, (d, d), tag)
+                mask = np.tril(np.ones((d, d), bool)) if uplo == "l" else np.triu(np.ones((d, d), bool))
+                tri = np.where(mask, vals, 0)
+                sub = win[ro:, ro:]
+                sub[mask] = vals[mask]
+                v = kb.MatrixView(torch.from_numpy(host).cuda(), d + ro, d + ro, ld, kb.precision(tag)).submatrix(
+                    ro, ro, d, d)
+                x, y = naive.fill(rng, d, tag), naive.fill(rng, d, tag)
+                rep = kb.symv_hemv(uplo, 0.75, kb.HermitianView(v, uplo), dvec(x), 1.25, dvec(y))
+                assert ("symv_tma" in rep.plan) == (symv_path == "tma" and (ld * v.precision.element_bytes) % 16 == 0)
+                herm = tag in "cz"
+                want = naive.naive_symv_hemv(0.75, tri, uplo, x, 1.25, y, hermitian=herm)
+                got = rep.y_out
+                assert torch.isfinite(got).all()
+                check(got, want, tag, 0.75, np.abs(naive.dense_from_triangle(tri, uplo, herm)), x, 1.25, y)
+
+    def test_paths_agree_and_are_deterministic(self, symv_path):
+        rng = np.random.default_rng(122)
+        v, a = dev_matrix(rng, 5000, 5000, "d")
+        x, y = dvec(naive.fill(rng, 5000, "d")), dvec(naive.fill(rng, 5000, "d"))
+        r1 = kb.symv_hemv("l", 1.0, kb.HermitianView(v, "l"), x, 0.5, y).y_out
+        r2 = kb.symv_hemv("l", 1.0, kb.HermitianView(v, "l"), x, 0.5, y).y_out
+        assert torch.equal(r1, r2)
+        want = streamed.symv("l", 1.0, a, x.cpu().numpy(), 0.5, y.cpu().numpy())
+        check(r1, want, "d", 1.0, np.abs(naive.dense_from_triangle(a, "l", False)), x.cpu().numpy(), 0.5,
+              y.cpu().numpy())
