@@ -384,17 +384,21 @@ int tma_mode() {
   return g_use_tma;
 }
 bool use_tma() { return tma_mode() != 0; }
-// tuned defaults: TMA for s and z (variants 0 / 1), registers for d and c
-template <class T> bool prefer_tma() { return sizeof(T) == 16 || sizeof(T) == 4; }
-template <class T> int default_variant() { return sizeof(T) == 16 ? 1 : 0; }
+// tuned defaults (profiles/r1_tune_symv_v2.jsonl): the software-pipelined
+// register kernel wins for every precision from N ~ 16k up; the TMA kernel
+// wins for z and s at N <= ~8-12k (variant 0 for z, 4 for s)
+template <class T> bool prefer_tma(int d) {
+  return (sizeof(T) == 16 && d <= 12288) || (sizeof(T) == 4 && d <= 8192);
+}
+template <class T> int default_variant() { return sizeof(T) == 16 ? 0 : 4; }
 
 // A00: element (0,0) of the d x d operand (any row alignment); needs a
 // 16-byte multiple column stride.
 template <class T>
-bool tma_ok(const T *A00, long long lda) {
+bool tma_ok(const T *A00, long long lda, int d) {
   const uintptr_t addr = reinterpret_cast<uintptr_t>(A00);
   const int mode = tma_mode();
-  const bool want = mode == 1 || (mode == -1 && prefer_tma<T>());
+  const bool want = mode == 1 || (mode == -1 && prefer_tma<T>(d));
   return want && tensor_map_encoder() != nullptr && (lda * (long long)sizeof(T)) % 16 == 0 &&
          addr % sizeof(T) == 0;
 }
@@ -484,7 +488,7 @@ cudaError_t dispatch_symv_h(bool lower, const Path<T> &pa, long long lda, int d,
                             int ncols_local, T *y, T alpha, T beta, bool beta_zero, cudaStream_t st) {
   using C = Cfg<T>;
   const T *A00 = pa.base + pa.lead;
-  if (tma_ok(A00, lda)) {
+  if (tma_ok(A00, lda, d)) {
 #define KB_TMA(NC, CW, RS, S)                                                                                 \
   return lower ? run_symv_tma<T, NC, CW, RS, S, true, HERM>(A00, lda, d, x, cm, ncols_local, y, alpha, beta,  \
                                                              beta_zero, st)                                  \

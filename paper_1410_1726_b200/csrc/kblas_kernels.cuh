@@ -291,134 +291,153 @@ __global__ void __launch_bounds__(NW * 32, 1) symv_kernel(const SymParams p) {
   griddep_launch_dependents();
   constexpr int NT = NW * 32;
   constexpr int H = 32 * V * R;
-  constexpr int W = NW * CW;
   __shared__ T red[2][NW][H];
-  __shared__ T xs[W];
   const T *__restrict__ A = static_cast<const T *>(p.A);
   const T *__restrict__ x = static_cast<const T *>(p.x);
   T *__restrict__ ws1 = static_cast<T *>(p.ws1);
   T *__restrict__ ws2 = static_cast<T *>(p.ws2);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t pol = policy_evict_first();
-  long long it = sk_start(blockIdx.x, p.total, p.P);
+  const uint64_t keep = policy_evict_last();
+  const long long it0 = sk_start(blockIdx.x, p.total, p.P);
   const long long end = sk_start(blockIdx.x + 1, p.total, p.P);
-  if (it >= end) return;
+  if (it0 >= end) return;
+  const int cl = warp * CW;
 
-  // tile holding item `it`: the last tile whose prefix <= it
+  // tile holding item it0: the last tile whose prefix <= it0
   int k;
   {
     int lo = 0, hi = p.ntiles - 1;
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
-      if (p.tiles[mid].prefix <= it) lo = mid; else hi = mid - 1;
+      if (p.tiles[mid].prefix <= it0) lo = mid; else hi = mid - 1;
     }
     k = lo;
   }
+
+  // Software pipeline over the CTA's items: the loads of item q+1 (possibly
+  // in the next tile) are issued right after item q's FMAs, so they are in
+  // flight while item q's t1 partial goes through shared memory, the
+  // barrier and the fixed-order cross-warp reduction.
+  Pack<T, V> a[CW][R];
+  T xr[R][V];
+  auto load = [&](const SymTile &t, long long q) {
+    const int p0 = (t.chunk0 + (int)(q - t.prefix)) * H;
+    const int vlo = t.row0 + p.lead, vhi = t.row1 + p.lead;
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        const int ps = p0 + r * 32 * V + lane * V + v;
+        xr[r][v] = (ps >= vlo && ps < vhi) ? __ldg(x + (ps - p.lead)) : zero<T>();
+      }
+    const T *Aw = A + (long long)(t.lcol0 + cl) * p.lda;
+#pragma unroll
+    for (int j = 0; j < CW; ++j) {
+      const bool cok = cl + j < t.ncols;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int vs = p0 + r * 32 * V + lane * V;
+        ld_pack(a[j][r], Aw + (long long)j * p.lda + vs, cok && vs < vhi && vs + V > vlo, pol);
+      }
+    }
+  };
+
+  SymTile tl = p.tiles[k];
+  long long tnext = (k + 1 < p.ntiles) ? p.tiles[k + 1].prefix : p.total;
+  T xc[CW], t2[CW];
+#pragma unroll
+  for (int j = 0; j < CW; ++j) {
+    xc[j] = (cl + j < tl.ncols) ? __ldg(x + tl.gcol0 + cl + j) : zero<T>();
+    t2[j] = zero<T>();
+  }
+  load(tl, it0);
   int buf = 0;
-  const int cl = warp * CW;
-  const uint64_t keep = policy_evict_last();
-
-  while (it < end) {
-    const SymTile tl = p.tiles[k];
-    const long long tnext = (k + 1 < p.ntiles) ? p.tiles[k + 1].prefix : p.total;
-    const long long stop = min(end, tnext);
-    __syncthreads();
-    for (int t = threadIdx.x; t < W; t += NT) xs[t] = t < tl.ncols ? __ldg(x + tl.gcol0 + t) : zero<T>();
-    __syncthreads();
-    const T *xc = xs + cl;  // x of this warp's columns (shared-memory broadcast)
-
-    T t2[CW];
+  for (long long q = it0; q < end; ++q) {
+    const int p0 = (tl.chunk0 + (int)(q - tl.prefix)) * H;
+    const int vlo = tl.row0 + p.lead, vhi = tl.row1 + p.lead;
+    const int g0 = p0 - p.lead;  // logical row of the chunk's first physical row
+    T acc[R][V];
 #pragma unroll
-    for (int j = 0; j < CW; ++j) t2[j] = zero<T>();
-    const T *Aw = A + (long long)(tl.lcol0 + cl) * p.lda;
-    const long long vlo = (long long)tl.row0 + p.lead;  // physical stored range
-    const long long vhi = (long long)tl.row1 + p.lead;
-
-    for (long long q = it; q < stop; ++q) {
-      const long long p0 = (long long)(tl.chunk0 + (q - tl.prefix)) * H;
-      T xr[R][V];
-      bool ok[R][V];
+    for (int r = 0; r < R; ++r)
 #pragma unroll
-      for (int r = 0; r < R; ++r)
+      for (int v = 0; v < V; ++v) acc[r][v] = zero<T>();
+    const bool diag = (g0 < tl.gcol0 + tl.ncols) && (g0 + H > tl.gcol0);
+    const bool inside = p0 >= vlo && p0 + H <= vhi;
+    if (!diag && inside) {
 #pragma unroll
-        for (int v = 0; v < V; ++v) {
-          const long long ps = p0 + r * 32 * V + lane * V + v;
-          ok[r][v] = (ps >= vlo) && (ps < vhi);
-          xr[r][v] = ok[r][v] ? __ldg(x + (ps - p.lead)) : zero<T>();
-        }
-      Pack<T, V> a[CW][R];
+      for (int j = 0; j < CW; ++j)
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            const T e = a[j][r].v(v);
+            acc[r][v] = fma_(e, xc[j], acc[r][v]);
+            t2[j] = fmax_<HERM>(e, xr[r][v], t2[j]);
+          }
+    } else {
 #pragma unroll
       for (int j = 0; j < CW; ++j) {
-        const bool cok = cl + j < tl.ncols;
+        const int c = tl.gcol0 + cl + j;
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const long long vs = p0 + r * 32 * V + lane * V;
-          ld_pack(a[j][r], Aw + (long long)j * p.lda + vs, cok && vs < vhi && vs + V > vlo, pol);
-        }
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            const int ps = p0 + r * 32 * V + lane * V + v;
+            const int i = ps - p.lead;
+            const bool ok = ps >= vlo && ps < vhi;
+            const bool in1 = ok && (LOWER ? i >= c : i <= c);
+            const bool in2 = ok && (LOWER ? i > c : i < c);
+            T e1 = sel(in1, a[j][r].v(v));
+            if (HERM && i == c) e1 = realify(e1);
+            acc[r][v] = fma_(e1, xc[j], acc[r][v]);
+            t2[j] = fmax_<HERM>(sel(in2, a[j][r].v(v)), xr[r][v], t2[j]);
+          }
       }
-      T acc[R][V];
-#pragma unroll
-      for (int r = 0; r < R; ++r)
-#pragma unroll
-        for (int v = 0; v < V; ++v) acc[r][v] = zero<T>();
+    }
 
-      const long long g0 = p0 - p.lead;  // logical row of the chunk's first physical row
-      const bool diag = (g0 < (long long)tl.gcol0 + tl.ncols) && (g0 + H > tl.gcol0);
-      if (!diag) {
+    // tile boundary: flush this tile's column sums (t2) once
+    const bool last_of_tile = q + 1 >= tnext || q + 1 >= end;
+    if (last_of_tile) {
+      const long long slot = (long long)blockIdx.x - sk_owner(tl.prefix, p.total, p.P);
 #pragma unroll
-        for (int j = 0; j < CW; ++j)
-#pragma unroll
-          for (int r = 0; r < R; ++r)
-#pragma unroll
-            for (int v = 0; v < V; ++v) {
-              const T e = sel(ok[r][v], a[j][r].v(v));
-              acc[r][v] = fma_(e, xc[j], acc[r][v]);
-              t2[j] = fmax_<HERM>(e, xr[r][v], t2[j]);
-            }
-      } else {
-#pragma unroll
-        for (int j = 0; j < CW; ++j) {
-          const long long c = (long long)tl.gcol0 + cl + j;
-#pragma unroll
-          for (int r = 0; r < R; ++r)
-#pragma unroll
-            for (int v = 0; v < V; ++v) {
-              const long long i = g0 + r * 32 * V + lane * V + v;
-              const bool in1 = ok[r][v] && (LOWER ? i >= c : i <= c);
-              const bool in2 = ok[r][v] && (LOWER ? i > c : i < c);
-              T e1 = sel(in1, a[j][r].v(v));
-              if (HERM && i == c) e1 = realify(e1);
-              acc[r][v] = fma_(e1, xc[j], acc[r][v]);
-              t2[j] = fmax_<HERM>(sel(in2, a[j][r].v(v)), xr[r][v], t2[j]);
-            }
-        }
+      for (int j = 0; j < CW; ++j) {
+        const T sum = warp_sum(t2[j]);
+        if (lane == 0 && cl + j < tl.ncols) ws2[slot * p.ws2_ld + tl.gcol0 + cl + j] = sum;
+        t2[j] = zero<T>();
       }
+    }
+    const SymTile cur = tl;  // the tile this chunk's t1 belongs to
+    const int kcur = k;
+    if (q + 1 < end) {
+      if (q + 1 >= tnext) {
+        ++k;
+        tl = p.tiles[k];
+        tnext = (k + 1 < p.ntiles) ? p.tiles[k + 1].prefix : p.total;
+#pragma unroll
+        for (int j = 0; j < CW; ++j) xc[j] = (cl + j < tl.ncols) ? __ldg(x + tl.gcol0 + cl + j) : zero<T>();
+      }
+      load(tl, q + 1);  // in flight during the reduction below
+    }
 
 #pragma unroll
-      for (int r = 0; r < R; ++r)
+    for (int r = 0; r < R; ++r)
 #pragma unroll
-        for (int v = 0; v < V; ++v) red[buf][warp][r * 32 * V + lane * V + v] = acc[r][v];
-      __syncthreads();
+      for (int v = 0; v < V; ++v) red[buf][warp][r * 32 * V + lane * V + v] = acc[r][v];
+    __syncthreads();
+    {
+      const int clo = cur.row0 + p.lead, chi = cur.row1 + p.lead;
       for (int t = threadIdx.x; t < H; t += NT) {
-        const long long ps = p0 + t;
-        if (ps >= vlo && ps < vhi) {
+        const int ps = p0 + t;
+        if (ps >= clo && ps < chi) {
           T s = red[buf][0][t];
 #pragma unroll
           for (int w = 1; w < NW; ++w) s = add_(s, red[buf][w][t]);
-          st_keep(ws1 + (long long)k * p.ws1_ld + (ps - p.lead), s, keep);
+          st_keep(ws1 + (long long)kcur * p.ws1_ld + (ps - p.lead), s, keep);
         }
       }
-      buf ^= 1;
     }
-
-    const long long slot = (long long)blockIdx.x - sk_owner(tl.prefix, p.total, p.P);
-#pragma unroll
-    for (int j = 0; j < CW; ++j) {
-      const T s = warp_sum(t2[j]);
-      if (lane == 0 && cl + j < tl.ncols) ws2[slot * p.ws2_ld + tl.gcol0 + cl + j] = s;
-    }
-    it = stop;
-    ++k;
+    buf ^= 1;
   }
 }
 
