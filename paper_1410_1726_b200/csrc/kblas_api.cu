@@ -208,7 +208,7 @@ cudaError_t run_gemv_n(const Path<T> &pa, long long lda, int m, int n, const T *
     TimedScope ts(st);
     kfn<<<(unsigned)P, NW * 32, 0, st>>>(p);
   }
-  launch_pdl(gemv_n_epilogue<T>, (unsigned)cdiv(m, 256), 256, st, y, (const T *)ws, (long long)m, m, pa.lead,
+  launch_pdl(gemv_n_epilogue<T, 8>, (unsigned)cdiv(m, 32), 256, st, y, (const T *)ws, (long long)m, m, pa.lead,
              (int)RB, (int)KS, total, (int)P, alpha, beta, (int)beta_zero);
   launched(2);
   char buf[256];
@@ -239,7 +239,7 @@ cudaError_t run_gemv_t(const Path<T> &pa, long long lda, int m, int n, long long
     TimedScope ts(st);
     kfn<<<(unsigned)P, NW * 32, 0, st>>>(p);
   }
-  launch_pdl(gemv_t_epilogue<T>, (unsigned)cdiv(nglob, 256), 256, st, y, (const T *)ws, ws_ld, nglob, (int)CBW,
+  launch_pdl(gemv_t_epilogue<T, 8>, (unsigned)cdiv(nglob, 32), 256, st, y, (const T *)ws, ws_ld, nglob, (int)CBW,
              (int)KS, total, (int)P, cm, alpha, beta, (int)beta_zero);
   launched(2);
   char buf[256];
@@ -347,7 +347,7 @@ cudaError_t run_symv(const Path<T> &pa, long long lda, int d, const T *x, ColMap
     TimedScope ts(st);
     kfn<<<(unsigned)P, NW * 32, 0, st>>>(p);
   }
-  launch_pdl(symv_epilogue<T, LOWER, 8>, (unsigned)cdiv(d, 32), 256, st, y, p, alpha, beta, (int)beta_zero);
+  launch_pdl(symv_epilogue<T, LOWER, 16>, (unsigned)cdiv(d, 32), 512, st, y, p, alpha, beta, (int)beta_zero);
   launched(2);
   char buf[256];
   snprintf(buf, sizeof buf, "symv %s %s %s%s lead=%d d=%d W=%d H=%d tiles=%d items=%lld P=%lld slots=%lld",
@@ -456,7 +456,7 @@ cudaError_t run_symv_tma(const T *A00, long long lda, int d, const T *x, ColMap 
     TimedScope ts(st);
     kfn<<<(unsigned)P, (NC + 2) * 32, smem, st>>>(map, tp);
   }
-  launch_pdl(symv_epilogue<T, LOWER, 8>, (unsigned)cdiv(d, 32), 256, st, y, tp.sp, alpha, beta, (int)beta_zero);
+  launch_pdl(symv_epilogue<T, LOWER, 16>, (unsigned)cdiv(d, 32), 512, st, y, tp.sp, alpha, beta, (int)beta_zero);
   launched(2);
   char buf[256];
   snprintf(buf, sizeof buf, "symv_tma %s %s%s lead=%d d=%d W=%d H=%d S=%d tiles=%d items=%lld P=%lld slots=%lld smem=%zu",

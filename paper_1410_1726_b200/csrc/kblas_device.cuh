@@ -173,6 +173,25 @@ __device__ __forceinline__ void ld_pack(Pack<T, V> &a, const T *p, bool pred, ui
   }
 }
 
+// V consecutive elements of a vector operand (x): cached in L1 (every warp of
+// a CTA reads the same rows) and kept in L2 (every CTA of a column range
+// does).  One 256-bit load when V * sizeof(T) == 32 (p 32-byte aligned).
+template <class T, int V>
+__device__ __forceinline__ void ld_xvec(T (&out)[V], const T *p) {
+  if constexpr (V * sizeof(T) == 32) {
+    Pack<T, V> a;
+    asm("ld.global.nc.L2::evict_last.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=r"(a.w[0]), "=r"(a.w[1]), "=r"(a.w[2]), "=r"(a.w[3]), "=r"(a.w[4]), "=r"(a.w[5]), "=r"(a.w[6]),
+          "=r"(a.w[7])
+        : "l"(p));
+#pragma unroll
+    for (int v = 0; v < V; ++v) out[v] = a.v(v);
+  } else {
+#pragma unroll
+    for (int v = 0; v < V; ++v) out[v] = __ldg(p + v);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // stream-K split: `total` equal work items over P CTAs; CTA c owns
 // [sk_start(c), sk_start(c+1)).  sk_owner(i) is the CTA owning item i.

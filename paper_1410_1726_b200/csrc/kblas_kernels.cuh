@@ -165,6 +165,8 @@ __global__ void __launch_bounds__(NW * 32) gemv_t_kernel(const GemvParams p) {
   long long it = sk_start(blockIdx.x, p.total, p.P);
   const long long end = sk_start(blockIdx.x + 1, p.total, p.P);
   const long long plimit = (long long)p.lead + p.m;
+  // x rows can be fetched as whole vectors when they share A's alignment
+  const bool xvec = V > 1 && p.lead == 0 && (reinterpret_cast<uintptr_t>(x) % (V * sizeof(T))) == 0;
 
   while (it < end) {
     const long long cb = it / p.KS;
@@ -182,12 +184,18 @@ __global__ void __launch_bounds__(NW * 32) gemv_t_kernel(const GemvParams p) {
     auto load = [&](long long q, Pack<T, V> (&a)[CW][R], T (&xr)[R][V]) {
       const long long p0 = (q - cb_first) * H;
 #pragma unroll
-      for (int r = 0; r < R; ++r)
+      for (int r = 0; r < R; ++r) {
+        const long long i0 = p0 + r * 32 * V + lane * V - p.lead;
+        if (xvec && i0 + V <= p.m) {
+          ld_xvec<T, V>(xr[r], x + i0);
+        } else {
 #pragma unroll
-        for (int v = 0; v < V; ++v) {
-          const long long i = p0 + r * 32 * V + lane * V + v - p.lead;
-          xr[r][v] = (i >= 0 && i < p.m) ? __ldg(x + i) : zero<T>();
+          for (int v = 0; v < V; ++v) {
+            const long long i = i0 + v;
+            xr[r][v] = (i >= 0 && i < p.m) ? __ldg(x + i) : zero<T>();
+          }
         }
+      }
 #pragma unroll
       for (int j = 0; j < CW; ++j) {
         const bool cok = col0 + j < p.n;
@@ -303,6 +311,7 @@ __global__ void __launch_bounds__(NW * 32, 1) symv_kernel(const SymParams p) {
   const long long end = sk_start(blockIdx.x + 1, p.total, p.P);
   if (it0 >= end) return;
   const int cl = warp * CW;
+  const bool xvec = V > 1 && p.lead == 0 && (reinterpret_cast<uintptr_t>(x) % (V * sizeof(T))) == 0;
 
   // tile holding item it0: the last tile whose prefix <= it0
   int k;
@@ -325,12 +334,18 @@ __global__ void __launch_bounds__(NW * 32, 1) symv_kernel(const SymParams p) {
     const int p0 = (t.chunk0 + (int)(q - t.prefix)) * H;
     const int vlo = t.row0 + p.lead, vhi = t.row1 + p.lead;
 #pragma unroll
-    for (int r = 0; r < R; ++r)
+    for (int r = 0; r < R; ++r) {
+      const int ps0 = p0 + r * 32 * V + lane * V;
+      if (xvec && ps0 >= vlo && ps0 + V <= vhi) {
+        ld_xvec<T, V>(xr[r], x + ps0);
+      } else {
 #pragma unroll
-      for (int v = 0; v < V; ++v) {
-        const int ps = p0 + r * 32 * V + lane * V + v;
-        xr[r][v] = (ps >= vlo && ps < vhi) ? __ldg(x + (ps - p.lead)) : zero<T>();
+        for (int v = 0; v < V; ++v) {
+          const int ps = ps0 + v;
+          xr[r][v] = (ps >= vlo && ps < vhi) ? __ldg(x + (ps - p.lead)) : zero<T>();
+        }
       }
+    }
     const T *Aw = A + (long long)(t.lcol0 + cl) * p.lda;
 #pragma unroll
     for (int j = 0; j < CW; ++j) {
@@ -375,6 +390,22 @@ __global__ void __launch_bounds__(NW * 32, 1) symv_kernel(const SymParams p) {
             acc[r][v] = fma_(e, xc[j], acc[r][v]);
             t2[j] = fmax_<HERM>(e, xr[r][v], t2[j]);
           }
+    } else if (!diag) {
+      // first/last chunk of a tile: rows outside the stored range are masked
+      // (x is already zero there, so only t1 needs the select)
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          const int ps = p0 + r * 32 * V + lane * V + v;
+          const bool ok = ps >= vlo && ps < vhi;
+#pragma unroll
+          for (int j = 0; j < CW; ++j) {
+            const T e = sel(ok, a[j][r].v(v));
+            acc[r][v] = fma_(e, xc[j], acc[r][v]);
+            t2[j] = fmax_<HERM>(e, xr[r][v], t2[j]);
+          }
+        }
     } else {
 #pragma unroll
       for (int j = 0; j < CW; ++j) {
@@ -452,38 +483,68 @@ __device__ __forceinline__ void store_axpby(T *y, long long i, T alpha, T s, T b
   y[i] = r;
 }
 
-template <class T>
-__global__ void gemv_n_epilogue(T *y, const T *__restrict__ ws, long long ws_ld, int m, int lead,
-                                int RB, int KS, long long total, int P, T alpha, T beta,
-                                int beta_zero) {
+// GEMV epilogues: one CTA per 32 outputs (lane = output), the EW warps split
+// the output's slot range into EW fixed contiguous parts (deterministic),
+// warp 0 adds the parts in order.
+template <class T, int EW>
+__device__ __forceinline__ T slot_sum(const T *__restrict__ ws, long long ws_ld, long long idx, int nslots,
+                                      bool valid, T (*part)[32]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int len = valid ? nslots : 0;
+  const int s0 = (int)((long long)len * warp / EW), s1 = (int)((long long)len * (warp + 1) / EW);
+  T a0 = zero<T>(), a1 = zero<T>();
+  int sl = s0;
+  for (; sl + 2 <= s1; sl += 2) {
+    a0 = add_(a0, ws[sl * ws_ld + idx]);
+    a1 = add_(a1, ws[(sl + 1) * ws_ld + idx]);
+  }
+  if (sl < s1) a0 = add_(a0, ws[sl * ws_ld + idx]);
+  part[warp][lane] = add_(a0, a1);
+  __syncthreads();
+  T s = part[0][lane];
+#pragma unroll
+  for (int w = 1; w < EW; ++w) s = add_(s, part[w][lane]);
+  return s;
+}
+
+template <class T, int EW>
+__global__ void __launch_bounds__(EW * 32) gemv_n_epilogue(T *y, const T *__restrict__ ws, long long ws_ld, int m,
+                                                          int lead, int RB, int KS, long long total, int P,
+                                                          T alpha, T beta, int beta_zero) {
   griddep_wait();
-  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= m) return;
-  const long long rb = (i + lead) / RB;
-  const int first = sk_owner(rb * KS, total, P);
-  const int last = sk_owner(rb * KS + KS - 1, total, P);
-  T s = ws[i];
-  for (int sl = 1; sl <= last - first; ++sl) s = add_(s, ws[sl * ws_ld + i]);
-  store_axpby(y, i, alpha, s, beta, beta_zero);
+  __shared__ T part[EW][32];
+  const long long i = (long long)blockIdx.x * 32 + (threadIdx.x & 31);
+  const bool valid = i < m;
+  int nslots = 0;
+  if (valid) {
+    const long long rb = (i + lead) / RB;
+    nslots = sk_owner(rb * KS + KS - 1, total, P) - sk_owner(rb * KS, total, P) + 1;
+  }
+  const T s = slot_sum<T, EW>(ws, ws_ld, valid ? i : 0, nslots, valid, part);
+  if ((threadIdx.x >> 5) == 0 && valid) store_axpby(y, i, alpha, s, beta, beta_zero);
 }
 
 // y indexed by global column c in [0, nglob); columns not owned by this GPU
 // (mgpu partial mode) are written as zero.
-template <class T>
-__global__ void gemv_t_epilogue(T *y, const T *__restrict__ ws, long long ws_ld, long long nglob,
-                                int CBW, int KS, long long total, int P, ColMap cm, T alpha, T beta,
-                                int beta_zero) {
+template <class T, int EW>
+__global__ void __launch_bounds__(EW * 32) gemv_t_epilogue(T *y, const T *__restrict__ ws, long long ws_ld,
+                                                          long long nglob, int CBW, int KS, long long total, int P,
+                                                          ColMap cm, T alpha, T beta, int beta_zero) {
   griddep_wait();
-  const long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= nglob) return;
-  const long long l = unmap_col(cm, c);
-  if (l < 0) { y[c] = zero<T>(); return; }
-  const long long cb = l / CBW;
-  const int first = sk_owner(cb * KS, total, P);
-  const int last = sk_owner(cb * KS + KS - 1, total, P);
-  T s = ws[l];
-  for (int sl = 1; sl <= last - first; ++sl) s = add_(s, ws[sl * ws_ld + l]);
-  store_axpby(y, c, alpha, s, beta, beta_zero);
+  __shared__ T part[EW][32];
+  const long long c = (long long)blockIdx.x * 32 + (threadIdx.x & 31);
+  const long long l = c < nglob ? unmap_col(cm, c) : -1;
+  const bool valid = l >= 0;
+  int nslots = 0;
+  if (valid) {
+    const long long cb = l / CBW;
+    nslots = sk_owner(cb * KS + KS - 1, total, P) - sk_owner(cb * KS, total, P) + 1;
+  }
+  const T s = slot_sum<T, EW>(ws, ws_ld, valid ? l : 0, nslots, valid, part);
+  if ((threadIdx.x >> 5) == 0 && c < nglob) {
+    if (valid) store_axpby(y, c, alpha, s, beta, beta_zero);
+    else y[c] = zero<T>();
+  }
 }
 
 // One CTA per 32 rows (lane = row).  The t1 partials of a row are spread
@@ -518,16 +579,21 @@ __global__ void __launch_bounds__(EW * 32) symv_epilogue(T *y, const SymParams p
   }
   const int len = valid ? ke - kb : 0;
   const int k0 = kb + (int)((long long)len * warp / EW), k1 = kb + (int)((long long)len * (warp + 1) / EW);
-  T s0 = zero<T>(), s1 = zero<T>(), s2 = zero<T>(), s3 = zero<T>();
+  // eight independent loads in flight per lane; fixed combination order
+  T acc[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) acc[u] = zero<T>();
   int k = k0;
-  for (; k + 4 <= k1; k += 4) {
-    s0 = add_(s0, ws1[(long long)k * p.ws1_ld + i]);
-    s1 = add_(s1, ws1[(long long)(k + 1) * p.ws1_ld + i]);
-    s2 = add_(s2, ws1[(long long)(k + 2) * p.ws1_ld + i]);
-    s3 = add_(s3, ws1[(long long)(k + 3) * p.ws1_ld + i]);
+  for (; k + 8 <= k1; k += 8) {
+    T t[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) t[u] = ws1[(long long)(k + u) * p.ws1_ld + i];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc[u] = add_(acc[u], t[u]);
   }
-  for (; k < k1; ++k) s0 = add_(s0, ws1[(long long)k * p.ws1_ld + i]);
-  part[warp][lane] = add_(add_(s0, s1), add_(s2, s3));
+  for (; k < k1; ++k) acc[0] = add_(acc[0], ws1[(long long)k * p.ws1_ld + i]);
+  part[warp][lane] = add_(add_(add_(acc[0], acc[1]), add_(acc[2], acc[3])),
+                          add_(add_(acc[4], acc[5]), add_(acc[6], acc[7])));
   __syncthreads();
   if (warp != 0 || !valid) return;
   T s = part[0][lane];

@@ -5,10 +5,12 @@ called through ctypes on the same buffers) as the library comparator.
 
     python scripts/sweep.py [--ops dsymv,zhemv,...] [--sizes 1024,...] [--out FILE]
 
-Timing: CUDA events per call; matrices smaller than 512 MB are timed one
-call at a time with a 512 MB L2 flush (memset) between calls, larger ones
-back-to-back (they exceed the 126 MB L2 by >4x).  Median of the timed
-calls.  GB/s uses the algorithmic bytes (roofline.py / SURVEY §8d).
+Timing: CUDA events around back-to-back calls (throughput).  Operands
+smaller than 512 MB are replicated and the calls rotate over the copies,
+so every call streams its matrix from HBM (the copies together exceed the
+126 MB L2 by >4x).  `single_ms` is the median single-call time after a
+512 MB L2 flush (latency, launch included).  GB/s uses the algorithmic
+bytes (roofline.py / SURVEY §8d).
 """
 
 from __future__ import annotations
@@ -73,27 +75,34 @@ class Cublas:
         return rc == 0
 
 
-def measure(fn, nbytes_matrix, reps, flush):
-    times = []
+def measure(fn, reps, ncopies):
+    """Back-to-back calls (throughput); fn(k) uses operand copy k % ncopies so
+    the operands streamed per window exceed the L2 several times over."""
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    for _ in range(3):
-        fn()
+    for k in range(3):
+        fn(k % ncopies)
     torch.cuda.synchronize()
-    if nbytes_matrix < (512 << 20):
-        for _ in range(reps):
-            flush.zero_()
-            e0.record()
-            fn()
-            e1.record()
-            torch.cuda.synchronize()
-            times.append(e0.elapsed_time(e1))
-        return statistics.median(times)
+    calls = max(reps, ncopies)
     e0.record()
-    for _ in range(reps):
-        fn()
+    for k in range(calls):
+        fn(k % ncopies)
     e1.record()
     torch.cuda.synchronize()
-    return e0.elapsed_time(e1) / reps
+    return e0.elapsed_time(e1) / calls
+
+
+def measure_single(fn, reps, flush):
+    """One call at a time after a 512 MB L2 flush (single-call latency)."""
+    times = []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for _ in range(min(reps, 10)):
+        flush.zero_()
+        e0.record()
+        fn(0)
+        e1.record()
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1))
+    return statistics.median(times)
 
 
 def main():
@@ -120,8 +129,13 @@ def main():
             ld = -(-m // 32) * 32
             if n * ld * p.element_bytes > args.max_gb * 1e9:
                 continue
-            A = torch.empty(n, ld, dtype=p.torch_dtype, device=dev)
-            (torch.view_as_real(A) if p.is_complex else A).uniform_(-1, 1)
+            mat_alloc = n * ld * p.element_bytes
+            ncop = max(1, min(64, -(-(512 << 20) // mat_alloc)))
+            As = []
+            for _ in range(ncop):
+                A = torch.empty(n, ld, dtype=p.torch_dtype, device=dev)
+                (torch.view_as_real(A) if p.is_complex else A).uniform_(-1, 1)
+                As.append(A)
             x = torch.empty(n, dtype=p.torch_dtype, device=dev)
             y = torch.empty(n, dtype=p.torch_dtype, device=dev)
             (torch.view_as_real(x) if p.is_complex else x).uniform_(-1, 1)
@@ -131,30 +145,32 @@ def main():
                 name = {("s", False): "ssymv", ("d", False): "dsymv", ("c", True): "chemv", ("z", True): "zhemv"}[(tag, herm)]
                 f = getattr(lib, f"kblas_{name}_async")
 
-                def ours():
-                    assert f(op.encode(), n, one, A.data_ptr(), ld, x.data_ptr(), 1, zero, y.data_ptr(), 1, sh) == 0
+                def ours(k):
+                    assert f(op.encode(), n, one, As[k].data_ptr(), ld, x.data_ptr(), 1, zero, y.data_ptr(), 1, sh) == 0
             else:
                 f = getattr(lib, f"kblas_{tag}gemv_async")
 
-                def ours():
-                    assert f(op.encode(), m, n, one, A.data_ptr(), ld, x.data_ptr(), 1, zero, y.data_ptr(), 1, sh) == 0
+                def ours(k):
+                    assert f(op.encode(), m, n, one, As[k].data_ptr(), ld, x.data_ptr(), 1, zero, y.data_ptr(), 1, sh) == 0
 
             nbytes = alg_bytes(tag, family, m, n, op)
-            mat_bytes = n * ld * p.element_bytes if family == "gemv" else n * (n + 1) // 2 * p.element_bytes
-            ms = measure(ours, mat_bytes, args.reps, flush)
+            ms = measure(ours, args.reps, ncop)
+            sms = measure_single(ours, args.reps, flush)
             plan = _lib.last_plan()
             row = {"op": opname, "n": n, "ms": round(ms, 5), "gbs": round(nbytes / ms / 1e6, 1),
-                   "pct_peak": round(100 * nbytes / ms / 1e6 / PEAK, 1), "plan": plan}
+                   "pct_peak": round(100 * nbytes / ms / 1e6 / PEAK, 1), "single_ms": round(sms, 5),
+                   "single_gbs": round(nbytes / sms / 1e6, 1), "copies": ncop, "plan": plan}
             if cub is not None and cub.lib is not None:
                 y2 = torch.empty_like(y)
 
-                def theirs():
-                    cub.call(tag, family, op, herm, m, n, A.data_ptr(), ld, x.data_ptr(), y2.data_ptr(), sh)
+                def theirs(k):
+                    cub.call(tag, family, op, herm, m, n, As[k].data_ptr(), ld, x.data_ptr(), y2.data_ptr(), sh)
 
-                if cub.call(tag, family, op, herm, m, n, A.data_ptr(), ld, x.data_ptr(), y2.data_ptr(), sh):
-                    cms = measure(theirs, mat_bytes, args.reps, flush)
+                if cub.call(tag, family, op, herm, m, n, As[0].data_ptr(), ld, x.data_ptr(), y2.data_ptr(), sh):
+                    cms = measure(theirs, args.reps, ncop)
                     row["cublas_gbs"] = round(nbytes / cms / 1e6, 1)
                     row["speedup_vs_cublas"] = round(cms / ms, 3)
+                    ours(0)
                     scale = float((y2.abs().max()).item()) or 1.0
                     row["rel_diff_vs_cublas"] = float(((y - y2).abs().max() / scale).item())
             rows.append(row)
@@ -163,7 +179,7 @@ def main():
             if out:
                 out.write(line + "\n")
                 out.flush()
-            del A, x, y
+            del As, x, y
             torch.cuda.empty_cache()
     if out:
         out.close()
