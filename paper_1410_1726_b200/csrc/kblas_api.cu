@@ -342,7 +342,7 @@ cudaError_t run_symv(const Path<T> &pa, long long lda, int d, const T *x, ColMap
   e = workspace(b1 + b2, st, &ws);
   if (e != cudaSuccess) return e;
   SymParams p{pa.base, lda, d, pa.lead, x, ws, (long long)d, (char *)ws + b1, (long long)d,
-              tt.dev, tt.ntiles, tt.total, (int)P};
+              tt.dev, tt.ntiles, tt.total, (int)P, (cm.G == 1 && cm.nb >= d) ? W : 0};
   {
     TimedScope ts(st);
     kfn<<<(unsigned)P, NW * 32, 0, st>>>(p);
@@ -450,7 +450,7 @@ cudaError_t run_symv_tma(const T *A00, long long lda, int d, const T *x, ColMap 
   if (e != cudaSuccess) return e;
   SymTmaParams tp;
   tp.sp = SymParams{base, lda, d, lead, x, ws, (long long)d, (char *)ws + b1, (long long)d,
-                    tt.dev, tt.ntiles, tt.total, (int)P};
+                    tt.dev, tt.ntiles, tt.total, (int)P, (cm.G == 1 && cm.nb >= d) ? W : 0};
   tp.unit_per_elem = upe;
   {
     TimedScope ts(st);

@@ -292,6 +292,7 @@ struct SymParams {
   int ntiles;
   long long total;
   int P;
+  int tile_w;  // > 0: tiles are uniform, tile k = columns [k*tile_w, (k+1)*tile_w) (single GPU)
 };
 
 template <class T, int V, int NW, int CW, int R, bool LOWER, bool HERM>
@@ -557,41 +558,46 @@ __global__ void __launch_bounds__(EW * 32) symv_epilogue(T *y, const SymParams p
   griddep_wait();
   __shared__ T part[EW][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const long long i = (long long)blockIdx.x * 32 + lane;
-  const bool valid = i < p.d;
+  const long long i = min((long long)blockIdx.x * 32 + lane, (long long)p.d - 1);
+  const bool valid = (long long)blockIdx.x * 32 + lane < p.d;
   const T *__restrict__ ws1 = static_cast<const T *>(p.ws1);
   const T *__restrict__ ws2 = static_cast<const T *>(p.ws2);
   // nle = number of tiles with gcol0 <= i (tiles sorted by gcol0)
-  int lo = 0, hi = p.ntiles;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (p.tiles[mid].gcol0 <= i) lo = mid + 1; else hi = mid;
+  int nle;
+  if (p.tile_w > 0) {
+    nle = min(p.ntiles, (int)(i / p.tile_w) + 1);
+  } else {
+    int lo = 0, hi = p.ntiles;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (p.tiles[mid].gcol0 <= i) lo = mid + 1; else hi = mid;
+    }
+    nle = lo;
   }
-  const int nle = lo;
   int kb, ke;
   if (LOWER) {
     kb = 0;
     ke = nle;
   } else {
     kb = nle;
-    if (nle > 0 && p.tiles[nle - 1].gcol0 + p.tiles[nle - 1].ncols > i) kb = nle - 1;
+    if (nle > 0 && (p.tile_w > 0 || p.tiles[nle - 1].gcol0 + p.tiles[nle - 1].ncols > i)) kb = nle - 1;
     ke = p.ntiles;
   }
-  const int len = valid ? ke - kb : 0;
-  const int k0 = kb + (int)((long long)len * warp / EW), k1 = kb + (int)((long long)len * (warp + 1) / EW);
-  // eight independent loads in flight per lane; fixed combination order
+  // warp w takes tiles kb+w, kb+w+EW, ... (a fixed partition: the summation
+  // order depends only on the row); eight loads in flight per lane
+  if (!valid) ke = kb;
   T acc[8];
 #pragma unroll
   for (int u = 0; u < 8; ++u) acc[u] = zero<T>();
-  int k = k0;
-  for (; k + 8 <= k1; k += 8) {
+  int k = kb + warp;
+  for (; k + 7 * EW < ke; k += 8 * EW) {
     T t[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) t[u] = ws1[(long long)(k + u) * p.ws1_ld + i];
+    for (int u = 0; u < 8; ++u) t[u] = ws1[(long long)(k + u * EW) * p.ws1_ld + i];
 #pragma unroll
     for (int u = 0; u < 8; ++u) acc[u] = add_(acc[u], t[u]);
   }
-  for (; k < k1; ++k) acc[0] = add_(acc[0], ws1[(long long)k * p.ws1_ld + i]);
+  for (; k < ke; k += EW) acc[0] = add_(acc[0], ws1[(long long)k * p.ws1_ld + i]);
   part[warp][lane] = add_(add_(add_(acc[0], acc[1]), add_(acc[2], acc[3])),
                           add_(add_(acc[4], acc[5]), add_(acc[6], acc[7])));
   __syncthreads();
