@@ -36,6 +36,53 @@ def stream_handle(device) -> int:
     return torch.cuda.current_stream(device).cuda_stream
 
 
+class _on_device:
+    """`torch.cuda.device(d)` only when d is not already current (saves the
+    context switch on the common path)."""
+
+    __slots__ = ("dev", "prev")
+
+    def __init__(self, dev):
+        self.dev = dev.index if isinstance(dev, torch.device) else dev
+        self.prev = None
+
+    def __enter__(self):
+        cur = torch.cuda.current_device()
+        if self.dev is not None and cur != self.dev:
+            self.prev = cur
+            torch.cuda.set_device(self.dev)
+
+    def __exit__(self, *exc):
+        if self.prev is not None:
+            torch.cuda.set_device(self.prev)
+
+
+def length_of(v) -> int:
+    if _is_torch(v):
+        return v.numel() if v.dim() == 1 else -1
+    a = np.asarray(v)
+    return a.size if a.ndim == 1 else -1
+
+
+def output_vector(y_in, length: int, prec: Precision, device, beta_zero: bool, inplace: bool) -> torch.Tensor:
+    """The buffer the kernels update: y itself (inplace), a fresh empty vector
+    when beta == 0 (y is never read, so it is not even uploaded), else a
+    private device copy of y."""
+    if inplace:
+        if not (_is_torch(y_in) and y_in.is_cuda and y_in.dim() == 1 and y_in.numel() == length
+                and y_in.dtype == prec.torch_dtype and y_in.is_contiguous()):
+            raise ValueError("inplace=True needs y to be a contiguous CUDA tensor of the operand dtype")
+        return y_in
+    if beta_zero:
+        if length_of(y_in) != length:
+            raise ValueError(f"y must be a vector of length {length}")
+        return torch.empty(length, dtype=prec.torch_dtype, device=device)
+    yd = vector_in(y_in, length, prec, "y", device)
+    if _is_torch(y_in) and yd.data_ptr() == y_in.data_ptr():
+        return yd.clone()
+    return yd
+
+
 def vector_in(v, length: int, prec: Precision, name: str, device) -> torch.Tensor:
     """1-D operand of the precision's dtype on `device` (kernels.py:395-399)."""
     if _is_torch(v):
@@ -47,19 +94,6 @@ def vector_in(v, length: int, prec: Precision, name: str, device) -> torch.Tenso
         raise ValueError(f"{name} must be a vector of length {length}")
     t = torch.from_numpy(np.ascontiguousarray(arr))
     return t.to(device, non_blocking=t.is_pinned())
-
-
-def output_like(y_in, y_dev: torch.Tensor, beta_zero: bool, inplace: bool) -> torch.Tensor:
-    """Buffer the kernel updates in place.  beta == 0 never reads y."""
-    if inplace:
-        if not (_is_torch(y_in) and y_in.is_cuda and y_in.is_contiguous() and y_dev.data_ptr() == y_in.data_ptr()):
-            raise ValueError("inplace=True needs y to be a contiguous CUDA tensor of the operand dtype")
-        return y_in
-    if beta_zero:
-        return torch.empty_like(y_dev)
-    if _is_torch(y_in) and y_dev.data_ptr() == y_in.data_ptr():
-        return y_dev.clone()
-    return y_dev  # already a private copy
 
 
 def result_like(y_in, y_out: torch.Tensor):
@@ -88,7 +122,7 @@ def matrix_in(view: MatrixView, device, lower_tri: str | None = None):
     st = stream_handle(device)
     hptr, dptr = src.ctypes.data, dev.data_ptr()
     r0 = view.row_offset
-    with torch.cuda.device(device):
+    with _on_device(device):
         if lower_tri is None:
             blocks = [(0, nc, 0, ld)]
         else:
@@ -108,11 +142,20 @@ def matrix_in(view: MatrixView, device, lower_tri: str | None = None):
     return dev.data_ptr() + view.row_offset * esize, ld, dev
 
 
+_FN_CACHE: dict = {}
+
+
+def _fn(name: str):
+    f = _FN_CACHE.get(name)
+    if f is None:
+        f = _FN_CACHE[name] = getattr(_lib.load(), name)
+    return f
+
+
 def call_gemv(prec: Precision, trans: str, m: int, n: int, alpha, a_ptr: int, lda: int,
               x: torch.Tensor, beta, y: torch.Tensor, device, off_r: int = 0, off_c: int = 0):
-    lib = _lib.load()
-    f = getattr(lib, f"kblas_{prec.tag}gemv_offset_async")
-    with torch.cuda.device(device):
+    f = _fn(f"kblas_{prec.tag}gemv_offset_async")
+    with _on_device(device):
         rc = f(trans.encode(), m, n, _lib.scalar(prec.tag, alpha), a_ptr, lda, x.data_ptr(), 1,
                _lib.scalar(prec.tag, beta), y.data_ptr(), 1, off_r, off_c, stream_handle(device))
     _lib.check(rc, f"kblas_{prec.tag}gemv_offset",
@@ -122,10 +165,9 @@ def call_gemv(prec: Precision, trans: str, m: int, n: int, alpha, a_ptr: int, ld
 def call_symv(prec: Precision, hermitian: bool, uplo: str, d: int, alpha, a_ptr: int, lda: int,
               x: torch.Tensor, beta, y: torch.Tensor, device, offset: int = 0):
     """offset: the (offset, offset) diagonal position of the d x d operand from a_ptr."""
-    lib = _lib.load()
     name = SYMV_FN[(prec.tag, bool(hermitian))]
-    f = getattr(lib, f"kblas_{name}_offset_async")
-    with torch.cuda.device(device):
+    f = _fn(f"kblas_{name}_offset_async")
+    with _on_device(device):
         rc = f(uplo.encode(), d, _lib.scalar(prec.tag, alpha), a_ptr, lda, x.data_ptr(), 1,
                _lib.scalar(prec.tag, beta), y.data_ptr(), 1, offset, stream_handle(device))
     _lib.check(rc, f"kblas_{name}_offset",

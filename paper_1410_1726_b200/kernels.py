@@ -129,12 +129,12 @@ def gemv(trans: str, alpha, a: MatrixView, x, beta, y, config: KernelConfig = DE
     x_len, y_len = (a.cols, a.rows) if trans == "n" else (a.rows, a.cols)
     dev = _ops.device_for(a, y, x)
     xd = _ops.vector_in(x, x_len, prec, "x", dev)
-    yd = _ops.vector_in(y, y_len, prec, "y", dev)
     if _is_zero(alpha) and _is_one(beta):
+        yd = _ops.vector_in(y, y_len, prec, "y", dev)
         out = yd if inplace else yd.clone()
         return ExecutionReport(y_out=_ops.result_like(y, out))
     bz = _is_zero(beta)
-    out = _ops.output_like(y, yd, bz, inplace)
+    out = _ops.output_vector(y, y_len, prec, dev, bz, inplace)
     if _is_zero(alpha):
         _ops.call_gemv(prec, trans, a.rows, a.cols, alpha, 0, max(1, a.rows), xd, beta, out, dev)
         rep = _scal_report(prec, y_len, bz)
@@ -170,12 +170,12 @@ def symv_hemv(uplo: str, alpha, a: HermitianView, x, beta, y, config: KernelConf
     d = a.dim
     dev = _ops.device_for(a.base, y, x)
     xd = _ops.vector_in(x, d, prec, "x", dev)
-    yd = _ops.vector_in(y, d, prec, "y", dev)
     if _is_zero(alpha) and _is_one(beta):
+        yd = _ops.vector_in(y, d, prec, "y", dev)
         out = yd if inplace else yd.clone()
         return ExecutionReport(y_out=_ops.result_like(y, out))
     bz = _is_zero(beta)
-    out = _ops.output_like(y, yd, bz, inplace)
+    out = _ops.output_vector(y, d, prec, dev, bz, inplace)
     if _is_zero(alpha):
         _ops.call_symv(prec, hermitian, uplo, d, alpha, 0, max(1, d), xd, beta, out, dev)
         rep = _scal_report(prec, d, bz)

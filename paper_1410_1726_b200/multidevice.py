@@ -159,7 +159,7 @@ def partial_mv(prec: Precision, kind: str, op: str, m: int, n: int, alpha, local
         a_ptr = local.data.data_ptr() + local.linear_index(0, 0) * prec.element_bytes
         lda = local.ld
     al = _lib.scalar(prec.tag, alpha)
-    with torch.cuda.device(dev):
+    with _ops._on_device(dev):
         rc = lib.kblas_mv_mgpu_partial_async(
             prec.tag.encode(), kind.encode(), op.encode(), m, n, ctypes.cast(ctypes.byref(al), ctypes.c_void_p),
             a_ptr, lda, x.data_ptr(), out.data_ptr(), device_count, device_index, nb, 1 if hermitian else 0,

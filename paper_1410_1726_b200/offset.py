@@ -83,13 +83,12 @@ def gemv_offset(trans: str, alpha, req: OffsetRequest, x, beta, y,
     dev = _ops.device_for(parent, y, x)
     try:
         xd = _ops.vector_in(x, x_len, prec, "x", dev)
-        yd = _ops.vector_in(y, y_len, prec, "y", dev)
+        bz = _is_zero(beta)
+        if _is_zero(alpha) and _is_one(beta):
+            return ExecutionReport(y_out=_ops.result_like(y, _ops.vector_in(y, y_len, prec, "y", dev).clone()))
+        out = _ops.output_vector(y, y_len, prec, dev, bz, False)
     except ValueError:
         raise ValueError(f"expected x of length {x_len} and y of length {y_len}")
-    if _is_zero(alpha) and _is_one(beta):
-        return ExecutionReport(y_out=_ops.result_like(y, yd.clone()))
-    bz = _is_zero(beta)
-    out = _ops.output_like(y, yd, bz, False)
     if _is_zero(alpha):
         _ops.call_gemv(prec, trans, req.sub_m, req.sub_n, alpha, 0, max(1, req.sub_m), xd, beta, out, dev)
         rep = _scal_report(prec, y_len, bz)
@@ -125,13 +124,12 @@ def symv_hemv_offset(uplo: str, alpha, parent: HermitianView, offset: int, sub_d
     dev = _ops.device_for(parent.base, y, x)
     try:
         xd = _ops.vector_in(x, sub_d, prec, "x", dev)
-        yd = _ops.vector_in(y, sub_d, prec, "y", dev)
+        bz = _is_zero(beta)
+        if _is_zero(alpha) and _is_one(beta):
+            return ExecutionReport(y_out=_ops.result_like(y, _ops.vector_in(y, sub_d, prec, "y", dev).clone()))
+        out = _ops.output_vector(y, sub_d, prec, dev, bz, False)
     except ValueError:
         raise ValueError(f"expected x and y of length {sub_d}")
-    if _is_zero(alpha) and _is_one(beta):
-        return ExecutionReport(y_out=_ops.result_like(y, yd.clone()))
-    bz = _is_zero(beta)
-    out = _ops.output_like(y, yd, bz, False)
     if _is_zero(alpha):
         _ops.call_symv(prec, hermitian, uplo, sub_d, alpha, 0, max(1, sub_d), xd, beta, out, dev)
         rep = _scal_report(prec, sub_d, bz)
