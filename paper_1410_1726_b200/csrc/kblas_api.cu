@@ -117,7 +117,37 @@ cudaError_t workspace(size_t bytes, cudaStream_t st, void **out) {
   return cudaSuccess;
 }
 
+// Arrival counters for the fused GEMV epilogue: one per row/column block,
+// zero between calls (the finishing CTA resets its counter), zeroed when
+// (re)allocated.  Cached per (device, stream) like the workspace.
+std::map<std::pair<int, cudaStream_t>, WsBuf> g_cnt;
+
+cudaError_t counters(size_t n, cudaStream_t st, unsigned **out) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_mu);
+  WsBuf &b = g_cnt[{dev, st}];
+  const size_t bytes = std::max<size_t>(n, 1024) * sizeof(unsigned);
+  if (b.bytes < bytes) {
+    if (b.ptr) {
+      cudaStreamSynchronize(st);
+      cudaFree(b.ptr);
+      b.ptr = nullptr;
+      b.bytes = 0;
+    }
+    const size_t want = bytes * 2;
+    cudaError_t e = cudaMalloc(&b.ptr, want);
+    if (e != cudaSuccess) { b.ptr = nullptr; return e; }
+    e = cudaMemsetAsync(b.ptr, 0, want, st);
+    if (e != cudaSuccess) return e;
+    b.bytes = want;
+  }
+  *out = static_cast<unsigned *>(b.ptr);
+  return cudaSuccess;
+}
+
 inline long long cdiv(long long a, long long b) { return (a + b - 1) / b; }
+constexpr long long kFuseMaxSlots = 8;
 inline size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
 
 // ------------------------------------------------------------ scalar utils
@@ -132,6 +162,11 @@ template <> bool is_one(double v) { return v == 1.0; }
 template <> bool is_one(float2 v) { return v.x == 1.f && v.y == 0.f; }
 template <> bool is_one(double2 v) { return v.x == 1.0 && v.y == 0.0; }
 template <class T> constexpr bool is_cplx() { return Elem<T>::cplx; }
+inline double2 widen(float v) { return make_double2(v, 0.0); }
+inline double2 widen(double v) { return make_double2(v, 0.0); }
+inline double2 widen(float2 v) { return make_double2(v.x, v.y); }
+inline double2 widen(double2 v) { return v; }
+
 template <class T> const char *tname();
 template <> const char *tname<float>() { return "s"; }
 template <> const char *tname<double>() { return "d"; }
@@ -203,14 +238,23 @@ cudaError_t run_gemv_n(const Path<T> &pa, long long lda, int m, int n, const T *
   void *ws = nullptr;
   cudaError_t e = workspace(align256((size_t)maxslots * m * sizeof(T)), st, &ws);
   if (e != cudaSuccess) return e;
-  GemvParams p{pa.base, lda, m, n, pa.lead, x, ws, (long long)m, total, (int)P, (int)KS, cm};
+  // fused epilogue (the last CTA of a row block reduces it) when few CTAs
+  // share a row block; otherwise a separate, parallel epilogue kernel
+  const bool fused = maxslots <= kFuseMaxSlots;
+  unsigned *cnt = nullptr;
+  if (fused && (e = counters((size_t)nrb, st, &cnt)) != cudaSuccess) return e;
+  GemvParams p{pa.base, lda, m, n, pa.lead, x, ws, (long long)m, total, (int)P, (int)KS, cm,
+               y, cnt, widen(alpha), widen(beta), beta_zero ? 1 : 0, (long long)m};
   {
     TimedScope ts(st);
     kfn<<<(unsigned)P, NW * 32, 0, st>>>(p);
   }
-  launch_pdl(gemv_n_epilogue<T, 8>, (unsigned)cdiv(m, 32), 256, st, y, (const T *)ws, (long long)m, m, pa.lead,
-             (int)RB, (int)KS, total, (int)P, alpha, beta, (int)beta_zero);
-  launched(2);
+  launched(1);
+  if (!fused) {
+    launch_pdl(gemv_n_epilogue<T, 8>, (unsigned)cdiv(m, 32), 256, st, y, (const T *)ws, (long long)m, m, pa.lead,
+               (int)RB, (int)KS, total, (int)P, alpha, beta, (int)beta_zero);
+    launched(1);
+  }
   char buf[256];
   snprintf(buf, sizeof buf, "gemv_n %s %s lead=%d m=%d n=%d RB=%d KS=%lld items=%lld P=%lld slots=%lld",
            tname<T>(), V > 1 ? "v256" : "scalar", pa.lead, m, n, RB, KS, total, P, maxslots);
@@ -233,15 +277,26 @@ cudaError_t run_gemv_t(const Path<T> &pa, long long lda, int m, int n, long long
   void *ws = nullptr;
   cudaError_t e = workspace(align256((size_t)maxslots * ncb * CBW * sizeof(T)), st, &ws);
   if (e != cudaSuccess) return e;
+  const bool fused = maxslots <= kFuseMaxSlots;
+  unsigned *cnt = nullptr;
+  if (fused && (e = counters((size_t)ncb, st, &cnt)) != cudaSuccess) return e;
   const long long ws_ld = ncb * CBW;
-  GemvParams p{pa.base, lda, m, n, pa.lead, x, ws, ws_ld, total, (int)P, (int)KS, cm};
+  if (fused && cm.G > 1) {
+    // mgpu partial: columns this GPU does not own stay zero
+    if ((e = cudaMemsetAsync(y, 0, (size_t)nglob * sizeof(T), st)) != cudaSuccess) return e;
+  }
+  GemvParams p{pa.base, lda, m, n, pa.lead, x, ws, ws_ld, total, (int)P, (int)KS, cm,
+               y, cnt, widen(alpha), widen(beta), beta_zero ? 1 : 0, nglob};
   {
     TimedScope ts(st);
     kfn<<<(unsigned)P, NW * 32, 0, st>>>(p);
   }
-  launch_pdl(gemv_t_epilogue<T, 8>, (unsigned)cdiv(nglob, 32), 256, st, y, (const T *)ws, ws_ld, nglob, (int)CBW,
-             (int)KS, total, (int)P, cm, alpha, beta, (int)beta_zero);
-  launched(2);
+  launched(1);
+  if (!fused) {
+    launch_pdl(gemv_t_epilogue<T, 8>, (unsigned)cdiv(nglob, 32), 256, st, y, (const T *)ws, ws_ld, nglob, (int)CBW,
+               (int)KS, total, (int)P, cm, alpha, beta, (int)beta_zero);
+    launched(1);
+  }
   char buf[256];
   snprintf(buf, sizeof buf, "gemv_t %s %s%s lead=%d m=%d n=%d H=%d KS=%lld items=%lld P=%lld slots=%lld",
            tname<T>(), V > 1 ? "v256" : "scalar", CONJ ? " conj" : "", pa.lead, m, n, H, KS, total, P,

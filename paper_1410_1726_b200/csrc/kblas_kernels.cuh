@@ -50,7 +50,45 @@ struct GemvParams {
   int P;            // CTAs
   int KS;           // N: column steps per row block; T: row chunks per column block
   ColMap cm;
+  // fused epilogue: the last CTA to finish a row (column) block sums its
+  // partial slots in slot order and writes y = alpha*sum + beta*y
+  void *y;
+  unsigned *counters;  // one per row/column block, zero between calls
+  double2 alpha, beta; // scalars of the operand type, widened
+  int beta_zero;
+  long long nglob;     // T: length of y (global columns); N: m
 };
+
+template <class T> __device__ __forceinline__ T scalar_of(double2 v);
+template <> __device__ __forceinline__ float scalar_of<float>(double2 v) { return (float)v.x; }
+template <> __device__ __forceinline__ double scalar_of<double>(double2 v) { return v.x; }
+template <> __device__ __forceinline__ float2 scalar_of<float2>(double2 v) { return make_float2((float)v.x, (float)v.y); }
+template <> __device__ __forceinline__ double2 scalar_of<double2>(double2 v) { return v; }
+
+// y[i] = alpha * s + beta * y[i] (beta == 0: y not read)
+template <class T>
+__device__ __forceinline__ void axpby_out(T *y, long long i, const GemvParams &p, T s) {
+  T r = mul_(scalar_of<T>(p.alpha), s);
+  if (!p.beta_zero) r = fma_(scalar_of<T>(p.beta), y[i], r);
+  y[i] = r;
+}
+
+// Arrival at a block's counter after this CTA wrote its partial slot.
+// Returns true (CTA-uniform) for the CTA that completes the block; its
+// reads of the other CTAs' slots must then bypass L1 (__ldcg).
+__device__ __forceinline__ bool arrive_last(unsigned *counter, int nslots) {
+  __shared__ int s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned prev = atomicAdd(counter, 1u);
+    s_last = (prev == (unsigned)(nslots - 1));
+    if (s_last) *counter = 0u;  // self-reset for the next call on this workspace
+  }
+  __syncthreads();
+  if (s_last) __threadfence();
+  return s_last != 0;
+}
 
 // ---------------------------------------------------------------------------
 // GEMV-N.  The NW warps of a CTA are stacked along the rows: a CTA row block
@@ -64,7 +102,7 @@ struct GemvParams {
 // its two half-block buffers).
 // ---------------------------------------------------------------------------
 template <class T, int V, int NW, int CW, int R>
-__global__ void __launch_bounds__(NW * 32) gemv_n_kernel(const GemvParams p) {
+__global__ void __launch_bounds__(NW * 32, 2) gemv_n_kernel(const GemvParams p) {
   griddep_launch_dependents();
   constexpr int WR = 32 * V * R;  // rows per warp
   constexpr int RB = NW * WR;     // rows per CTA row block
@@ -132,14 +170,48 @@ __global__ void __launch_bounds__(NW * 32) gemv_n_kernel(const GemvParams p) {
       q += 2;
     }
 
-    const long long slot = (long long)blockIdx.x - sk_owner(rb_first, p.total, p.P);
+    const int first = sk_owner(rb_first, p.total, p.P);
+    const int nslots = sk_owner(rb_first + p.KS - 1, p.total, p.P) - first + 1;
+    T *y = static_cast<T *>(p.y);
+    if (p.counters == nullptr) {
+      // unfused: partial slots only, gemv_n_epilogue sums them
+      const long long slot = (long long)blockIdx.x - first;
 #pragma unroll
-    for (int r = 0; r < R; ++r)
+      for (int r = 0; r < R; ++r)
 #pragma unroll
-      for (int v = 0; v < V; ++v) {
-        const long long i = pw + r * 32 * V + lane * V + v - p.lead;
-        if (i >= 0 && i < p.m) ws[slot * p.ws_ld + i] = acc[r][v];
+        for (int v = 0; v < V; ++v) {
+          const long long i = pw + r * 32 * V + lane * V + v - p.lead;
+          if (i >= 0 && i < p.m) ws[slot * p.ws_ld + i] = acc[r][v];
+        }
+    } else if (nslots == 1) {
+      // this CTA owns the whole row block: write y directly
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          const long long i = pw + r * 32 * V + lane * V + v - p.lead;
+          if (i >= 0 && i < p.m) axpby_out(y, i, p, acc[r][v]);
+        }
+    } else {
+      const long long slot = (long long)blockIdx.x - first;
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          const long long i = pw + r * 32 * V + lane * V + v - p.lead;
+          if (i >= 0 && i < p.m) ws[slot * p.ws_ld + i] = acc[r][v];
+        }
+      if (arrive_last(p.counters + rb, nslots)) {
+        // fixed slot order: the result does not depend on which CTA finishes last
+        for (int t = threadIdx.x; t < RB; t += NW * 32) {
+          const long long i = rb * RB + t - p.lead;
+          if (i < 0 || i >= p.m) continue;
+          T sum = __ldcg(ws + i);
+          for (int sl = 1; sl < nslots; ++sl) sum = add_(sum, __ldcg(ws + sl * p.ws_ld + i));
+          axpby_out(y, i, p, sum);
+        }
       }
+    }
     it = stop;
   }
 }
@@ -153,7 +225,7 @@ __global__ void __launch_bounds__(NW * 32) gemv_n_kernel(const GemvParams p) {
 // parent's neighbouring rows (possibly NaN) never enter a sum.
 // ---------------------------------------------------------------------------
 template <class T, int V, int NW, int CW, int R, bool CONJ>
-__global__ void __launch_bounds__(NW * 32) gemv_t_kernel(const GemvParams p) {
+__global__ void __launch_bounds__(NW * 32, 2) gemv_t_kernel(const GemvParams p) {
   griddep_launch_dependents();
   constexpr int H = 32 * V * R;
   constexpr int CBW = NW * CW;
@@ -234,11 +306,38 @@ __global__ void __launch_bounds__(NW * 32) gemv_t_kernel(const GemvParams p) {
       q += 2;
     }
 
-    const long long slot = (long long)blockIdx.x - sk_owner(cb_first, p.total, p.P);
+    const int first = sk_owner(cb_first, p.total, p.P);
+    const int nslots = sk_owner(cb_first + p.KS - 1, p.total, p.P) - first + 1;
+    T *y = static_cast<T *>(p.y);
+    if (p.counters == nullptr) {
+      const long long slot = (long long)blockIdx.x - first;
 #pragma unroll
-    for (int j = 0; j < CW; ++j) {
-      const T s = warp_sum(t2[j]);
-      if (lane == 0 && col0 + j < p.n) ws[slot * p.ws_ld + col0 + j] = s;
+      for (int j = 0; j < CW; ++j) {
+        const T s = warp_sum(t2[j]);
+        if (lane == 0 && col0 + j < p.n) ws[slot * p.ws_ld + col0 + j] = s;
+      }
+    } else if (nslots == 1) {
+#pragma unroll
+      for (int j = 0; j < CW; ++j) {
+        const T s = warp_sum(t2[j]);
+        if (lane == 0 && col0 + j < p.n) axpby_out(y, map_col(p.cm, col0 + j), p, s);
+      }
+    } else {
+      const long long slot = (long long)blockIdx.x - first;
+#pragma unroll
+      for (int j = 0; j < CW; ++j) {
+        const T s = warp_sum(t2[j]);
+        if (lane == 0 && col0 + j < p.n) ws[slot * p.ws_ld + col0 + j] = s;
+      }
+      if (arrive_last(p.counters + cb, nslots)) {
+        for (int t = threadIdx.x; t < CBW; t += NW * 32) {
+          const long long c = cb * CBW + t;
+          if (c >= p.n) continue;
+          T sum = __ldcg(ws + c);
+          for (int sl = 1; sl < nslots; ++sl) sum = add_(sum, __ldcg(ws + sl * p.ws_ld + c));
+          axpby_out(y, map_col(p.cm, c), p, sum);
+        }
+      }
     }
     it = stop;
   }

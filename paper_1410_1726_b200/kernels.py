@@ -104,7 +104,8 @@ def fill_report(rep: ExecutionReport, prec: Precision, mat_elems: int, x_len: in
     rep.flops = flops
     rep.plan = plan
     ctas, slots = plan_counters(plan)
-    rep.tb_count = ctas + -(-y_len // 256)
+    # SYMV/HEMV add one epilogue CTA per 32 rows; GEMV's epilogue is fused
+    rep.tb_count = ctas + (-(-y_len // 32) if plan.startswith("symv") else 0)
     rep.reduction_events = slots
 
 
