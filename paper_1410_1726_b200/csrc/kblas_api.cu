@@ -78,14 +78,14 @@ int dev_sms() {
   return sms;
 }
 
-int occupancy(const void *fn, int threads) {
+int occupancy(const void *fn, int threads, size_t smem = 0) {
   {
     std::lock_guard<std::mutex> lk(g_mu);
     auto it = g_occ.find(fn);
     if (it != g_occ.end()) return it->second;
   }
   int occ = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, 0) != cudaSuccess || occ < 1)
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem) != cudaSuccess || occ < 1)
     occ = 1;
   std::lock_guard<std::mutex> lk(g_mu);
   g_occ[fn] = occ;
@@ -380,8 +380,17 @@ template <class T, int V, int NW, int CW, int R, bool LOWER, bool HERM>
 cudaError_t run_symv(const Path<T> &pa, long long lda, int d, const T *x, ColMap cm, int ncols_local, T *y,
                      T alpha, T beta, bool beta_zero, cudaStream_t st) {
   constexpr int H = 32 * V * R, W = NW * CW;
+  constexpr size_t smem = 2 * (size_t)NW * H * sizeof(T);
   auto kfn = symv_kernel<T, V, NW, CW, R, LOWER, HERM>;
-  const long long Pmax = (long long)dev_sms() * occupancy((const void *)kfn, NW * 32);
+  {
+    static std::once_flag once;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(once, [&] {
+      attr_err = cudaFuncSetAttribute((const void *)kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    });
+    if (attr_err != cudaSuccess) return attr_err;
+  }
+  const long long Pmax = (long long)dev_sms() * occupancy((const void *)kfn, NW * 32, smem);
   TileTable tt;
   cudaError_t e = tile_table(d, pa.lead, LOWER, W, H, cm, ncols_local, Pmax, &tt);
   if (e != cudaSuccess) return e;
@@ -400,7 +409,7 @@ cudaError_t run_symv(const Path<T> &pa, long long lda, int d, const T *x, ColMap
               tt.dev, tt.ntiles, tt.total, (int)P, (cm.G == 1 && cm.nb >= d) ? W : 0};
   {
     TimedScope ts(st);
-    kfn<<<(unsigned)P, NW * 32, 0, st>>>(p);
+    kfn<<<(unsigned)P, NW * 32, smem, st>>>(p);
   }
   launch_pdl(symv_epilogue<T, LOWER, 16>, (unsigned)cdiv(d, 32), 512, st, y, p, alpha, beta, (int)beta_zero);
   launched(2);
@@ -439,13 +448,12 @@ int tma_mode() {
   return g_use_tma;
 }
 bool use_tma() { return tma_mode() != 0; }
-// tuned defaults (profiles/r1_tune_symv_v2.jsonl): the software-pipelined
-// register kernel wins for every precision from N ~ 16k up; the TMA kernel
-// wins for z and s at N <= ~8-12k (variant 0 for z, 4 for s)
-template <class T> bool prefer_tma(int d) {
-  return (sizeof(T) == 16 && d <= 12288) || (sizeof(T) == 4 && d <= 8192);
-}
-template <class T> int default_variant() { return sizeof(T) == 16 ? 0 : 4; }
+// tuned defaults (profiles/r1_tune_symv_v3.jsonl): the software-pipelined
+// register kernel wins for every precision and size except SSYMV at
+// N <= 8192, where the TMA kernel (variant 1: 16 consumers x 8 columns,
+// 256 B boxes, 5 stages) is ahead
+template <class T> bool prefer_tma(int d) { return sizeof(T) == 4 && d <= 8192; }
+template <class T> int default_variant() { return sizeof(T) == 16 ? 0 : 1; }
 
 // A00: element (0,0) of the d x d operand (any row alignment); needs a
 // 16-byte multiple column stride.
@@ -569,12 +577,18 @@ cudaError_t dispatch_symv_h(bool lower, const Path<T> &pa, long long lda, int d,
     }
 #undef KB_TMA
   }
-  if (lower) {
-    if (pa.vec) return run_symv<T, C::V, C::S_NW, C::S_CW, C::S_R, true, HERM>(pa, lda, d, x, cm, ncols_local, y, alpha, beta, beta_zero, st);
-    return run_symv<T, 1, C::S_NW, C::S_CW, C::S_RS, true, HERM>(pa, lda, d, x, cm, ncols_local, y, alpha, beta, beta_zero, st);
+#define KB_REG(V, NW, CW, R)                                                                                  \
+  return lower ? run_symv<T, V, NW, CW, R, true, HERM>(pa, lda, d, x, cm, ncols_local, y, alpha, beta, beta_zero, \
+                                                       st)                                                     \
+               : run_symv<T, V, NW, CW, R, false, HERM>(pa, lda, d, x, cm, ncols_local, y, alpha, beta, beta_zero, st)
+  if (!pa.vec) KB_REG(1, C::S_NW, C::S_CW, C::S_RS);
+  // register-kernel tuning variants (kblas_set_symv_variant 100+)
+  switch (g_symv_variant) {
+    case 101: KB_REG(C::V, 16, (sizeof(T) == 16 ? 4 : 4), 2);  // 2 KiB column segments
+    case 102: KB_REG(C::V, 8, (sizeof(T) == 16 ? 8 : 16), 1);  // 8 warps, wider per-warp column sets
+    default: KB_REG(C::V, C::S_NW, C::S_CW, C::S_R);
   }
-  if (pa.vec) return run_symv<T, C::V, C::S_NW, C::S_CW, C::S_R, false, HERM>(pa, lda, d, x, cm, ncols_local, y, alpha, beta, beta_zero, st);
-  return run_symv<T, 1, C::S_NW, C::S_CW, C::S_RS, false, HERM>(pa, lda, d, x, cm, ncols_local, y, alpha, beta, beta_zero, st);
+#undef KB_REG
 }
 
 template <class T>

@@ -399,7 +399,9 @@ __global__ void __launch_bounds__(NW * 32, 1) symv_kernel(const SymParams p) {
   griddep_launch_dependents();
   constexpr int NT = NW * 32;
   constexpr int H = 32 * V * R;
-  __shared__ T red[2][NW][H];
+  // t1 partials, double-buffered: red[buf][warp][row] (dynamic: 2*NW*H*sizeof(T))
+  extern __shared__ __align__(16) unsigned char symv_smem[];
+  T(*red)[NW][H] = reinterpret_cast<T(*)[NW][H]>(symv_smem);
   const T *__restrict__ A = static_cast<const T *>(p.A);
   const T *__restrict__ x = static_cast<const T *>(p.x);
   T *__restrict__ ws1 = static_cast<T *>(p.ws1);

@@ -57,6 +57,10 @@ def main():
             for v in ["regs"] + args.variants.split(","):
                 if v == "regs":
                     _lib.set_tma(False)
+                    lib.kblas_set_symv_variant(-1)
+                elif int(v) >= 100:
+                    _lib.set_tma(False)
+                    lib.kblas_set_symv_variant(int(v))
                 else:
                     _lib.set_tma(True)
                     lib.kblas_set_symv_variant(int(v))
