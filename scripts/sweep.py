@@ -108,7 +108,7 @@ def measure_single(fn, reps, flush):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--ops", default="dgemv,dgemv_t,zgemv,zgemv_c,sgemv,sgemv_t,cgemv,cgemv_c,"
-                                     "dsymv,dsymv_u,zhemv,zhemv_u,ssymv,chemv")
+                                     "cgemv_t,zgemv_t,dsymv,dsymv_u,zhemv,zhemv_u,ssymv,ssymv_u,chemv,chemv_u")
     ap.add_argument("--sizes", default="1024,2048,4096,8192,12288,16383,16384,20480,24576,32768,40960,49152,60000")
     ap.add_argument("--max-gb", type=float, default=60.0)
     ap.add_argument("--reps", type=int, default=20)
@@ -171,6 +171,7 @@ def main():
                     row["cublas_gbs"] = round(nbytes / cms / 1e6, 1)
                     row["speedup_vs_cublas"] = round(cms / ms, 3)
                     ours(0)
+                    theirs(0)  # same operand copy on both sides
                     scale = float((y2.abs().max()).item()) or 1.0
                     row["rel_diff_vs_cublas"] = float(((y - y2).abs().max() / scale).item())
             rows.append(row)
