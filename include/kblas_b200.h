@@ -311,6 +311,15 @@ int kblas_set_tma(int mode);
 /* per-precision default.  Used by scripts/tune_symv.py; returns the  */
 /* previous variant.                                                  */
 int kblas_set_symv_variant(int variant);
+/* Select the GEMV-N form: -1 (default) = automatic (the split form,   */
+/* narrow row blocks reduced inside one kernel, for small and short    */
+/* matrices; the stacked-rows stream-K form otherwise), 1 = always the */
+/* split form, 0 = never.  Returns the previous mode.                  */
+int kblas_set_gemv_split(int mode);
+/* Register SYMV/HEMV kernel: orders up to max_order use narrow column */
+/* tiles (more work items for small operands).  Returns the previous   */
+/* threshold (default 2048).                                           */
+int kblas_set_symv_narrow(int max_order);
 /* Description of the last plan chosen for a call on this thread      */
 /* (kernel family, grid, items, workspace bytes) as a NUL-terminated   */
 /* string; for reports and tests.                                      */

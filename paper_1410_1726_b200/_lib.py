@@ -129,6 +129,10 @@ def load():
         lib.kblas_set_symv_variant.restype = c_int
         lib.kblas_set_tma.argtypes = [c_int]
         lib.kblas_set_tma.restype = c_int
+        lib.kblas_set_gemv_split.argtypes = [c_int]
+        lib.kblas_set_gemv_split.restype = c_int
+        lib.kblas_set_symv_narrow.argtypes = [c_int]
+        lib.kblas_set_symv_narrow.restype = c_int
         lib.kblas_last_plan.restype = ctypes.c_char_p
         lib.kblas_last_plan.argtypes = []
         lib.kblas_version.restype = ctypes.c_char_p
@@ -173,6 +177,19 @@ def set_tma(mode) -> int:
     kernel, -1 tuned per-precision default.  Returns the previous mode."""
     m = -1 if mode == -1 else (1 if mode else 0)
     return int(load().kblas_set_tma(m))
+
+
+def set_gemv_split(mode) -> int:
+    """GEMV-N form: True/1 split form always, False/0 never, -1 automatic.
+    Returns the previous mode."""
+    m = -1 if mode == -1 else (1 if mode else 0)
+    return int(load().kblas_set_gemv_split(m))
+
+
+def set_symv_narrow(max_order: int) -> int:
+    """Register SYMV/HEMV: narrow tiles up to this order.  Returns the
+    previous threshold."""
+    return int(load().kblas_set_symv_narrow(int(max_order)))
 
 
 def timing_enable(on: bool):

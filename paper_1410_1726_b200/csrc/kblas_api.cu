@@ -14,6 +14,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
+#include <initializer_list>
 #include <map>
 #include <mutex>
 #include <string>
@@ -32,6 +34,7 @@ using namespace kb;
 namespace {
 
 std::atomic<unsigned long long> g_launches{0};
+int g_symv_narrow_max = 2048;  // register SYMV: narrow tiles up to this order (kblas_set_symv_narrow)
 thread_local std::string g_last_plan;
 
 // ------------------------------------------------------------- timing hook
@@ -148,6 +151,7 @@ cudaError_t counters(size_t n, cudaStream_t st, unsigned **out) {
 
 inline long long cdiv(long long a, long long b) { return (a + b - 1) / b; }
 constexpr long long kFuseMaxSlots = 8;
+constexpr long long kFuseMaxSlotsT = 64;
 inline size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
 
 // ------------------------------------------------------------ scalar utils
@@ -224,6 +228,35 @@ template <class T> struct Cfg {
 };
 
 // ============================================================= GEMV-N
+// Split-form GEMV-N (gemv_ns_kernel) choice: -1 auto, 0 never, 1 always
+// (kblas_set_gemv_split, for the tuner).
+int g_gemv_split = -1;
+constexpr long long kSplitMaxSlots = 64;
+
+template <class T, int V, int NW, int CW>
+cudaError_t run_gemv_ns(const Path<T> &pa, long long lda, int m, int n, const T *x, ColMap cm, T *y, T alpha,
+                        T beta, bool beta_zero, cudaStream_t st, long long S, long long nrb) {
+  constexpr int RB = 32 * V;
+  auto kfn = gemv_ns_kernel<T, V, NW, CW>;
+  void *ws = nullptr;
+  cudaError_t e = workspace(align256((size_t)S * m * sizeof(T)), st, &ws);
+  if (e != cudaSuccess) return e;
+  unsigned *cnt = nullptr;
+  if (S > 1 && (e = counters((size_t)nrb, st, &cnt)) != cudaSuccess) return e;
+  GemvParams p{pa.base, lda, m, n, pa.lead, x, ws, (long long)m, nrb * S, (int)(nrb * S), (int)S, cm,
+               y, cnt, widen(alpha), widen(beta), beta_zero ? 1 : 0, (long long)m};
+  {
+    TimedScope ts(st);
+    kfn<<<(unsigned)(nrb * S), NW * 32, 0, st>>>(p);
+  }
+  launched(1);
+  char buf[256];
+  snprintf(buf, sizeof buf, "gemv_ns %s %s lead=%d m=%d n=%d RB=%d P=%lld slots=%lld", tname<T>(),
+           V > 1 ? "v256" : "scalar", pa.lead, m, n, RB, nrb * S, S);
+  g_last_plan = buf;
+  return cudaGetLastError();
+}
+
 template <class T, int V, int NW, int CW, int R>
 cudaError_t run_gemv_n(const Path<T> &pa, long long lda, int m, int n, const T *x, ColMap cm, T *y,
                        T alpha, T beta, bool beta_zero, cudaStream_t st) {
@@ -235,12 +268,25 @@ cudaError_t run_gemv_n(const Path<T> &pa, long long lda, int m, int n, const T *
   const long long P = std::min<long long>(total, (long long)dev_sms() * occupancy((const void *)kfn, NW * 32));
   const long long per = std::max<long long>(1, total / P);
   const long long maxslots = std::min<long long>(P, cdiv(KS, per) + 1);
-  void *ws = nullptr;
-  cudaError_t e = workspace(align256((size_t)maxslots * m * sizeof(T)), st, &ws);
-  if (e != cudaSuccess) return e;
   // fused epilogue (the last CTA of a row block reduces it) when few CTAs
   // share a row block; otherwise a separate, parallel epilogue kernel
   const bool fused = maxslots <= kFuseMaxSlots;
+  {
+    // small / short matrices: the split form keeps the row blocks narrow so
+    // few CTAs share one, and reduces them in the same kernel
+    constexpr int NWs = 8, CWs = 4, RBs = 32 * V;
+    const long long nrb_s = cdiv((long long)pa.lead + m, RBs);
+    const long long Ps = (long long)dev_sms() * occupancy((const void *)gemv_ns_kernel<T, V, NWs, CWs>, NWs * 32);
+    const long long S = std::max<long long>(
+        1, std::min<long long>({cdiv(Ps, nrb_s), kSplitMaxSlots, std::max<long long>(1, n / (NWs * CWs))}));
+    const bool fills = nrb_s * S >= dev_sms();
+    const bool small = (long long)m * n * (long long)sizeof(T) <= (512LL << 20);
+    if (g_gemv_split == 1 || (g_gemv_split == -1 && !fused && fills && small))
+      return run_gemv_ns<T, V, NWs, CWs>(pa, lda, m, n, x, cm, y, alpha, beta, beta_zero, st, S, nrb_s);
+  }
+  void *ws = nullptr;
+  cudaError_t e = workspace(align256((size_t)maxslots * m * sizeof(T)), st, &ws);
+  if (e != cudaSuccess) return e;
   unsigned *cnt = nullptr;
   if (fused && (e = counters((size_t)nrb, st, &cnt)) != cudaSuccess) return e;
   GemvParams p{pa.base, lda, m, n, pa.lead, x, ws, (long long)m, total, (int)P, (int)KS, cm,
@@ -277,7 +323,9 @@ cudaError_t run_gemv_t(const Path<T> &pa, long long lda, int m, int n, long long
   void *ws = nullptr;
   cudaError_t e = workspace(align256((size_t)maxslots * ncb * CBW * sizeof(T)), st, &ws);
   if (e != cudaSuccess) return e;
-  const bool fused = maxslots <= kFuseMaxSlots;
+  // the last CTA of a column block sums CBW columns x maxslots slots with the
+  // whole CTA, so the fused form pays off up to many slots
+  const bool fused = maxslots <= kFuseMaxSlotsT;
   unsigned *cnt = nullptr;
   if (fused && (e = counters((size_t)ncb, st, &cnt)) != cudaSuccess) return e;
   const long long ws_ld = ncb * CBW;
@@ -308,6 +356,7 @@ cudaError_t run_gemv_t(const Path<T> &pa, long long lda, int m, int n, long long
 // ============================================================= SYMV/HEMV
 struct TileTable {
   SymTile *dev = nullptr;
+  int *start = nullptr;  // per CTA (of min(P, total)): tile holding its first item
   int ntiles = 0;
   long long total = 0;
   long long maxslots = 0;
@@ -365,9 +414,24 @@ cudaError_t tile_table(int d, int lead, bool lower, int W, int H, ColMap cm, int
       tt.maxslots = std::max<long long>(tt.maxslots, sk_owner(bnext - 1, prefix, Pe) - sk_owner(a, prefix, Pe) + 1);
   }
   if (!tiles.empty()) {
-    cudaError_t e = cudaMalloc(&tt.dev, tiles.size() * sizeof(SymTile));
+    // per-CTA start tiles: CTA c's first item sk_start(c) lies in the last
+    // tile whose prefix <= it (saves the kernels a binary search)
+    std::vector<int> start((size_t)Pe);
+    size_t k = 0;
+    for (long long c = 0; c < Pe; ++c) {
+      const long long it = sk_start(c, prefix, Pe);
+      while (k + 1 < tiles.size() && tiles[k + 1].prefix <= it) ++k;
+      start[(size_t)c] = (int)k;
+    }
+    const size_t tb = align256(tiles.size() * sizeof(SymTile));
+    void *mem = nullptr;
+    cudaError_t e = cudaMalloc(&mem, tb + start.size() * sizeof(int));
     if (e != cudaSuccess) return e;
+    tt.dev = static_cast<SymTile *>(mem);
+    tt.start = reinterpret_cast<int *>(static_cast<char *>(mem) + tb);
     e = cudaMemcpy(tt.dev, tiles.data(), tiles.size() * sizeof(SymTile), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return e;
+    e = cudaMemcpy(tt.start, start.data(), start.size() * sizeof(int), cudaMemcpyHostToDevice);
     if (e != cudaSuccess) return e;
   }
   std::lock_guard<std::mutex> lk(g_mu);
@@ -406,7 +470,7 @@ cudaError_t run_symv(const Path<T> &pa, long long lda, int d, const T *x, ColMap
   e = workspace(b1 + b2, st, &ws);
   if (e != cudaSuccess) return e;
   SymParams p{pa.base, lda, d, pa.lead, x, ws, (long long)d, (char *)ws + b1, (long long)d,
-              tt.dev, tt.ntiles, tt.total, (int)P, (cm.G == 1 && cm.nb >= d) ? W : 0};
+              tt.dev, tt.ntiles, tt.total, (int)P, (cm.G == 1 && cm.nb >= d) ? W : 0, tt.start};
   {
     TimedScope ts(st);
     kfn<<<(unsigned)P, NW * 32, smem, st>>>(p);
@@ -452,7 +516,7 @@ bool use_tma() { return tma_mode() != 0; }
 // register kernel wins for every precision and size except SSYMV at
 // N <= 8192, where the TMA kernel (variant 1: 16 consumers x 8 columns,
 // 256 B boxes, 5 stages) is ahead
-template <class T> bool prefer_tma(int d) { return sizeof(T) == 4 && d <= 8192; }
+template <class T> bool prefer_tma(int) { return false; }
 template <class T> int default_variant() { return sizeof(T) == 16 ? 0 : 1; }
 
 // A00: element (0,0) of the d x d operand (any row alignment); needs a
@@ -513,7 +577,7 @@ cudaError_t run_symv_tma(const T *A00, long long lda, int d, const T *x, ColMap 
   if (e != cudaSuccess) return e;
   SymTmaParams tp;
   tp.sp = SymParams{base, lda, d, lead, x, ws, (long long)d, (char *)ws + b1, (long long)d,
-                    tt.dev, tt.ntiles, tt.total, (int)P, (cm.G == 1 && cm.nb >= d) ? W : 0};
+                    tt.dev, tt.ntiles, tt.total, (int)P, (cm.G == 1 && cm.nb >= d) ? W : 0, tt.start};
   tp.unit_per_elem = upe;
   {
     TimedScope ts(st);
@@ -582,10 +646,16 @@ cudaError_t dispatch_symv_h(bool lower, const Path<T> &pa, long long lda, int d,
                                                        st)                                                     \
                : run_symv<T, V, NW, CW, R, false, HERM>(pa, lda, d, x, cm, ncols_local, y, alpha, beta, beta_zero, st)
   if (!pa.vec) KB_REG(1, C::S_NW, C::S_CW, C::S_RS);
-  // register-kernel tuning variants (kblas_set_symv_variant 100+)
-  switch (g_symv_variant) {
+  // register-kernel tuning variants (kblas_set_symv_variant 100+); small
+  // operands use narrow tiles (variant 103, W = 32 columns, 16 for z) so
+  // there are enough items to occupy every SM
+  int v = g_symv_variant;
+  if (v < 100 && d <= g_symv_narrow_max) v = 103;
+  switch (v) {
     case 101: KB_REG(C::V, 16, (sizeof(T) == 16 ? 4 : 4), 2);  // 2 KiB column segments
     case 102: KB_REG(C::V, 8, (sizeof(T) == 16 ? 8 : 16), 1);  // 8 warps, wider per-warp column sets
+    case 103: KB_REG(C::V, 8, 4, 1);                           // 8 warps x 4 columns (small operands)
+    case 104: KB_REG(C::V, 8, 8, 1);                           // 8 warps x 8 columns
     default: KB_REG(C::V, C::S_NW, C::S_CW, C::S_R);
   }
 #undef KB_REG
@@ -952,6 +1022,18 @@ const char *kblas_last_plan(void) { return g_last_plan.c_str(); }
 int kblas_set_symv_variant(int v) {
   const int prev = g_symv_variant;
   g_symv_variant = v;
+  return prev;
+}
+
+int kblas_set_symv_narrow(int max_order) {
+  const int prev = g_symv_narrow_max;
+  g_symv_narrow_max = max_order;
+  return prev;
+}
+
+int kblas_set_gemv_split(int mode) {
+  const int prev = g_gemv_split;
+  g_gemv_split = mode < 0 ? -1 : (mode ? 1 : 0);
   return prev;
 }
 

@@ -90,6 +90,49 @@ __device__ __forceinline__ bool arrive_last(unsigned *counter, int nslots) {
   return s_last != 0;
 }
 
+// Sum of slots [s0, s1) of ws[slot * ld + idx] in slot order; the loads are
+// issued eight at a time (independent, so one L2 round trip per batch) and
+// added in order, so the result does not depend on timing.
+template <class T>
+__device__ __forceinline__ T sum_slots(const T *ws, long long ld, long long idx, int s0, int s1) {
+  T acc = zero<T>();
+  for (int sl = s0; sl < s1; sl += 8) {
+    T t[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) t[u] = (sl + u < s1) ? __ldcg(ws + (long long)(sl + u) * ld + idx) : zero<T>();
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (sl + u < s1) acc = add_(acc, t[u]);
+  }
+  return acc;
+}
+
+// Whole-CTA fixed-order reduction of nslots partial slots for the nidx
+// consecutive workspace indices idx0 .. idx0+nidx-1: the threads split each
+// index's slot range into NT/nidx contiguous parts (a function of nidx and
+// nslots only), the parts are added in order, and out(k, sum) is called for
+// index k by one thread.  Used by the last CTA to arrive at a block.
+template <class T, int NT, class F>
+__device__ __forceinline__ void cta_slot_sum(const T *ws, long long ld, long long idx0, int nidx, int nslots, F out) {
+  __shared__ T sbuf[NT];
+  for (int base = 0; base < nidx; base += NT) {
+    const int chunk = min(NT, nidx - base);
+    const int parts = NT / chunk;
+    const int k = threadIdx.x % chunk, part = threadIdx.x / chunk;
+    if (part < parts) {
+      const int s0 = nslots * part / parts, s1 = nslots * (part + 1) / parts;
+      sbuf[part * chunk + k] = sum_slots(ws, ld, idx0 + base + k, s0, s1);
+    }
+    __syncthreads();
+    if ((int)threadIdx.x < chunk) {
+      T r = sbuf[threadIdx.x];
+      for (int q = 1; q < parts; ++q) r = add_(r, sbuf[q * chunk + threadIdx.x]);
+      out(base + (int)threadIdx.x, r);
+    }
+    __syncthreads();
+  }
+}
+
 // ---------------------------------------------------------------------------
 // GEMV-N.  The NW warps of a CTA are stacked along the rows: a CTA row block
 // is RB = NW*32*V*R rows, so every column visit reads RB*sizeof(T) contiguous
@@ -203,17 +246,89 @@ __global__ void __launch_bounds__(NW * 32, 2) gemv_n_kernel(const GemvParams p) 
         }
       if (arrive_last(p.counters + rb, nslots)) {
         // fixed slot order: the result does not depend on which CTA finishes last
-        for (int t = threadIdx.x; t < RB; t += NW * 32) {
-          const long long i = rb * RB + t - p.lead;
-          if (i < 0 || i >= p.m) continue;
-          T sum = __ldcg(ws + i);
-          for (int sl = 1; sl < nslots; ++sl) sum = add_(sum, __ldcg(ws + sl * p.ws_ld + i));
-          axpby_out(y, i, p, sum);
-        }
+        const long long i0 = max(rb * RB - p.lead, 0LL), i1 = min(rb * RB + RB - p.lead, (long long)p.m);
+        cta_slot_sum<T, NW * 32>(ws, p.ws_ld, i0, (int)(i1 - i0), nslots,
+                                 [&](int k, T sum) { axpby_out(y, i0 + k, p, sum); });
       }
     }
     it = stop;
   }
+}
+
+// ---------------------------------------------------------------------------
+// GEMV-N for small and short matrices (the split form).  When the matrix is
+// small the stacked-rows kernel above has few row blocks, so many CTAs share
+// each one and the partial-slot traffic and its reduction dominate.  Here a
+// CTA owns one RB = 32*V-row block (one warp width) and a contiguous range of
+// columns; its NW warps take the range's CW-column groups round robin and
+// are combined through shared memory, so a row block is shared by only
+// KS = #CTAs / #row blocks CTAs.  Those combine through per-CTA slots; the
+// last CTA to arrive sums them in slot order and writes y (one kernel,
+// deterministic).  Grid: (row block, split) = blockIdx.x / KS, % KS.
+// ---------------------------------------------------------------------------
+template <class T, int V, int NW, int CW>
+__global__ void __launch_bounds__(NW * 32, 2) gemv_ns_kernel(const GemvParams p) {
+  constexpr int RB = 32 * V;
+  __shared__ T red[NW][RB];
+  const T *__restrict__ A = static_cast<const T *>(p.A);
+  const T *__restrict__ x = static_cast<const T *>(p.x);
+  T *__restrict__ ws = static_cast<T *>(p.ws);
+  T *y = static_cast<T *>(p.y);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t pol = policy_evict_first();
+  const long long rb = blockIdx.x / p.KS;
+  const int split = (int)(blockIdx.x % p.KS);
+  const int c0 = (int)((long long)split * p.n / p.KS), c1 = (int)((long long)(split + 1) * p.n / p.KS);
+  const long long pw = rb * RB;  // first physical row of the block
+  const bool rok = pw + lane * V < (long long)p.lead + p.m;
+  T acc[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) acc[v] = zero<T>();
+  auto load = [&](int g, Pack<T, V> (&a)[CW], T (&xv)[CW]) {
+#pragma unroll
+    for (int j = 0; j < CW; ++j) {
+      const int col = g + j;
+      const bool cok = col < c1;
+      xv[j] = cok ? __ldg(x + map_col(p.cm, col)) : zero<T>();
+      ld_pack(a[j], A + (long long)col * p.lda + pw + lane * V, cok && rok, pol);
+    }
+  };
+  auto fma_group = [&](const Pack<T, V> (&a)[CW], const T (&xv)[CW]) {
+#pragma unroll
+    for (int j = 0; j < CW; ++j)
+#pragma unroll
+      for (int v = 0; v < V; ++v) acc[v] = fma_(a[j].v(v), xv[j], acc[v]);
+  };
+  constexpr int STEP = NW * CW;
+  Pack<T, V> a0[CW], a1[CW];
+  T x0[CW], x1[CW];
+  int g = c0 + warp * CW;
+  if (g < c1) load(g, a0, x0);
+  while (g < c1) {
+    const bool more = g + STEP < c1;
+    if (more) load(g + STEP, a1, x1);
+    fma_group(a0, x0);
+    if (!more) break;
+    if (g + 2 * STEP < c1) load(g + 2 * STEP, a0, x0);
+    fma_group(a1, x1);
+    g += 2 * STEP;
+  }
+#pragma unroll
+  for (int v = 0; v < V; ++v) red[warp][lane * V + v] = acc[v];
+  __syncthreads();
+  const long long i0 = max(pw - p.lead, 0LL), i1 = min(pw + RB - p.lead, (long long)p.m);
+  for (int t = threadIdx.x; t < RB; t += NW * 32) {
+    const long long i = pw + t - p.lead;
+    if (i < i0 || i >= i1) continue;
+    T sum = red[0][t];
+#pragma unroll
+    for (int w = 1; w < NW; ++w) sum = add_(sum, red[w][t]);
+    if (p.KS == 1) axpby_out(y, i, p, sum);
+    else ws[(long long)split * p.ws_ld + i] = sum;
+  }
+  if (p.KS > 1 && arrive_last(p.counters + rb, p.KS))
+    cta_slot_sum<T, NW * 32>(ws, p.ws_ld, i0, (int)(i1 - i0), p.KS,
+                             [&](int k, T sum) { axpby_out(y, i0 + k, p, sum); });
 }
 
 // ---------------------------------------------------------------------------
@@ -330,13 +445,9 @@ __global__ void __launch_bounds__(NW * 32, 2) gemv_t_kernel(const GemvParams p) 
         if (lane == 0 && col0 + j < p.n) ws[slot * p.ws_ld + col0 + j] = s;
       }
       if (arrive_last(p.counters + cb, nslots)) {
-        for (int t = threadIdx.x; t < CBW; t += NW * 32) {
-          const long long c = cb * CBW + t;
-          if (c >= p.n) continue;
-          T sum = __ldcg(ws + c);
-          for (int sl = 1; sl < nslots; ++sl) sum = add_(sum, __ldcg(ws + sl * p.ws_ld + c));
-          axpby_out(y, map_col(p.cm, c), p, sum);
-        }
+        const long long c0 = cb * CBW, c1 = min(c0 + CBW, (long long)p.n);
+        cta_slot_sum<T, NW * 32>(ws, p.ws_ld, c0, (int)(c1 - c0), nslots,
+                                 [&](int k, T sum) { axpby_out(y, map_col(p.cm, c0 + k), p, sum); });
       }
     }
     it = stop;
@@ -392,7 +503,14 @@ struct SymParams {
   long long total;
   int P;
   int tile_w;  // > 0: tiles are uniform, tile k = columns [k*tile_w, (k+1)*tile_w) (single GPU)
+  const int *start_tile;  // per CTA: the tile holding its first item (host-built)
 };
+
+// The tile holding CTA blockIdx.x's first item: one load from the per-CTA
+// start table the host builds with the tile table.
+__device__ __forceinline__ int sym_start_tile(const SymParams &p, long long) {
+  return p.start_tile[blockIdx.x];
+}
 
 template <class T, int V, int NW, int CW, int R, bool LOWER, bool HERM>
 __global__ void __launch_bounds__(NW * 32, 1) symv_kernel(const SymParams p) {
@@ -402,6 +520,7 @@ __global__ void __launch_bounds__(NW * 32, 1) symv_kernel(const SymParams p) {
   // t1 partials, double-buffered: red[buf][warp][row] (dynamic: 2*NW*H*sizeof(T))
   extern __shared__ __align__(16) unsigned char symv_smem[];
   T(*red)[NW][H] = reinterpret_cast<T(*)[NW][H]>(symv_smem);
+
   const T *__restrict__ A = static_cast<const T *>(p.A);
   const T *__restrict__ x = static_cast<const T *>(p.x);
   T *__restrict__ ws1 = static_cast<T *>(p.ws1);
@@ -416,15 +535,7 @@ __global__ void __launch_bounds__(NW * 32, 1) symv_kernel(const SymParams p) {
   const bool xvec = V > 1 && p.lead == 0 && (reinterpret_cast<uintptr_t>(x) % (V * sizeof(T))) == 0;
 
   // tile holding item it0: the last tile whose prefix <= it0
-  int k;
-  {
-    int lo = 0, hi = p.ntiles - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (p.tiles[mid].prefix <= it0) lo = mid; else hi = mid - 1;
-    }
-    k = lo;
-  }
+  int k = sym_start_tile(p, it0);
 
   // Software pipeline over the CTA's items: the loads of item q+1 (possibly
   // in the next tile) are issued right after item q's FMAs, so they are in
@@ -594,14 +705,7 @@ __device__ __forceinline__ T slot_sum(const T *__restrict__ ws, long long ws_ld,
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int len = valid ? nslots : 0;
   const int s0 = (int)((long long)len * warp / EW), s1 = (int)((long long)len * (warp + 1) / EW);
-  T a0 = zero<T>(), a1 = zero<T>();
-  int sl = s0;
-  for (; sl + 2 <= s1; sl += 2) {
-    a0 = add_(a0, ws[sl * ws_ld + idx]);
-    a1 = add_(a1, ws[(sl + 1) * ws_ld + idx]);
-  }
-  if (sl < s1) a0 = add_(a0, ws[sl * ws_ld + idx]);
-  part[warp][lane] = add_(a0, a1);
+  part[warp][lane] = sum_slots(ws, ws_ld, idx, s0, s1);
   __syncthreads();
   T s = part[0][lane];
 #pragma unroll
@@ -650,10 +754,12 @@ __global__ void __launch_bounds__(EW * 32) gemv_t_epilogue(T *y, const T *__rest
 }
 
 // One CTA per 32 rows (lane = row).  The t1 partials of a row are spread
-// over up to d/W tiles; the EW warps split that tile range into EW fixed
-// contiguous parts (a function of the row only, so the summation order is
-// fixed and results are bit-reproducible), then warp 0 adds the parts in
-// order plus the row's t2 slots.
+// over up to d/W tiles and its t2 partials over the CTA slots of the tile
+// owning the row's column.  Warp w takes tiles kb+w, kb+w+EW, ... and t2
+// slots w, w+EW, ... (a partition that depends only on the row, so the
+// summation order is fixed and results are bit-reproducible); the tile
+// record is fetched alongside the t1 loads, so a call costs about two L2
+// round trips.  Warp 0 then adds the EW parts in order.
 template <class T, bool LOWER, int EW>
 __global__ void __launch_bounds__(EW * 32) symv_epilogue(T *y, const SymParams p, T alpha, T beta, int beta_zero) {
   griddep_wait();
@@ -675,49 +781,43 @@ __global__ void __launch_bounds__(EW * 32) symv_epilogue(T *y, const SymParams p
     }
     nle = lo;
   }
+  // the tile owning column i (if any on this GPU) and the next tile's prefix
+  SymTile own{};
+  long long tnext = 0;
+  if (nle > 0) {
+    own = p.tiles[nle - 1];
+    tnext = (nle < p.ntiles) ? p.tiles[nle].prefix : p.total;
+  }
   int kb, ke;
   if (LOWER) {
     kb = 0;
     ke = nle;
   } else {
     kb = nle;
-    if (nle > 0 && (p.tile_w > 0 || p.tiles[nle - 1].gcol0 + p.tiles[nle - 1].ncols > i)) kb = nle - 1;
+    if (nle > 0 && (p.tile_w > 0 || own.gcol0 + own.ncols > i)) kb = nle - 1;
     ke = p.ntiles;
   }
-  // warp w takes tiles kb+w, kb+w+EW, ... (a fixed partition: the summation
-  // order depends only on the row); eight loads in flight per lane
   if (!valid) ke = kb;
-  T acc[8];
-#pragma unroll
-  for (int u = 0; u < 8; ++u) acc[u] = zero<T>();
-  int k = kb + warp;
-  for (; k + 7 * EW < ke; k += 8 * EW) {
+  T acc = zero<T>();
+  for (int k = kb + warp; k < ke; k += 8 * EW) {
     T t[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) t[u] = ws1[(long long)(k + u * EW) * p.ws1_ld + i];
+    for (int u = 0; u < 8; ++u) t[u] = (k + u * EW < ke) ? ws1[(long long)(k + u * EW) * p.ws1_ld + i] : zero<T>();
 #pragma unroll
-    for (int u = 0; u < 8; ++u) acc[u] = add_(acc[u], t[u]);
+    for (int u = 0; u < 8; ++u)
+      if (k + u * EW < ke) acc = add_(acc, t[u]);
   }
-  for (; k < ke; k += EW) acc[0] = add_(acc[0], ws1[(long long)k * p.ws1_ld + i]);
-  part[warp][lane] = add_(add_(add_(acc[0], acc[1]), add_(acc[2], acc[3])),
-                          add_(add_(acc[4], acc[5]), add_(acc[6], acc[7])));
+  // t2: the slots of the tile owning column i
+  if (valid && nle > 0 && i < (long long)own.gcol0 + own.ncols && tnext > own.prefix) {
+    const int nsl = sk_owner(tnext - 1, p.total, p.P) - sk_owner(own.prefix, p.total, p.P) + 1;
+    for (int sl = warp; sl < nsl; sl += EW) acc = add_(acc, ws2[(long long)sl * p.ws2_ld + i]);
+  }
+  part[warp][lane] = acc;
   __syncthreads();
   if (warp != 0 || !valid) return;
   T s = part[0][lane];
 #pragma unroll
   for (int w = 1; w < EW; ++w) s = add_(s, part[w][lane]);
-  // t2: the tile owning column i (if any on this GPU)
-  if (nle > 0) {
-    const SymTile tl = p.tiles[nle - 1];
-    if (i < (long long)tl.gcol0 + tl.ncols) {
-      const long long tnext = (nle < p.ntiles) ? p.tiles[nle].prefix : p.total;
-      if (tnext > tl.prefix) {
-        const int first = sk_owner(tl.prefix, p.total, p.P);
-        const int last = sk_owner(tnext - 1, p.total, p.P);
-        for (int sl = 0; sl <= last - first; ++sl) s = add_(s, ws2[sl * p.ws2_ld + i]);
-      }
-    }
-  }
   store_axpby(y, i, alpha, s, beta, beta_zero);
 }
 

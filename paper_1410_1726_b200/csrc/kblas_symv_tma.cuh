@@ -115,15 +115,7 @@ __global__ void __launch_bounds__((NC + 2) * 32, 1)
   __syncthreads();
 
   // tile holding item it0
-  int k0;
-  {
-    int lo = 0, hi = p.ntiles - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (p.tiles[mid].prefix <= it0) lo = mid; else hi = mid - 1;
-    }
-    k0 = lo;
-  }
+  const int k0 = sym_start_tile(p, it0);
 
   if (warp == NC) {
     // ---------------------------------------------------------- producer

@@ -447,3 +447,91 @@ class TestGemvEpilogueModes:
         want = streamed.gemv(trans, 0.5, a_host, xh, -2.0, yh)
         dense = np.abs(a_host) if trans == "n" else np.abs(a_host).T
         check(r1.y_out, want, tag, 0.5, dense, xh, -2.0, yh)
+
+
+@pytest.fixture(params=["split", "stacked"])
+def gemv_form(request):
+    """Run a test on both GEMV-N forms: the split form (narrow row blocks,
+    CTAs of a row block reduced by the last to arrive) and the stacked-rows
+    stream-K form."""
+    prev = _lib.set_gemv_split(request.param == "split")
+    yield request.param
+    _lib.set_gemv_split(prev)
+
+
+class TestGemvNForms:
+    @pytest.mark.parametrize("tag", "sdcz")
+    def test_oracle_both_forms(self, gemv_form, tag):
+        rng = np.random.default_rng(131)
+        for m, n in [(1, 1), (7, 5), (65, 33), (100, 3000), (1000, 37), (2049, 1537), (129, 20000)]:
+            for ld, ro in ((-(-m // 32) * 32 + 32, 0), (m + 11, 5), (m + 40, 3)):
+                host = np.full(ld * n, np.nan, dtype=naive.DTYPES[tag])
+                win = naive.window(host, ld, ro + m, n)
+                a = naive.fill(rng, (m, n), tag)
+                win[ro:ro + m, :] = a
+                v = kb.MatrixView(torch.from_numpy(host).cuda(), ro + m, n, ld, kb.precision(tag)).submatrix(
+                    ro, 0, m, n)
+                x, y = naive.fill(rng, n, tag), naive.fill(rng, m, tag)
+                rep = kb.gemv("n", 0.7, v, dvec(x), -0.3, dvec(y))
+                if gemv_form == "split":
+                    assert rep.plan.startswith("gemv_ns"), rep.plan
+                got = rep.y_out
+                assert torch.isfinite(got).all()
+                check(got, naive.naive_gemv("n", 0.7, a, x, -0.3, y), tag, 0.7, np.abs(a), x, -0.3, y)
+
+    def test_forms_deterministic_and_beta_zero(self, gemv_form):
+        rng = np.random.default_rng(132)
+        v, a = dev_matrix(rng, 3000, 4000, "d")
+        x = naive.fill(rng, 4000, "d")
+        ynan = torch.full((3000,), float("nan"), dtype=torch.float64, device="cuda")
+        r1 = kb.gemv("n", 1.0, v, dvec(x), 0.0, ynan).y_out
+        r2 = kb.gemv("n", 1.0, v, dvec(x), 0.0, ynan).y_out
+        assert torch.equal(r1, r2)
+        want = naive.naive_gemv("n", 1.0, a, x, 0.0, np.zeros(3000))
+        check(r1, want, "d", 1.0, np.abs(a), x, 0.0, np.zeros(3000))
+
+    def test_auto_picks_split_for_small(self):
+        prev = _lib.set_gemv_split(-1)
+        try:
+            rng = np.random.default_rng(133)
+            v, a = dev_matrix(rng, 1024, 1024, "d")
+            x, y = naive.fill(rng, 1024, "d"), naive.fill(rng, 1024, "d")
+            rep = kb.gemv("n", 1.0, v, dvec(x), 1.0, dvec(y))
+            assert rep.plan.startswith("gemv_ns"), rep.plan
+            check(rep.y_out, naive.naive_gemv("n", 1.0, a, x, 1.0, y), "d", 1.0, np.abs(a), x, 1.0, y)
+        finally:
+            _lib.set_gemv_split(prev)
+
+
+@pytest.fixture(params=["narrow", "wide"])
+def symv_tiles(request):
+    """Register SYMV/HEMV kernel with narrow (small-operand) and wide tiles."""
+    prev_n = _lib.set_symv_narrow((1 << 30) if request.param == "narrow" else 0)
+    prev_t = _lib.set_tma(0)
+    yield request.param
+    _lib.set_symv_narrow(prev_n)
+    _lib.set_tma(prev_t)
+
+
+class TestSymvTiles:
+    @pytest.mark.parametrize("tag", "sdcz")
+    @pytest.mark.parametrize("uplo", "lu")
+    def test_oracle_tiles(self, symv_tiles, tag, uplo):
+        rng = np.random.default_rng(141)
+        for d in (1, 33, 130, 1000, 2500):
+            for ro in (0, 3):
+                ld = d + ro + 8
+                host = np.full(ld * (d + ro), np.nan, dtype=naive.DTYPES[tag])
+                win = naive.window(host, ld, d + ro, d + ro)
+                vals = naive.fill(rng, (d, d), tag)
+                mask = np.tril(np.ones((d, d), bool)) if uplo == "l" else np.triu(np.ones((d, d), bool))
+                tri = np.where(mask, vals, 0)
+                win[ro:, ro:][mask] = vals[mask]
+                v = kb.MatrixView(torch.from_numpy(host).cuda(), d + ro, d + ro, ld, kb.precision(tag)).submatrix(
+                    ro, ro, d, d)
+                x, y = naive.fill(rng, d, tag), naive.fill(rng, d, tag)
+                rep = kb.symv_hemv(uplo, 0.75, kb.HermitianView(v, uplo), dvec(x), 1.25, dvec(y))
+                herm = tag in "cz"
+                want = naive.naive_symv_hemv(0.75, tri, uplo, x, 1.25, y, hermitian=herm)
+                assert torch.isfinite(rep.y_out).all()
+                check(rep.y_out, want, tag, 0.75, np.abs(naive.dense_from_triangle(tri, uplo, herm)), x, 1.25, y)
