@@ -18,9 +18,16 @@ SYMV_FN = {("s", False): "ssymv", ("d", False): "dsymv", ("c", True): "chemv", (
            ("c", False): "csymv", ("z", False): "zsymv"}
 
 
+_CUDA_OK = False
+
+
 def require_cuda():
+    global _CUDA_OK
+    if _CUDA_OK:
+        return
     if not torch.cuda.is_available():
         raise RuntimeError("paper_1410_1726_b200 needs a CUDA device (sm_100a); none is visible")
+    _CUDA_OK = True
 
 
 def device_for(*objs) -> torch.device:
@@ -32,7 +39,15 @@ def device_for(*objs) -> torch.device:
     return torch.device("cuda", torch.cuda.current_device())
 
 
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def stream_handle(device) -> int:
+    """cudaStream_t of torch's current stream on `device` (the raw accessor
+    skips the Stream object construction, a few microseconds per call)."""
+    idx = device.index if isinstance(device, torch.device) else device
+    if _raw_stream is not None and idx is not None:
+        return _raw_stream(idx)
     return torch.cuda.current_stream(device).cuda_stream
 
 
@@ -92,15 +107,21 @@ def vector_in(v, length: int, prec: Precision, name: str, device) -> torch.Tenso
     arr = np.asarray(v, dtype=prec.dtype)
     if arr.ndim != 1 or arr.size != length:
         raise ValueError(f"{name} must be a vector of length {length}")
-    t = torch.from_numpy(np.ascontiguousarray(arr))
-    return t.to(device, non_blocking=t.is_pinned())
+    # non_blocking is safe for pageable memory too: the driver stages it
+    # before returning, so the caller may reuse the array immediately
+    return torch.from_numpy(np.ascontiguousarray(arr)).to(device, non_blocking=True)
 
 
 def result_like(y_in, y_out: torch.Tensor):
-    """numpy in -> numpy out (one D2H read); torch in -> torch out (stays in HBM)."""
+    """numpy in -> numpy out (one D2H read into a fresh page-locked buffer
+    from torch's caching host allocator, so the copy is a direct DMA);
+    torch in -> torch out (stays in HBM)."""
     if _is_torch(y_in):
         return y_out
-    return y_out.cpu().numpy()
+    h = torch.empty(y_out.shape, dtype=y_out.dtype, pin_memory=True)
+    h.copy_(y_out, non_blocking=True)
+    torch.cuda.current_stream(y_out.device).synchronize()
+    return h.numpy()
 
 
 def matrix_in(view: MatrixView, device, lower_tri: str | None = None):

@@ -440,12 +440,12 @@ cudaError_t tile_table(int d, int lead, bool lower, int W, int H, ColMap cm, int
   return cudaSuccess;
 }
 
-template <class T, int V, int NW, int CW, int R, bool LOWER, bool HERM>
+template <class T, int V, int NW, int CW, int R, bool LOWER, bool HERM, int MINB = 1>
 cudaError_t run_symv(const Path<T> &pa, long long lda, int d, const T *x, ColMap cm, int ncols_local, T *y,
                      T alpha, T beta, bool beta_zero, cudaStream_t st) {
   constexpr int H = 32 * V * R, W = NW * CW;
   constexpr size_t smem = 2 * (size_t)NW * H * sizeof(T);
-  auto kfn = symv_kernel<T, V, NW, CW, R, LOWER, HERM>;
+  auto kfn = symv_kernel<T, V, NW, CW, R, LOWER, HERM, MINB>;
   {
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
@@ -656,6 +656,11 @@ cudaError_t dispatch_symv_h(bool lower, const Path<T> &pa, long long lda, int d,
     case 102: KB_REG(C::V, 8, (sizeof(T) == 16 ? 8 : 16), 1);  // 8 warps, wider per-warp column sets
     case 103: KB_REG(C::V, 8, 4, 1);                           // 8 warps x 4 columns (small operands)
     case 104: KB_REG(C::V, 8, 8, 1);                           // 8 warps x 8 columns
+    case 105:                                                  // 8 warps x 8 columns, 2 CTAs per SM
+      return lower ? run_symv<T, C::V, 8, (sizeof(T) == 16 ? 4 : 8), 1, true, HERM, 2>(
+                         pa, lda, d, x, cm, ncols_local, y, alpha, beta, beta_zero, st)
+                   : run_symv<T, C::V, 8, (sizeof(T) == 16 ? 4 : 8), 1, false, HERM, 2>(
+                         pa, lda, d, x, cm, ncols_local, y, alpha, beta, beta_zero, st);
     default: KB_REG(C::V, C::S_NW, C::S_CW, C::S_R);
   }
 #undef KB_REG

@@ -512,8 +512,8 @@ __device__ __forceinline__ int sym_start_tile(const SymParams &p, long long) {
   return p.start_tile[blockIdx.x];
 }
 
-template <class T, int V, int NW, int CW, int R, bool LOWER, bool HERM>
-__global__ void __launch_bounds__(NW * 32, 1) symv_kernel(const SymParams p) {
+template <class T, int V, int NW, int CW, int R, bool LOWER, bool HERM, int MINB = 1>
+__global__ void __launch_bounds__(NW * 32, MINB) symv_kernel(const SymParams p) {
   griddep_launch_dependents();
   constexpr int NT = NW * 32;
   constexpr int H = 32 * V * R;

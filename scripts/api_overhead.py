@@ -43,3 +43,15 @@ print("kb.symv_hemv torch in/out  %.1f us" % per_call(lambda: kb.symv_hemv("l", 
 print("kb.symv_hemv inplace       %.1f us" % per_call(lambda: kb.symv_hemv("l", 1.0, hv, x, 0.0, y, inplace=True)))
 print("kb.symv_hemv numpy x,y     %.1f us" % per_call(lambda: kb.symv_hemv("l", 1.0, hv, hx, 0.0, hy), 500))
 print("kb.gemv torch in/out       %.1f us" % per_call(lambda: kb.gemv("n", 1.0, v, x, 0.0, y)))
+
+if len(sys.argv) > 1 and sys.argv[1] == "profile":
+    import cProfile
+    import pstats
+
+    pr = cProfile.Profile()
+    pr.enable()
+    for _ in range(2000):
+        kb.symv_hemv("l", 1.0, hv, hx, 0.0, hy)
+    torch.cuda.synchronize()
+    pr.disable()
+    pstats.Stats(pr).sort_stats("tottime").print_stats(25)
