@@ -292,6 +292,21 @@ int kblas_getmatrix_async(int rows, int cols, size_t esize, const void *dA, int 
 /* ------------------------------------------------------------------ */
 /* Instrumentation (bench/test harness).                               */
 /* ------------------------------------------------------------------ */
+/* Host-vector form of every single-GPU entry point (the path the      */
+/* Python API takes for numpy vectors): A is in HBM; x, y_in and y_out  */
+/* are HOST arrays.  prec in {s,d,c,z}; kind 'g' (gemv: op = trans,    */
+/* offsets (offset_r, offset_c) as kblas_xgemv_offset) or 's'           */
+/* (symv/hemv: op = uplo, hermitian selects HEMV for c/z, offset_r ==   */
+/* offset_c = the diagonal offset).  alpha/beta point to one scalar of  */
+/* the precision.  y_in may be NULL when *beta == 0.  Enqueues the      */
+/* H2D copies, the kernels and the D2H copy on `stream` and waits for  */
+/* it.  Same return codes as the entry points it wraps (-1: bad vector  */
+/* arguments).  Replaces blockmv's numpy-in/numpy-out call shape        */
+/* (kernels.py:402-440, 443-486; offset.py:83-208).                     */
+int kblas_mv_hostvec(char prec, char kind, char op, int hermitian, int m, int n,
+                     const void *alpha, const void *dA, int lda, int offset_r,
+                     int offset_c, const void *x, const void *beta,
+                     const void *y_in, void *y_out, cudaStream_t stream);
 /* Number of kernels this library has launched since load.             */
 unsigned long long kblas_launch_count(void);
 /* When enabled, the library brackets every main (matrix-streaming)    */

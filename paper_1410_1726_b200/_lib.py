@@ -106,6 +106,11 @@ def load():
             c_int, c_int, c_int, c_int, c_void_p,
         ]
         lib.kblas_mv_mgpu_partial_async.restype = c_int
+        lib.kblas_mv_hostvec.argtypes = [
+            c_char, c_char, c_char, c_int, c_int, c_int, c_void_p, c_void_p, c_int, c_int, c_int,
+            c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+        ]
+        lib.kblas_mv_hostvec.restype = c_int
         lib.kblas_mgpu_local_cols.argtypes = [c_int, c_int, c_int, c_int]
         lib.kblas_mgpu_local_cols.restype = c_int
         lib.kblas_mgpu_local_ld.argtypes = [c_int]

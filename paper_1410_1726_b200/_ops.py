@@ -193,3 +193,39 @@ def call_symv(prec: Precision, hermitian: bool, uplo: str, d: int, alpha, a_ptr:
                _lib.scalar(prec.tag, beta), y.data_ptr(), 1, offset, stream_handle(device))
     _lib.check(rc, f"kblas_{name}_offset",
                ["uplo", "n", "alpha", "A", "lda", "x", "incx", "beta", "y", "incy", "offset"])
+
+
+def host_vectors(x, y, inplace: bool) -> bool:
+    """numpy (host) x and y: the call goes through kblas_mv_hostvec."""
+    return not inplace and not _is_torch(x) and not _is_torch(y)
+
+
+def call_hostvec(prec: Precision, kind: str, op: str, hermitian: bool, m: int, n: int, alpha, a_ptr: int,
+                 lda: int, x, x_len: int, beta, y, y_len: int, device, off_r: int = 0, off_c: int = 0):
+    """One FFI crossing for a numpy-vector call: H2D of x (and y when beta
+    != 0), the kernels, D2H of the result into a fresh page-locked buffer
+    (torch's caching host allocator), wait.  Returns the numpy result."""
+    xa = np.ascontiguousarray(np.asarray(x, dtype=prec.dtype))
+    if xa.ndim != 1 or xa.size != x_len:
+        raise ValueError(f"x must be a vector of length {x_len}")
+    bz = complex(beta) == 0
+    ya = None
+    if bz:
+        if length_of(y) != y_len:
+            raise ValueError(f"y must be a vector of length {y_len}")
+    else:
+        ya = np.ascontiguousarray(np.asarray(y, dtype=prec.dtype))
+        if ya.ndim != 1 or ya.size != y_len:
+            raise ValueError(f"y must be a vector of length {y_len}")
+    out = torch.empty(y_len, dtype=prec.torch_dtype, pin_memory=True)
+    a_c, b_c = _lib.scalar(prec.tag, alpha), _lib.scalar(prec.tag, beta)
+    import ctypes
+
+    with _on_device(device):
+        rc = _fn("kblas_mv_hostvec")(prec.tag.encode(), kind.encode(), op.encode(), 1 if hermitian else 0, m, n,
+                                     ctypes.addressof(a_c), a_ptr, lda, off_r, off_c, xa.ctypes.data,
+                                     ctypes.addressof(b_c), None if ya is None else ya.ctypes.data,
+                                     out.data_ptr(), stream_handle(device))
+    _lib.check(rc, "kblas_mv_hostvec")
+    return out.numpy()
+

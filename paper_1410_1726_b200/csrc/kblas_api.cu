@@ -280,7 +280,7 @@ cudaError_t run_gemv_n(const Path<T> &pa, long long lda, int m, int n, const T *
     const long long S = std::max<long long>(
         1, std::min<long long>({cdiv(Ps, nrb_s), kSplitMaxSlots, std::max<long long>(1, n / (NWs * CWs))}));
     const bool fills = nrb_s * S >= dev_sms();
-    const bool small = (long long)m * n * (long long)sizeof(T) <= (512LL << 20);
+    const bool small = (long long)m * n * (long long)sizeof(T) <= (80LL << 20);
     if (g_gemv_split == 1 || (g_gemv_split == -1 && !fused && fills && small))
       return run_gemv_ns<T, V, NWs, CWs>(pa, lda, m, n, x, cm, y, alpha, beta, beta_zero, st, S, nrb_s);
   }
@@ -843,6 +843,62 @@ int mgpu_entry(bool is_gemv, char op, bool herm, int m, int n, T alpha, T *const
   return code(e);
 }
 
+// Host-vector call: x (and y when beta != 0) are host arrays, A is in HBM.
+// One entry enqueues H2D of the vectors into a per-(device, stream) staging
+// pair, the kernels, and the D2H of the result, then waits for the stream.
+// This is the path the Python API takes for numpy vectors (one crossing of
+// the FFI per call instead of a handful of tensor operations).
+std::map<std::pair<int, cudaStream_t>, WsBuf> g_vecs;
+
+cudaError_t vec_staging(size_t bytes, cudaStream_t st, void **out) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_mu);
+  WsBuf &b = g_vecs[{dev, st}];
+  if (b.bytes < bytes) {
+    if (b.ptr) {
+      cudaStreamSynchronize(st);
+      cudaFree(b.ptr);
+      b.ptr = nullptr;
+      b.bytes = 0;
+    }
+    cudaError_t e = cudaMalloc(&b.ptr, bytes * 2);
+    if (e != cudaSuccess) { b.ptr = nullptr; return e; }
+    b.bytes = bytes * 2;
+  }
+  *out = b.ptr;
+  return cudaSuccess;
+}
+
+template <class T>
+int hostvec_entry(bool is_gemv, char op, bool herm, int m, int n, T alpha, const T *dA, int lda,
+                         int off_r, int off_c, const T *hx, T beta, const T *hy_in, T *hy_out, cudaStream_t st) {
+  const char o = (char)(op | 0x20);
+  const bool tr = is_gemv && o != 'n';
+  const long long xlen = is_gemv ? (tr ? m : n) : n;
+  const long long ylen = is_gemv ? (tr ? n : m) : n;
+  if (xlen < 0 || ylen < 0 || hx == nullptr || hy_out == nullptr) return -1;
+  const bool bz = is_zero(beta);
+  if (!bz && hy_in == nullptr) return -1;
+  void *stage = nullptr;
+  const size_t xb = align256((size_t)std::max<long long>(xlen, 1) * sizeof(T));
+  cudaError_t e = vec_staging(xb + (size_t)std::max<long long>(ylen, 1) * sizeof(T), st, &stage);
+  if (e != cudaSuccess) return (int)e;
+  T *dx = static_cast<T *>(stage);
+  T *dy = reinterpret_cast<T *>(static_cast<char *>(stage) + xb);
+  if (xlen > 0 && (e = cudaMemcpyAsync(dx, hx, xlen * sizeof(T), cudaMemcpyHostToDevice, st)) != cudaSuccess)
+    return (int)e;
+  if (!bz && ylen > 0 &&
+      (e = cudaMemcpyAsync(dy, hy_in, ylen * sizeof(T), cudaMemcpyHostToDevice, st)) != cudaSuccess)
+    return (int)e;
+  const int rc = is_gemv ? gemv_entry<T>(o, m, n, alpha, dA, lda, dx, 1, beta, dy, 1, off_r, off_c, st)
+                         : symv_entry<T>(o, herm, n, alpha, dA, lda, dx, 1, beta, dy, 1, off_r, st);
+  if (rc != 0) return rc;
+  if (ylen > 0 && (e = cudaMemcpyAsync(hy_out, dy, ylen * sizeof(T), cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+    return (int)e;
+  return code(cudaStreamSynchronize(st));
+}
+
 }  // namespace
 
 // ====================================================================
@@ -988,6 +1044,21 @@ int kblas_getmatrix_async(int rows, int cols, size_t esize, const void *dA, int 
   if (rows == 0 || cols == 0) return 0;
   return code(cudaMemcpy2DAsync(hA, (size_t)ldha * esize, dA, (size_t)ldda * esize, (size_t)rows * esize,
                                 (size_t)cols, cudaMemcpyDeviceToHost, stream));
+}
+
+int kblas_mv_hostvec(char prec, char kind, char op, int hermitian, int m, int n, const void *alpha,
+                     const void *dA, int lda, int offset_r, int offset_c, const void *hx, const void *beta,
+                     const void *hy_in, void *hy_out, cudaStream_t stream) {
+  const bool g = (kind | 0x20) == 'g';
+  if (!g && (kind | 0x20) != 's') return -2;
+  if (!g && offset_r != offset_c) return -11;
+  switch (prec | 0x20) {
+    case 's': return hostvec_entry<float>(g, op, false, m, n, *(const float *)alpha, (const float *)dA, lda, offset_r, offset_c, (const float *)hx, *(const float *)beta, (const float *)hy_in, (float *)hy_out, stream);
+    case 'd': return hostvec_entry<double>(g, op, false, m, n, *(const double *)alpha, (const double *)dA, lda, offset_r, offset_c, (const double *)hx, *(const double *)beta, (const double *)hy_in, (double *)hy_out, stream);
+    case 'c': return hostvec_entry<float2>(g, op, hermitian != 0, m, n, *(const float2 *)alpha, (const float2 *)dA, lda, offset_r, offset_c, (const float2 *)hx, *(const float2 *)beta, (const float2 *)hy_in, (float2 *)hy_out, stream);
+    case 'z': return hostvec_entry<double2>(g, op, hermitian != 0, m, n, *(const double2 *)alpha, (const double2 *)dA, lda, offset_r, offset_c, (const double2 *)hx, *(const double2 *)beta, (const double2 *)hy_in, (double2 *)hy_out, stream);
+  }
+  return -1;
 }
 
 unsigned long long kblas_launch_count(void) { return g_launches.load(); }

@@ -87,11 +87,21 @@ def _is_one(v) -> bool:
     return complex(v) == 1
 
 
+_PLAN_CACHE: dict = {}
+
+
 def plan_counters(plan: str) -> tuple[int, int]:
-    """(CTAs of the main kernel, partial slots) parsed from kblas_last_plan()."""
+    """(CTAs of the main kernel, partial slots) parsed from kblas_last_plan()
+    (memoised: a shape's plan string repeats from call to call)."""
+    hit = _PLAN_CACHE.get(plan)
+    if hit is not None:
+        return hit
     p = re.search(r"\bP=(\d+)", plan)
     s = re.search(r"\bslots=(\d+)", plan)
-    return (int(p.group(1)) if p else 0, int(s.group(1)) if s else 0)
+    res = (int(p.group(1)) if p else 0, int(s.group(1)) if s else 0)
+    if len(_PLAN_CACHE) < 4096:
+        _PLAN_CACHE[plan] = res
+    return res
 
 
 def fill_report(rep: ExecutionReport, prec: Precision, mat_elems: int, x_len: int, y_len: int,
@@ -129,6 +139,8 @@ def gemv(trans: str, alpha, a: MatrixView, x, beta, y, config: KernelConfig = DE
         trans = "t"
     x_len, y_len = (a.cols, a.rows) if trans == "n" else (a.rows, a.cols)
     dev = _ops.device_for(a, y, x)
+    if _ops.host_vectors(x, y, inplace) and not _is_zero(alpha):
+        return _gemv_hostvec(trans, alpha, a, x, beta, y, prec, x_len, y_len, dev)
     xd = _ops.vector_in(x, x_len, prec, "x", dev)
     if _is_zero(alpha) and _is_one(beta):
         yd = _ops.vector_in(y, y_len, prec, "y", dev)
@@ -153,6 +165,20 @@ def gemv(trans: str, alpha, a: MatrixView, x, beta, y, config: KernelConfig = DE
     return rep
 
 
+def _gemv_hostvec(trans, alpha, a: MatrixView, x, beta, y, prec, x_len, y_len, dev) -> ExecutionReport:
+    """numpy x and y: one kblas_mv_hostvec call (copies, kernels, result)."""
+    ptr, lda, keep = _ops.matrix_in(a, dev)
+    y_out = _ops.call_hostvec(prec, "g", trans, False, a.rows, a.cols, alpha, ptr, lda, x, x_len, beta, y, y_len,
+                              dev)
+    rep = ExecutionReport()
+    fill_report(rep, prec, a.rows * a.cols, x_len, y_len, _is_zero(beta),
+                roofline.gemv_flops(prec, a.rows, a.cols, trans), _lib.last_plan())
+    rep.scal_invocations = 1
+    rep.y_out = y_out
+    del keep
+    return rep
+
+
 def symv_hemv(uplo: str, alpha, a: HermitianView, x, beta, y, config: KernelConfig = DEFAULT_CONFIG,
               hermitian: bool | None = None, inplace: bool = False) -> ExecutionReport:
     """y = alpha * A x + beta * y from one stored triangle (kernels.py:443-486)."""
@@ -170,6 +196,16 @@ def symv_hemv(uplo: str, alpha, a: HermitianView, x, beta, y, config: KernelConf
         raise ValueError("hermitian treatment requires a complex precision")
     d = a.dim
     dev = _ops.device_for(a.base, y, x)
+    if _ops.host_vectors(x, y, inplace) and not _is_zero(alpha):
+        # numpy x and y: one kblas_mv_hostvec call (copies, kernels, result)
+        ptr, lda, keep = _ops.matrix_in(a.base, dev, lower_tri=uplo)
+        y_out = _ops.call_hostvec(prec, "s", uplo, hermitian, d, d, alpha, ptr, lda, x, d, beta, y, d, dev)
+        rep = ExecutionReport()
+        fill_report(rep, prec, d * (d + 1) // 2, d, d, _is_zero(beta), roofline.symv_flops(prec, d),
+                    _lib.last_plan())
+        rep.y_out = y_out
+        del keep
+        return rep
     xd = _ops.vector_in(x, d, prec, "x", dev)
     if _is_zero(alpha) and _is_one(beta):
         yd = _ops.vector_in(y, d, prec, "y", dev)

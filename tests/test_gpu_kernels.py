@@ -535,3 +535,62 @@ class TestSymvTiles:
                 want = naive.naive_symv_hemv(0.75, tri, uplo, x, 1.25, y, hermitian=herm)
                 assert torch.isfinite(rep.y_out).all()
                 check(rep.y_out, want, tag, 0.75, np.abs(naive.dense_from_triangle(tri, uplo, herm)), x, 1.25, y)
+
+
+class TestHostVectorPath:
+    """numpy x and y with an HBM-resident matrix go through one
+    kblas_mv_hostvec call (H2D, kernels, D2H); results must equal the
+    torch-vector path bit for bit and match the oracle."""
+
+    @pytest.mark.parametrize("tag", "sdcz")
+    def test_gemv_numpy_vectors(self, tag):
+        rng = np.random.default_rng(151)
+        v, a = dev_matrix(rng, 700, 450, tag, ld=704)
+        for trans in "ntc":
+            for beta in (0.0, -0.5):
+                xl, yl = (450, 700) if trans == "n" else (700, 450)
+                x, y = naive.fill(rng, xl, tag), naive.fill(rng, yl, tag)
+                if beta == 0.0:
+                    y = np.full(yl, np.nan, dtype=naive.DTYPES[tag])
+                rep = kb.gemv(trans, 1.5, v, x, beta, y)
+                assert isinstance(rep.y_out, np.ndarray) and rep.y_out.dtype == naive.DTYPES[tag]
+                ref = kb.gemv(trans, 1.5, v, dvec(x), beta, dvec(y)).y_out.cpu().numpy()
+                assert np.array_equal(rep.y_out, ref)
+                dense = np.abs(a) if trans == "n" else np.abs(a).T
+                yy = np.zeros(yl, naive.DTYPES[tag]) if beta == 0.0 else y
+                check(rep.y_out, naive.naive_gemv(trans, 1.5, a, x, beta, yy), tag, 1.5, dense, x, beta, yy)
+
+    @pytest.mark.parametrize("tag", "sdcz")
+    @pytest.mark.parametrize("uplo", "lu")
+    def test_symv_numpy_vectors(self, tag, uplo):
+        rng = np.random.default_rng(152)
+        d = 900
+        v, a = dev_matrix(rng, d, d, tag)
+        herm = tag in "cz"
+        x, y = naive.fill(rng, d, tag), naive.fill(rng, d, tag)
+        hv = kb.HermitianView(v, uplo)
+        rep = kb.symv_hemv(uplo, 0.5, hv, x, 2.0, y)
+        ref = kb.symv_hemv(uplo, 0.5, hv, dvec(x), 2.0, dvec(y)).y_out.cpu().numpy()
+        assert np.array_equal(rep.y_out, ref)
+        tri = np.tril(a) if uplo == "l" else np.triu(a)
+        want = naive.naive_symv_hemv(0.5, tri, uplo, x, 2.0, y, hermitian=herm)
+        check(rep.y_out, want, tag, 0.5, np.abs(naive.dense_from_triangle(tri, uplo, herm)), x, 2.0, y)
+        assert rep.flops > 0 and rep.plan.startswith("symv")
+
+    def test_inputs_not_mutated_and_errors(self):
+        rng = np.random.default_rng(153)
+        v, a = dev_matrix(rng, 300, 200, "d")
+        x, y = naive.fill(rng, 200, "d"), naive.fill(rng, 300, "d")
+        x0, y0 = x.copy(), y.copy()
+        kb.gemv("n", 1.0, v, x, 1.0, y)
+        assert np.array_equal(x, x0) and np.array_equal(y, y0)
+        with pytest.raises(ValueError):
+            kb.gemv("n", 1.0, v, x[:10], 1.0, y)
+        with pytest.raises(ValueError):
+            kb.gemv("n", 1.0, v, x, 1.0, y[:10])
+        lib = _lib.load()
+        one = ctypes.c_double(1.0)
+        assert lib.kblas_mv_hostvec(b"d", b"q", b"n", 0, 4, 4, ctypes.addressof(one), v.data.data_ptr(), 300, 0, 0,
+                                    x.ctypes.data, ctypes.addressof(one), y.ctypes.data, y.ctypes.data, None) == -2
+        assert lib.kblas_mv_hostvec(b"d", b"g", b"n", 0, 4, 4, ctypes.addressof(one), v.data.data_ptr(), 300, 0, 0,
+                                    None, ctypes.addressof(one), y.ctypes.data, y.ctypes.data, None) == -1
