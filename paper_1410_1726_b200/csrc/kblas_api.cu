@@ -221,9 +221,12 @@ template <class T> struct Cfg {
   static constexpr int V = 32 / sizeof(T);
   // gemv N / T (register double-buffered: 2 x CW x R loads in flight per lane)
   static constexpr int G_NW = 8, G_CW = 4, G_R = 1, G_RS = V;
-  // symv / hemv: W = S_NW * S_CW columns per tile (the t1 partial traffic
-  // is 2/W of the triangle); z halves CW to stay within 128 registers
-  static constexpr int S_NW = 16, S_CW = sizeof(T) == 16 ? 4 : 8, S_R = 1, S_RS = V;
+  // symv / hemv: W = S_NW * S_CW = 128 columns per tile (the t1 partial
+  // traffic is 2/W of the triangle); z keeps the tile's x_col values in
+  // shared memory (S_XS) to fit 8 columns per warp in 128 registers
+  // (+4-6 % over 4 columns per warp, profiles/r1h_tune_symv_xs_variant108.jsonl)
+  static constexpr int S_NW = 16, S_CW = 8, S_R = 1, S_RS = V;
+  static constexpr bool S_XS = sizeof(T) == 16;
 
 };
 
@@ -440,12 +443,12 @@ cudaError_t tile_table(int d, int lead, bool lower, int W, int H, ColMap cm, int
   return cudaSuccess;
 }
 
-template <class T, int V, int NW, int CW, int R, bool LOWER, bool HERM, int MINB = 1>
+template <class T, int V, int NW, int CW, int R, bool LOWER, bool HERM, int MINB = 1, bool XS = false>
 cudaError_t run_symv(const Path<T> &pa, long long lda, int d, const T *x, ColMap cm, int ncols_local, T *y,
                      T alpha, T beta, bool beta_zero, cudaStream_t st) {
   constexpr int H = 32 * V * R, W = NW * CW;
   constexpr size_t smem = 2 * (size_t)NW * H * sizeof(T);
-  auto kfn = symv_kernel<T, V, NW, CW, R, LOWER, HERM, MINB>;
+  auto kfn = symv_kernel<T, V, NW, CW, R, LOWER, HERM, MINB, XS>;
   {
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
@@ -645,7 +648,11 @@ cudaError_t dispatch_symv_h(bool lower, const Path<T> &pa, long long lda, int d,
   return lower ? run_symv<T, V, NW, CW, R, true, HERM>(pa, lda, d, x, cm, ncols_local, y, alpha, beta, beta_zero, \
                                                        st)                                                     \
                : run_symv<T, V, NW, CW, R, false, HERM>(pa, lda, d, x, cm, ncols_local, y, alpha, beta, beta_zero, st)
-  if (!pa.vec) KB_REG(1, C::S_NW, C::S_CW, C::S_RS);
+  if (!pa.vec)  // odd ld: one element per lane
+    return lower ? run_symv<T, 1, C::S_NW, C::S_CW, C::S_RS, true, HERM, 1, C::S_XS>(
+                       pa, lda, d, x, cm, ncols_local, y, alpha, beta, beta_zero, st)
+                 : run_symv<T, 1, C::S_NW, C::S_CW, C::S_RS, false, HERM, 1, C::S_XS>(
+                       pa, lda, d, x, cm, ncols_local, y, alpha, beta, beta_zero, st);
   // register-kernel tuning variants (kblas_set_symv_variant 100+); small
   // operands use narrow tiles (variant 103, W = 32 columns, 16 for z) so
   // there are enough items to occupy every SM
@@ -656,12 +663,21 @@ cudaError_t dispatch_symv_h(bool lower, const Path<T> &pa, long long lda, int d,
     case 102: KB_REG(C::V, 8, (sizeof(T) == 16 ? 8 : 16), 1);  // 8 warps, wider per-warp column sets
     case 103: KB_REG(C::V, 8, 4, 1);                           // 8 warps x 4 columns (small operands)
     case 104: KB_REG(C::V, 8, 8, 1);                           // 8 warps x 8 columns
+    case 108:                                                  // 16 warps x 8 columns, x_col in shared memory
+      return lower ? run_symv<T, C::V, 16, 8, 1, true, HERM, 1, true>(pa, lda, d, x, cm, ncols_local, y, alpha,
+                                                                      beta, beta_zero, st)
+                   : run_symv<T, C::V, 16, 8, 1, false, HERM, 1, true>(pa, lda, d, x, cm, ncols_local, y, alpha,
+                                                                       beta, beta_zero, st);
     case 105:                                                  // 8 warps x 8 columns, 2 CTAs per SM
       return lower ? run_symv<T, C::V, 8, (sizeof(T) == 16 ? 4 : 8), 1, true, HERM, 2>(
                          pa, lda, d, x, cm, ncols_local, y, alpha, beta, beta_zero, st)
                    : run_symv<T, C::V, 8, (sizeof(T) == 16 ? 4 : 8), 1, false, HERM, 2>(
                          pa, lda, d, x, cm, ncols_local, y, alpha, beta, beta_zero, st);
-    default: KB_REG(C::V, C::S_NW, C::S_CW, C::S_R);
+    default:
+      return lower ? run_symv<T, C::V, C::S_NW, C::S_CW, C::S_R, true, HERM, 1, C::S_XS>(
+                         pa, lda, d, x, cm, ncols_local, y, alpha, beta, beta_zero, st)
+                   : run_symv<T, C::V, C::S_NW, C::S_CW, C::S_R, false, HERM, 1, C::S_XS>(
+                         pa, lda, d, x, cm, ncols_local, y, alpha, beta, beta_zero, st);
   }
 #undef KB_REG
 }

@@ -512,7 +512,10 @@ __device__ __forceinline__ int sym_start_tile(const SymParams &p, long long) {
   return p.start_tile[blockIdx.x];
 }
 
-template <class T, int V, int NW, int CW, int R, bool LOWER, bool HERM, int MINB = 1>
+// XS: keep the tile's x_col values in shared memory (each warp its own CW
+// slots, so no extra barrier) instead of CW registers per thread, which
+// frees registers for wider per-warp column sets.
+template <class T, int V, int NW, int CW, int R, bool LOWER, bool HERM, int MINB = 1, bool XS = false>
 __global__ void __launch_bounds__(NW * 32, MINB) symv_kernel(const SymParams p) {
   griddep_launch_dependents();
   constexpr int NT = NW * 32;
@@ -573,12 +576,24 @@ __global__ void __launch_bounds__(NW * 32, MINB) symv_kernel(const SymParams p) 
 
   SymTile tl = p.tiles[k];
   long long tnext = (k + 1 < p.ntiles) ? p.tiles[k + 1].prefix : p.total;
-  T xc[CW], t2[CW];
+  T t2[CW];
+  __shared__ T xs_buf[XS ? NW * CW : 1];
+  T xr_c[XS ? 1 : CW];  // x_col in registers (!XS)
+  auto set_xc = [&](const SymTile &t) {
+    if constexpr (XS) {
+      if (lane < CW) xs_buf[cl + lane] = (cl + lane < t.ncols) ? __ldg(x + t.gcol0 + cl + lane) : zero<T>();
+      __syncwarp();
+    } else {
 #pragma unroll
-  for (int j = 0; j < CW; ++j) {
-    xc[j] = (cl + j < tl.ncols) ? __ldg(x + tl.gcol0 + cl + j) : zero<T>();
-    t2[j] = zero<T>();
-  }
+      for (int j = 0; j < CW; ++j) xr_c[j] = (cl + j < t.ncols) ? __ldg(x + t.gcol0 + cl + j) : zero<T>();
+    }
+  };
+  auto xcj = [&](int j) -> T {
+    if constexpr (XS) return xs_buf[cl + j]; else return xr_c[j];
+  };
+  set_xc(tl);
+#pragma unroll
+  for (int j = 0; j < CW; ++j) t2[j] = zero<T>();
   load(tl, it0);
   int buf = 0;
   for (long long q = it0; q < end; ++q) {
@@ -600,7 +615,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) symv_kernel(const SymParams p) 
 #pragma unroll
           for (int v = 0; v < V; ++v) {
             const T e = a[j][r].v(v);
-            acc[r][v] = fma_(e, xc[j], acc[r][v]);
+            acc[r][v] = fma_(e, xcj(j), acc[r][v]);
             t2[j] = fmax_<HERM>(e, xr[r][v], t2[j]);
           }
     } else if (!diag) {
@@ -615,7 +630,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) symv_kernel(const SymParams p) 
 #pragma unroll
           for (int j = 0; j < CW; ++j) {
             const T e = sel(ok, a[j][r].v(v));
-            acc[r][v] = fma_(e, xc[j], acc[r][v]);
+            acc[r][v] = fma_(e, xcj(j), acc[r][v]);
             t2[j] = fmax_<HERM>(e, xr[r][v], t2[j]);
           }
         }
@@ -634,7 +649,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) symv_kernel(const SymParams p) 
             const bool in2 = ok && (LOWER ? i > c : i < c);
             T e1 = sel(in1, a[j][r].v(v));
             if (HERM && i == c) e1 = realify(e1);
-            acc[r][v] = fma_(e1, xc[j], acc[r][v]);
+            acc[r][v] = fma_(e1, xcj(j), acc[r][v]);
             t2[j] = fmax_<HERM>(sel(in2, a[j][r].v(v)), xr[r][v], t2[j]);
           }
       }
@@ -658,8 +673,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) symv_kernel(const SymParams p) 
         ++k;
         tl = p.tiles[k];
         tnext = (k + 1 < p.ntiles) ? p.tiles[k + 1].prefix : p.total;
-#pragma unroll
-        for (int j = 0; j < CW; ++j) xc[j] = (cl + j < tl.ncols) ? __ldg(x + tl.gcol0 + cl + j) : zero<T>();
+        set_xc(tl);
       }
       load(tl, q + 1);  // in flight during the reduction below
     }
