@@ -331,6 +331,10 @@ int kblas_set_symv_variant(int variant);
 /* matrices; the stacked-rows stream-K form otherwise), 1 = always the */
 /* split form, 0 = never.  Returns the previous mode.                  */
 int kblas_set_gemv_split(int mode);
+/* Tuning hook for the stacked GEMV-N and the GEMV-T/C kernel shapes     */
+/* (warps, columns per warp, vectors per lane, CTAs per SM); 0 = tuned   */
+/* default.  Returns the previous variant.                               */
+int kblas_set_gemv_variant(int variant);
 /* Register SYMV/HEMV kernel: orders up to max_order use narrow column */
 /* tiles (more work items for small operands).  Returns the previous   */
 /* threshold (default 2048).                                           */

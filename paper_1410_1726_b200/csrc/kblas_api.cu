@@ -234,6 +234,7 @@ template <class T> struct Cfg {
 // Split-form GEMV-N (gemv_ns_kernel) choice: -1 auto, 0 never, 1 always
 // (kblas_set_gemv_split, for the tuner).
 int g_gemv_split = -1;
+int g_gemv_variant = 0;  // 0: tuned default shape (kblas_set_gemv_variant)
 constexpr long long kSplitMaxSlots = 64;
 
 template <class T, int V, int NW, int CW>
@@ -260,11 +261,11 @@ cudaError_t run_gemv_ns(const Path<T> &pa, long long lda, int m, int n, const T 
   return cudaGetLastError();
 }
 
-template <class T, int V, int NW, int CW, int R>
+template <class T, int V, int NW, int CW, int R, int MINB = 2>
 cudaError_t run_gemv_n(const Path<T> &pa, long long lda, int m, int n, const T *x, ColMap cm, T *y,
                        T alpha, T beta, bool beta_zero, cudaStream_t st) {
   constexpr int RB = NW * 32 * V * R;
-  auto kfn = gemv_n_kernel<T, V, NW, CW, R>;
+  auto kfn = gemv_n_kernel<T, V, NW, CW, R, MINB>;
   const long long nrb = cdiv((long long)pa.lead + m, RB);
   const long long KS = cdiv(n, CW);
   const long long total = nrb * KS;
@@ -312,11 +313,11 @@ cudaError_t run_gemv_n(const Path<T> &pa, long long lda, int m, int n, const T *
 }
 
 // ============================================================= GEMV-T/C
-template <class T, int V, int NW, int CW, int R, bool CONJ>
+template <class T, int V, int NW, int CW, int R, bool CONJ, int MINB = 2>
 cudaError_t run_gemv_t(const Path<T> &pa, long long lda, int m, int n, long long nglob, const T *x,
                        ColMap cm, T *y, T alpha, T beta, bool beta_zero, cudaStream_t st) {
   constexpr int H = 32 * V * R, CBW = NW * CW;
-  auto kfn = gemv_t_kernel<T, V, NW, CW, R, CONJ>;
+  auto kfn = gemv_t_kernel<T, V, NW, CW, R, CONJ, MINB>;
   const long long ncb = cdiv(n, CBW);
   const long long KS = cdiv((long long)pa.lead + m, H);
   const long long total = ncb * KS;
@@ -601,6 +602,27 @@ template <class T>
 cudaError_t dispatch_gemv(char trans, const Path<T> &pa, long long lda, int m, int n, long long nglob,
                           const T *x, ColMap cm, T *y, T alpha, T beta, bool beta_zero, cudaStream_t st) {
   using C = Cfg<T>;
+  // tuned per-precision shapes (profiles/r1j_tune_gemv_*.jsonl): S uses 16
+  // warps at 1 CTA/SM (variant 4), Z GEMV-N 4 warps x 4 columns x 2 vectors
+  // per lane (variant 3); D, C and Z-T/C keep the 8 x 4 x 1 default
+  int gv = g_gemv_variant;
+  if (gv == 0) gv = sizeof(T) == 4 ? 4 : (sizeof(T) == 16 && trans == 'n') ? 3 : 0;
+  if (pa.vec && gv > 0) {
+    // tuning variants (kblas_set_gemv_variant): (warps, columns per warp,
+    // vectors per lane per column, CTAs per SM)
+#define KB_GV(NW, CW, R, MB)                                                                                  \
+  if (trans == 'n') return run_gemv_n<T, C::V, NW, CW, R, MB>(pa, lda, m, n, x, cm, y, alpha, beta, beta_zero, st); \
+  if (trans == 'c' && is_cplx<T>())                                                                          \
+    return run_gemv_t<T, C::V, NW, CW, R, true, MB>(pa, lda, m, n, nglob, x, cm, y, alpha, beta, beta_zero, st);   \
+  return run_gemv_t<T, C::V, NW, CW, R, false, MB>(pa, lda, m, n, nglob, x, cm, y, alpha, beta, beta_zero, st);
+    switch (gv) {
+      case 1: KB_GV(4, 4, 1, 4)
+      case 2: KB_GV(8, 2, 2, 2)
+      case 3: KB_GV(4, 4, 2, 2)
+      default: KB_GV(16, 4, 1, 1)
+    }
+#undef KB_GV
+  }
   if (trans == 'n') {
     if (pa.vec) return run_gemv_n<T, C::V, C::G_NW, C::G_CW, C::G_R>(pa, lda, m, n, x, cm, y, alpha, beta, beta_zero, st);
     return run_gemv_n<T, 1, C::G_NW, C::G_CW, C::G_RS>(pa, lda, m, n, x, cm, y, alpha, beta, beta_zero, st);
@@ -1120,6 +1142,12 @@ int kblas_set_symv_variant(int v) {
 int kblas_set_symv_narrow(int max_order) {
   const int prev = g_symv_narrow_max;
   g_symv_narrow_max = max_order;
+  return prev;
+}
+
+int kblas_set_gemv_variant(int v) {
+  const int prev = g_gemv_variant;
+  g_gemv_variant = v;
   return prev;
 }
 

@@ -144,8 +144,8 @@ __device__ __forceinline__ void cta_slot_sum(const T *ws, long long ld, long lon
 // item's FMAs (register double buffering, as the paper's Alg. 1 does with
 // its two half-block buffers).
 // ---------------------------------------------------------------------------
-template <class T, int V, int NW, int CW, int R>
-__global__ void __launch_bounds__(NW * 32, 2) gemv_n_kernel(const GemvParams p) {
+template <class T, int V, int NW, int CW, int R, int MINB = 2>
+__global__ void __launch_bounds__(NW * 32, MINB) gemv_n_kernel(const GemvParams p) {
   griddep_launch_dependents();
   constexpr int WR = 32 * V * R;  // rows per warp
   constexpr int RB = NW * WR;     // rows per CTA row block
@@ -339,8 +339,8 @@ __global__ void __launch_bounds__(NW * 32, 2) gemv_ns_kernel(const GemvParams p)
 // Rows outside the logical range are masked with selects, so padding or a
 // parent's neighbouring rows (possibly NaN) never enter a sum.
 // ---------------------------------------------------------------------------
-template <class T, int V, int NW, int CW, int R, bool CONJ>
-__global__ void __launch_bounds__(NW * 32, 2) gemv_t_kernel(const GemvParams p) {
+template <class T, int V, int NW, int CW, int R, bool CONJ, int MINB = 2>
+__global__ void __launch_bounds__(NW * 32, MINB) gemv_t_kernel(const GemvParams p) {
   griddep_launch_dependents();
   constexpr int H = 32 * V * R;
   constexpr int CBW = NW * CW;
