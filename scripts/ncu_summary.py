@@ -49,7 +49,8 @@ def main():
     main_bytes = None
     for d in rows:
         name = d["Kernel Name"]
-        t = num(d.get("gpu__time_duration.sum")) * (1e-3 if units.get("gpu__time_duration.sum") == "ns" else 1.0)
+        t = num(d.get("gpu__time_duration.sum")) * {"ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3,
+                                                     "ms": 1e3}.get(units.get("gpu__time_duration.sum"), 1.0)
         rd = num(d.get("dram__bytes_read.sum"))
         wr = num(d.get("dram__bytes_write.sum"))
         scale_r = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}.get(units.get("dram__bytes_read.sum"), 1.0)
