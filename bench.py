@@ -9,11 +9,13 @@ kblas_dsymv call (main streaming kernel + fixed-order epilogue) on
 HBM-resident operands.  The 8.6 GB matrix is 68x the 126 MB L2, so every
 step streams A from HBM (no flush needed).
 
-N>1 (torchrun, one process per GPU, NCCL): mgpu DSYMV lower over the 1D
+N>1 (torchrun, one process per GPU): mgpu DSYMV lower over the 1D
 block-column-cyclic layout (nb=128) with per-GPU work fixed (weak scaling):
 n = 32768 * sqrt(N) rounded to nb, each rank streams its panel's stored
-triangle and the partial y vectors are combined by one NCCL reduce onto
-rank 0 (multidevice.py:276 restated over NCCL).
+triangle and writes its partial y straight into its slot in rank 0's HBM
+(CUDA IPC, NVLink stores); a device-flag handshake and a rank-order
+combine kernel on rank 0 finish y (multidevice.py:276, 282-283) with no
+NCCL on the data path.  `--reduce nccl` uses an NCCL reduce instead.
 
 `--impl reference` times the reference's CPU path for the same metric:
 the C restatement of the reference oracle (oracle/streamed.c, all host
@@ -57,7 +59,9 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--mgpu", action="store_true",
-                    help="run the one-process-per-GPU mgpu path even at N=1 (exercises the NCCL reduce path)")
+                    help="run the one-process-per-GPU mgpu path even at N=1 (exercises the exchange path)")
+    ap.add_argument("--reduce", choices=["p2p", "nccl"], default="p2p",
+                    help="mgpu exchange: peer-memory slots + device flags (p2p, default) or an NCCL reduce")
     return ap.parse_args()
 
 
@@ -374,7 +378,7 @@ def e2e_single(args, A, x, y, tag, family, op, herm, m, n, ld, dev, nbytes):
 
 def bench_mgpu(args, dev, rank, world):
     """Weak-scaling mgpu DSYMV: per-rank panel of the block-cyclic layout,
-    partial via the sm_100a kernels, NCCL reduce of y onto rank 0."""
+    partial via the sm_100a kernels, exchange of y onto rank 0 (--reduce)."""
     import torch
     import torch.distributed as dist
 
@@ -400,9 +404,23 @@ def bench_mgpu(args, dev, rank, world):
     (torch.view_as_real(x) if p.is_complex else x).uniform_(-1, 1, generator=torch.Generator(device=dev).manual_seed(7))
     out = torch.empty(n, dtype=p.torch_dtype, device=dev)
 
-    def step():
-        partial_mv(p, "s", op, n, n, 1.0, panel, x, out, world, rank, nb, herm)
-        combine(out, None, 0.0)
+    ex = None
+    if args.reduce == "p2p":
+        from paper_1410_1726_b200.dist import P2PExchange, p2p_mv
+
+        try:
+            ex = P2PExchange(n, p.torch_dtype)
+        except Exception as err:  # no IPC between these ranks: fall back to the NCCL reduce
+            print(f"p2p exchange unavailable ({err}); using the NCCL reduce", file=sys.stderr, flush=True)
+            args.reduce = "nccl"
+    if ex is not None:
+
+        def step():
+            p2p_mv(p, "s", op, n, n, 1.0, panel, x, 0.0, None, nb, ex, hermitian=herm)
+    else:
+        def step():
+            partial_mv(p, "s", op, n, n, 1.0, panel, x, out, world, rank, nb, herm)
+            combine(out, None, 0.0)
 
     nbytes = alg_bytes(tag, "symv", n, n, op)
     for _ in range(args.warmup):
@@ -438,16 +456,16 @@ def bench_mgpu(args, dev, rank, world):
         my_bytes += ((c1 - c0) * (c1 - c0 + 1) // 2 + (n - c1) * (c1 - c0)) * p.element_bytes
     e2e = None
     if not args.no_e2e and args.e2e_steps > 0:
-        e2e = e2e_mgpu(args, panel, panel_t, x, out, p, n, nb, lc, ld, world, rank, dev, op, herm, nbytes)
+        e2e = e2e_mgpu(args, panel, panel_t, x, out, p, n, nb, lc, ld, world, rank, dev, op, herm, nbytes, ex)
     return dict(e2e=e2e, tag=tag, family="symv", op=op, m=n, n=n, ld=ld, nbytes=nbytes, ms_step=ms_step,
                 gbs=nbytes / (ms_step * 1e-3) / 1e9, kern_avg_ms=kern_ms / max(kern_n, 1), kern_launches=kern_n,
                 launches=launches, plan=_lib.last_plan(), clocks=clocks, my_bytes=my_bytes, nb=nb)
 
 
-def e2e_mgpu(args, panel, panel_t, x, out, p, n, nb, lc, ld, world, rank, dev, op, herm, nbytes):
+def e2e_mgpu(args, panel, panel_t, x, out, p, n, nb, lc, ld, world, rank, dev, op, herm, nbytes, ex=None):
     """Per step on every rank: x from pinned host to HBM, the partial kernels
-    on the resident panel, the NCCL reduce onto rank 0, and on rank 0 the
-    D2H read of y.  Max over ranks."""
+    on the resident panel, the exchange onto rank 0 (peer-memory slots, or
+    an NCCL reduce), and on rank 0 the D2H read of y.  Max over ranks."""
     import torch
     import torch.distributed as dist
 
@@ -462,8 +480,13 @@ def e2e_mgpu(args, panel, panel_t, x, out, p, n, nb, lc, ld, world, rank, dev, o
 
     def step():
         dx.copy_(hx, non_blocking=True)
-        partial_mv(p, "s", op, n, n, 1.0, panel, dx, out, world, rank, nb, herm)
-        res = combine(out, None, 0.0)
+        if ex is not None:
+            from paper_1410_1726_b200.dist import p2p_mv
+
+            res = p2p_mv(p, "s", op, n, n, 1.0, panel, dx, 0.0, None, nb, ex, hermitian=herm)
+        else:
+            partial_mv(p, "s", op, n, n, 1.0, panel, dx, out, world, rank, nb, herm)
+            res = combine(out, None, 0.0)
         if rank == 0:
             hy.copy_(res)  # synchronous D2H read of the result
 
@@ -479,10 +502,12 @@ def e2e_mgpu(args, panel, panel_t, x, out, p, n, nb, lc, ld, world, rank, dev, o
     el = torch.tensor([(time.perf_counter() - t0) / steps], device=dev)
     dist.all_reduce(el, op=dist.ReduceOp.MAX)
     el = el.item()
+    how = ("partial written into rank 0's peer-memory slot, device-flag handshake, rank-order combine kernel "
+           "on rank 0" if ex is not None else "NCCL reduce to rank 0")
     return {"value": round(nbytes / el / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": int(n * eb),
             "d2h_bytes_per_step": int(n * eb), "steps": steps, "ms_per_step": round(el * 1e3, 4),
-            "path": "per rank: x from pinned host, kblas_mv_mgpu_partial_async on the HBM-resident panel, "
-                    "NCCL reduce to rank 0, D2H of y on rank 0; max over ranks"}
+            "path": f"per rank: x from pinned host, kblas_mv_mgpu_partial_async on the HBM-resident panel, {how}, "
+                    "D2H of y on rank 0; max over ranks"}
 
 
 def main():
@@ -517,8 +542,10 @@ def main():
     if rank == 0:
         opname = args.op
         if mgpu:
+            xch = ("peer-memory exchange of y (IPC slots + device flags, rank-order combine)"
+                   if args.reduce == "p2p" else "NCCL reduce of y")
             workload = (f"mgpu {opname} N={res['n']} 1D block-column-cyclic nb={res['nb']} over {world} GPUs, "
-                        f"NCCL reduce of y (weak scaling: n = 32768*sqrt(G))")
+                        f"{xch} (weak scaling: n = 32768*sqrt(G))")
         elif args.op == "dsymv" and res["n"] == 32768:
             workload = "DSYMV lower N=32768 (BASELINE configs[1])"
         else:

@@ -264,6 +264,30 @@ int kblas_mv_mgpu_partial_async(char prec, char kind, char op, int m, int n,
                                 const void *dx, void *dy_partial, int ngpus, int gpu,
                                 int nb, int hermitian, cudaStream_t stream);
 
+/* One-process-per-GPU exchange over peer memory, replacing the host-  */
+/* side device-order sum of the partials (multidevice.py:276, 282-283)  */
+/* without NCCL.  The root owns `slots` (nranks x slot_ld elements),    */
+/* `flags` (nranks u64), `consumed` (u64) and `counter` (u32, zero),    */
+/* shares them with CUDA IPC handles (64 bytes), and every rank writes  */
+/* its partial into its slot through kblas_mv_mgpu_partial_async, then */
+/* kblas_p2p_signal_async(&flags[rank], seq).  Before reusing its slot */
+/* for call seq a rank waits for consumed >= seq-1                     */
+/* (kblas_p2p_wait_async).  kblas_p2p_combine_async (root) waits for    */
+/* all flags >= seq, writes y = beta*y + sum_g slots[g] in rank order   */
+/* and publishes consumed = seq.  All calls are stream-ordered.         */
+int kblas_ipc_get_handle(const void *dptr, void *handle_out);
+int kblas_ipc_open_handle(const void *handle, void **dptr_out);
+int kblas_ipc_close(void *dptr);
+int kblas_p2p_signal_async(unsigned long long *flag, unsigned long long seq,
+                           cudaStream_t stream);
+int kblas_p2p_wait_async(const unsigned long long *flag, unsigned long long seq,
+                         cudaStream_t stream);
+int kblas_p2p_combine_async(char prec, int nranks, const void *slots, long long slot_ld,
+                            const unsigned long long *flags, unsigned long long seq,
+                            const void *beta, void *y, long long n,
+                            unsigned long long *consumed, unsigned *counter,
+                            cudaStream_t stream);
+
 /* ------------------------------------------------------------------ */
 /* mgpu helpers: column count held by one GPU under */
 /* the cyclic layout (multidevice.py:38-43), and the local ld (rows    */

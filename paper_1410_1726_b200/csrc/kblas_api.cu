@@ -1099,6 +1099,66 @@ int kblas_mv_hostvec(char prec, char kind, char op, int hermitian, int m, int n,
   return -1;
 }
 
+// ------------------------------------------------ peer-memory exchange
+int kblas_ipc_get_handle(const void *dptr, void *handle_out) {
+  if (dptr == nullptr || handle_out == nullptr) return -1;
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, const_cast<void *>(dptr));
+  if (e != cudaSuccess) return (int)e;
+  memcpy(handle_out, &h, sizeof h);
+  return 0;
+}
+
+int kblas_ipc_open_handle(const void *handle, void **dptr_out) {
+  if (handle == nullptr || dptr_out == nullptr) return -1;
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof h);
+  return code(cudaIpcOpenMemHandle(dptr_out, h, cudaIpcMemLazyEnablePeerAccess));
+}
+
+int kblas_ipc_close(void *dptr) { return code(cudaIpcCloseMemHandle(dptr)); }
+
+int kblas_p2p_signal_async(unsigned long long *flag, unsigned long long seq, cudaStream_t stream) {
+  if (flag == nullptr) return -1;
+  p2p_signal_kernel<<<1, 32, 0, stream>>>(flag, seq);
+  launched();
+  return code(cudaGetLastError());
+}
+
+int kblas_p2p_wait_async(const unsigned long long *flag, unsigned long long seq, cudaStream_t stream) {
+  if (flag == nullptr) return -1;
+  p2p_wait_kernel<<<1, 32, 0, stream>>>(flag, seq);
+  launched();
+  return code(cudaGetLastError());
+}
+
+int kblas_p2p_combine_async(char prec, int nranks, const void *slots, long long slot_ld,
+                            const unsigned long long *flags, unsigned long long seq, const void *beta, void *y,
+                            long long n, unsigned long long *consumed, unsigned *counter, cudaStream_t stream) {
+  if (nranks < 1 || slots == nullptr || flags == nullptr || y == nullptr || consumed == nullptr ||
+      counter == nullptr || n < 0 || slot_ld < n)
+    return -1;
+  const unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>(cdiv(n, 256), 4LL * dev_sms()));
+  switch (prec | 0x20) {
+#define KB_P2P(CH, T)                                                                                         \
+  case CH: {                                                                                                  \
+    const T b = *static_cast<const T *>(beta);                                                                \
+    p2p_combine_kernel<T><<<grid, 256, 0, stream>>>(static_cast<const T *>(slots), slot_ld, nranks, flags, seq, \
+                                                    static_cast<T *>(y), n, b, is_zero(b) ? 1 : 0, consumed,      \
+                                                    counter);                                                 \
+    break;                                                                                                    \
+  }
+    KB_P2P('s', float)
+    KB_P2P('d', double)
+    KB_P2P('c', float2)
+    KB_P2P('z', double2)
+#undef KB_P2P
+    default: return -1;
+  }
+  launched();
+  return code(cudaGetLastError());
+}
+
 unsigned long long kblas_launch_count(void) { return g_launches.load(); }
 
 int kblas_timing_enable(int enable) {

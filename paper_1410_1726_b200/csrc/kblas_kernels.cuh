@@ -857,4 +857,75 @@ __global__ void mgpu_combine_kernel(T *y, PartList<T> parts, int G, long long n,
   y[i] = beta_zero ? s : fma_(beta, y[i], s);
 }
 
+// ---------------------------------------------------------------------------
+// One-process-per-GPU exchange over peer memory (no NCCL): every rank
+// writes its partial y straight into its slot of a root-resident buffer
+// (opened with CUDA IPC; NVLink stores when the ranks are on different
+// GPUs), then publishes the call's sequence number in flags[rank] with a
+// system-scope release.  The root's combine kernel acquires all flags,
+// sums the slots in rank order (the reference's device-order sum,
+// multidevice.py:276, so results do not depend on arrival order), adds
+// beta*y (282-283), and its last CTA publishes `consumed` so ranks may
+// reuse their slots.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// bounded spin: a peer that never arrives turns into a kernel error
+// (~30 s) instead of a hung GPU
+__device__ __forceinline__ void spin_until(const unsigned long long *flag, unsigned long long seq) {
+  for (unsigned long long it = 0; ld_acquire_sys(flag) < seq; ++it) {
+    __nanosleep(256);
+    if (it > (1ull << 27)) __trap();
+  }
+}
+
+// rank side: its partial (written by the preceding kernels on this stream)
+// becomes visible system-wide, then flags[rank] = seq
+__global__ void p2p_signal_kernel(unsigned long long *flag, unsigned long long seq) {
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    st_release_sys(flag, seq);
+  }
+}
+
+// wait until *flag >= seq (e.g. the root has consumed the previous call)
+__global__ void p2p_wait_kernel(const unsigned long long *flag, unsigned long long seq) {
+  if (threadIdx.x == 0) spin_until(flag, seq);
+  __syncthreads();
+}
+
+template <class T>
+__global__ void p2p_combine_kernel(const T *__restrict__ slots, long long slot_ld, int G,
+                                   const unsigned long long *flags, unsigned long long seq, T *y, long long n,
+                                   T beta, int beta_zero, unsigned long long *consumed, unsigned *counter) {
+  if (threadIdx.x == 0) {
+    for (int g = 0; g < G; ++g) spin_until(flags + g, seq);
+  }
+  __syncthreads();
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    T s = __ldcv(slots + i);
+    for (int g = 1; g < G; ++g) s = add_(s, __ldcv(slots + g * slot_ld + i));
+    y[i] = beta_zero ? s : fma_(beta, y[i], s);
+  }
+  // the last CTA to finish releases the slots for the next call
+  __shared__ bool last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+    if (last) {
+      *counter = 0u;
+      __threadfence_system();
+      st_release_sys(consumed, seq);
+    }
+  }
+}
+
 }  // namespace kb

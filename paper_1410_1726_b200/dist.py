@@ -68,3 +68,139 @@ def gpu_partial(prec):
         partial_mv(prec, kind, op, m, n, alpha, panel, x, out, world, rank, nb, hermitian)
 
     return fn
+
+
+class P2PExchange:
+    """Peer-memory exchange of the per-rank partials (no NCCL on the data
+    path): the root (rank 0) owns a slot per rank plus flags in HBM and
+    shares them with CUDA IPC; each rank's partial kernels write straight
+    into its slot (NVLink stores when ranks are on different GPUs), a
+    signal kernel publishes the call's sequence number, and the root's
+    combine kernel sums the slots in rank order with beta*y fused
+    (multidevice.py:276,282-283: the device-order sum, so the result does
+    not depend on arrival order).  All synchronisation is on the device;
+    the process group is used once, to exchange the IPC handles.
+
+    Usage per call:  out = ex.slot()  -> partial kernels write `out`;
+    res = ex.combine(y, beta)  (the result on rank 0, None elsewhere).
+    """
+
+    def __init__(self, n: int, dtype: torch.dtype, group=None):
+        import ctypes
+
+        from . import _lib
+        from ._ops import stream_handle
+
+        self._lib = _lib.load()
+        self._stream = stream_handle
+        self.group = group
+        self.world, self.rank = dist.get_world_size(group), dist.get_rank(group)
+        self.n, self.dtype = n, dtype
+        self.dev = torch.device("cuda", torch.cuda.current_device())
+        esize = torch.empty(0, dtype=dtype).element_size()
+        self.ld = -(-n * esize // 256) * 256 // esize  # 256-byte aligned slots
+        self.seq = 0
+        if self.rank == 0:
+            self._slots = torch.zeros(self.world * self.ld, dtype=dtype, device=self.dev)
+            self._ctl = torch.zeros(self.world + 2, dtype=torch.int64, device=self.dev)  # flags, consumed, counter
+            handles = []
+            for t in (self._slots, self._ctl):
+                h = (ctypes.c_char * 64)()
+                _lib.check(self._lib.kblas_ipc_get_handle(t.data_ptr(), h), "kblas_ipc_get_handle")
+                # the allocation may start before the tensor (caching allocator)
+                handles.append((bytes(h), t.data_ptr() - self._base_of(t)))
+            payload = [handles]
+        else:
+            payload = [None]
+        dist.broadcast_object_list(payload, src=0, group=group)
+        self._opened = []
+        if self.rank == 0:
+            self.slots_ptr, ctl_ptr = self._slots.data_ptr(), self._ctl.data_ptr()
+        else:
+            ptrs = []
+            for h, off in payload[0]:
+                p = ctypes.c_void_p()
+                _lib.check(self._lib.kblas_ipc_open_handle(h, ctypes.byref(p)), "kblas_ipc_open_handle")
+                self._opened.append(p.value)
+                ptrs.append(p.value + off)
+            self.slots_ptr, ctl_ptr = ptrs
+        self.flags_ptr = ctl_ptr
+        self.consumed_ptr = ctl_ptr + 8 * self.world
+        self.counter_ptr = ctl_ptr + 8 * (self.world + 1)
+        self._esize = esize
+
+    @staticmethod
+    def _base_of(t: torch.Tensor) -> int:
+        """Start of the cudaMalloc block holding t (what an IPC handle names)."""
+        import ctypes
+
+        base = ctypes.c_void_p()
+        size = ctypes.c_size_t()
+        lib = ctypes.CDLL("libcuda.so.1")
+        rc = lib.cuMemGetAddressRange_v2(ctypes.byref(base), ctypes.byref(size), ctypes.c_void_p(t.data_ptr()))
+        if rc != 0:
+            raise RuntimeError(f"cuMemGetAddressRange failed ({rc})")
+        return base.value
+
+    def slot_ptr(self) -> int:
+        """Device address (on this rank) of its slot for the next call; waits
+        on the stream until the root has consumed the previous call."""
+        from . import _lib
+
+        st = self._stream(self.dev)
+        if self.seq > 0 and self.rank != 0:
+            _lib.check(self._lib.kblas_p2p_wait_async(self.consumed_ptr, self.seq, st), "kblas_p2p_wait_async")
+        return self.slots_ptr + self.rank * self.ld * self._esize
+
+    def combine(self, y: torch.Tensor | None, beta, prec_tag: str):
+        """Publish this rank's partial; on rank 0 wait for all and return
+        beta*y + sum of the slots (rank order) in a fresh tensor."""
+        import ctypes
+
+        from . import _lib
+
+        self.seq += 1
+        st = self._stream(self.dev)
+        if self.rank != 0:
+            _lib.check(self._lib.kblas_p2p_signal_async(self.flags_ptr + 8 * self.rank, self.seq, st),
+                       "kblas_p2p_signal_async")
+            return None
+        _lib.check(self._lib.kblas_p2p_signal_async(self.flags_ptr, self.seq, st), "kblas_p2p_signal_async")
+        out = torch.empty(self.n, dtype=self.dtype, device=self.dev)
+        bz = complex(beta) == 0
+        if not bz:
+            out.copy_(y)
+        b = _lib.scalar(prec_tag, beta)
+        _lib.check(self._lib.kblas_p2p_combine_async(
+            prec_tag.encode(), self.world, self.slots_ptr, self.ld, self.flags_ptr, self.seq, ctypes.addressof(b),
+            out.data_ptr(), self.n, self.consumed_ptr, self.counter_ptr, st), "kblas_p2p_combine_async")
+        return out
+
+    def close(self):
+        for p in self._opened:
+            self._lib.kblas_ipc_close(p)
+        self._opened = []
+
+
+def p2p_mv(prec, kind: str, op: str, m: int, n: int, alpha, panel, x: torch.Tensor, beta, y, nb: int,
+           ex: P2PExchange, hermitian: bool = False):
+    """Distributed y = alpha * op(A) x + beta * y with the peer-memory
+    exchange: this rank's partial kernels write into its root slot, the
+    root combines on the device.  Returns the result on rank 0."""
+    import ctypes
+
+    from . import _lib
+    from ._ops import stream_handle
+
+    lib = _lib.load()
+    a_ptr, lda = (0, 1)
+    if panel is not None:
+        a_ptr = panel.data.data_ptr() + panel.linear_index(0, 0) * prec.element_bytes
+        lda = panel.ld
+    dst = ex.slot_ptr()
+    al = _lib.scalar(prec.tag, alpha)
+    rc = lib.kblas_mv_mgpu_partial_async(prec.tag.encode(), kind.encode(), op.encode(), m, n,
+                                         ctypes.addressof(al), a_ptr, lda, x.data_ptr(), dst, ex.world, ex.rank,
+                                         nb, 1 if hermitian else 0, stream_handle(x.device))
+    _lib.check(rc, "kblas_mv_mgpu_partial_async")
+    return ex.combine(y, beta, prec.tag)

@@ -1,0 +1,82 @@
+"""The peer-memory exchange of the one-process-per-GPU mgpu path
+(dist.P2PExchange / p2p_mv): world size 2 on one B200 (two processes,
+gloo for the one-time IPC handle exchange; the data path is CUDA IPC
+peer stores plus device flags, no NCCL).  Several calls in a row check the
+slot reuse handshake; rank 0's result must match the single-GPU API."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _worker(rank, world, port, kind, op, tag, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_1410_1726_b200 as kb
+    from paper_1410_1726_b200.dist import P2PExchange, p2p_mv
+
+    prec = kb.precision(tag)
+    n, nb = 1000, 64
+    g = torch.Generator(device="cuda").manual_seed(3)
+    A = torch.empty(n, n, dtype=prec.torch_dtype, device="cuda")
+    (torch.view_as_real(A) if A.is_complex() else A).uniform_(-1, 1, generator=g)
+    full = kb.view_of(A.T)  # column-major n x n
+    dist_mat = kb.distribute(full, nb, world, devices=["cuda:0"] * world)
+    panel = dist_mat.local_views[rank]
+    herm = kind == "s" and prec.is_complex
+    ex = P2PExchange(n, prec.torch_dtype)
+    errs = []
+    for it in range(4):
+        x = torch.empty(n, dtype=prec.torch_dtype, device="cuda")
+        (torch.view_as_real(x) if x.is_complex() else x).uniform_(-1, 1, generator=g)
+        y = torch.empty(n, dtype=prec.torch_dtype, device="cuda")
+        (torch.view_as_real(y) if y.is_complex() else y).uniform_(-1, 1, generator=g)
+        beta = 0.0 if it % 2 == 0 else -0.5
+        res = p2p_mv(prec, kind, op, n, n, 0.75, panel, x, beta, y, nb, ex, hermitian=herm)
+        if rank == 0:
+            if kind == "g":
+                want = kb.gemv(op, 0.75, full, x, beta, y).y_out
+            else:
+                want = kb.symv_hemv(op, 0.75, kb.HermitianView(full, op), x, beta, y, hermitian=herm).y_out
+            torch.cuda.synchronize()
+            errs.append(float((res - want).abs().max() / want.abs().max()))
+        else:
+            assert res is None
+    torch.cuda.synchronize()
+    dist.barrier()
+    ex.close()
+    if rank == 0:
+        q.put(max(errs))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kind,op,tag", [("s", "l", "d"), ("s", "u", "z"), ("g", "n", "d"), ("g", "t", "s")])
+def test_p2p_exchange_world2_one_gpu(kind, op, tag):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, kind, op, tag, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(300)
+        assert p.exitcode == 0
+    tol = 1e-5 if tag in "sc" else 1e-12
+    assert q.get(timeout=5) < tol
