@@ -282,6 +282,22 @@ int kblas_p2p_signal_async(unsigned long long *flag, unsigned long long seq,
                            cudaStream_t stream);
 int kblas_p2p_wait_async(const unsigned long long *flag, unsigned long long seq,
                          cudaStream_t stream);
+/* The whole per-rank step of a one-process-per-GPU mgpu call with the  */
+/* peer-memory exchange: this rank's partial (as                        */
+/* kblas_mv_mgpu_partial_async) into its slot, the handshake, and on    */
+/* rank 0 the rank-order combine with beta (y_out = beta*y_in + sum).   */
+/* For SYMV/HEMV the exchange is fused into the partial's epilogue      */
+/* kernel (waits, peer stores, flags); GEMV uses the separate kernels   */
+/* above.  slots/flags/consumed are this rank's mappings of rank 0's    */
+/* buffers; counter (rank 0) is a zeroed u32 in rank 0's HBM; seq      */
+/* counts calls from 1.                                                 */
+int kblas_mv_mgpu_partial_p2p_async(char prec, char kind, char op, int m, int n,
+                                    const void *alpha, const void *dA_local, int lda,
+                                    const void *dx, int ngpus, int gpu, int nb, int hermitian,
+                                    void *slots, long long slot_ld, unsigned long long *flags,
+                                    unsigned long long *consumed, unsigned *counter,
+                                    unsigned long long seq, const void *beta,
+                                    const void *y_in, void *y_out, cudaStream_t stream);
 int kblas_p2p_combine_async(char prec, int nranks, const void *slots, long long slot_ld,
                             const unsigned long long *flags, unsigned long long seq,
                             const void *beta, void *y, long long n,

@@ -113,6 +113,11 @@ def load():
         lib.kblas_p2p_wait_async.argtypes = [c_void_p, c_ulonglong, c_void_p]
         lib.kblas_p2p_combine_async.argtypes = [c_char, c_int, c_void_p, ctypes.c_longlong, c_void_p, c_ulonglong,
                                                 c_void_p, c_void_p, ctypes.c_longlong, c_void_p, c_void_p, c_void_p]
+        lib.kblas_mv_mgpu_partial_p2p_async.argtypes = [
+            c_char, c_char, c_char, c_int, c_int, c_void_p, c_void_p, c_int, c_void_p, c_int, c_int, c_int, c_int,
+            c_void_p, ctypes.c_longlong, c_void_p, c_void_p, c_void_p, c_ulonglong, c_void_p, c_void_p, c_void_p,
+            c_void_p]
+        lib.kblas_mv_mgpu_partial_p2p_async.restype = c_int
         for name in ("kblas_ipc_get_handle", "kblas_ipc_open_handle", "kblas_ipc_close", "kblas_p2p_signal_async",
                      "kblas_p2p_wait_async", "kblas_p2p_combine_async"):
             getattr(lib, name).restype = c_int

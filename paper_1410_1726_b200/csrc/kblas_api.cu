@@ -34,6 +34,9 @@ using namespace kb;
 namespace {
 
 std::atomic<unsigned long long> g_launches{0};
+// peer-memory exchange for the SYMV epilogue of the current call on this
+// thread (set by kblas_mv_mgpu_partial_p2p_async only; G == 0 otherwise)
+thread_local kb::Xchg g_xchg{};
 int g_symv_narrow_max = 2048;  // register SYMV: narrow tiles up to this order (kblas_set_symv_narrow)
 thread_local std::string g_last_plan;
 
@@ -479,7 +482,8 @@ cudaError_t run_symv(const Path<T> &pa, long long lda, int d, const T *x, ColMap
     TimedScope ts(st);
     kfn<<<(unsigned)P, NW * 32, smem, st>>>(p);
   }
-  launch_pdl(symv_epilogue<T, LOWER, 16>, (unsigned)cdiv(d, 32), 512, st, y, p, alpha, beta, (int)beta_zero);
+  launch_pdl(symv_epilogue<T, LOWER, 16>, (unsigned)cdiv(d, 32), 512, st, y, p, alpha, beta, (int)beta_zero,
+             g_xchg);
   launched(2);
   char buf[256];
   snprintf(buf, sizeof buf, "symv %s %s %s%s lead=%d d=%d W=%d H=%d tiles=%d items=%lld P=%lld slots=%lld",
@@ -587,7 +591,8 @@ cudaError_t run_symv_tma(const T *A00, long long lda, int d, const T *x, ColMap 
     TimedScope ts(st);
     kfn<<<(unsigned)P, (NC + 2) * 32, smem, st>>>(map, tp);
   }
-  launch_pdl(symv_epilogue<T, LOWER, 16>, (unsigned)cdiv(d, 32), 512, st, y, tp.sp, alpha, beta, (int)beta_zero);
+  launch_pdl(symv_epilogue<T, LOWER, 16>, (unsigned)cdiv(d, 32), 512, st, y, tp.sp, alpha, beta,
+             (int)beta_zero, g_xchg);
   launched(2);
   char buf[256];
   snprintf(buf, sizeof buf, "symv_tma %s %s%s lead=%d d=%d W=%d H=%d S=%d tiles=%d items=%lld P=%lld slots=%lld smem=%zu",
@@ -937,6 +942,52 @@ int hostvec_entry(bool is_gemv, char op, bool herm, int m, int n, T alpha, const
   return code(cudaStreamSynchronize(st));
 }
 
+template <class T>
+int partial_p2p(bool is_gemv, char op, bool herm, int m, int n, T alpha, const T *dA, int lda, const T *dx,
+                       int G, int g, int nb, T *slots, long long slot_ld, unsigned long long *flags,
+                       unsigned long long *consumed, unsigned *counter, unsigned long long seq, T beta,
+                       const T *y_in, T *y_out, cudaStream_t st) {
+  const long long plen = is_gemv ? ((op == 'n') ? m : n) : n;
+  if (slot_ld < plen) return -1;
+  const bool fused = !is_gemv && local_cols(n, nb, G, g) > 0 && !is_zero(alpha);
+  if (fused) {
+    // the exchange rides in the SYMV epilogue: one launch pair per call
+    unsigned *cnt = nullptr;
+    cudaError_t e = counters(1, st, &cnt);
+    if (e != cudaSuccess) return (int)e;
+    g_xchg = kb::Xchg{G, g, slots, slot_ld, flags, consumed, cnt, seq, y_in};
+    // root: epilogue writes y_out = beta*y_in + sum; others: their slot
+    T *dst = (g == 0) ? y_out : slots + (long long)g * slot_ld;
+    const bool bz = g != 0 || is_zero(beta);
+    Path<T> pa;
+    int rc = make_path(dA, lda, &pa) != 0 ? -5 : 0;
+    if (rc == 0)
+      rc = code(dispatch_symv<T>(op == 'l', herm, pa, lda, n, dx, ColMap{G, g, nb}, (int)local_cols(n, nb, G, g),
+                                 dst, alpha, g == 0 ? beta : zero<T>(), bz, st));
+    g_xchg = kb::Xchg{};
+    return rc;
+  }
+  // general path: wait for the slot, partial into it, signal; root combines
+  if (g != 0 && seq > 1) {
+    p2p_wait_kernel<<<1, 32, 0, st>>>(consumed, seq - 1);
+    launched();
+  }
+  int rc = partial_entry<T>(is_gemv, op, herm, m, n, alpha, dA, lda, dx, slots + (long long)g * slot_ld, G, g, nb, st);
+  if (rc) return rc;
+  p2p_signal_kernel<<<1, 32, 0, st>>>(flags + g, seq);
+  launched();
+  if (g != 0) return code(cudaGetLastError());
+  if (!is_zero(beta) && y_out != y_in) {
+    cudaError_t e = cudaMemcpyAsync(y_out, y_in, plen * sizeof(T), cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) return (int)e;
+  }
+  const unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>(cdiv(plen, 256), 4LL * dev_sms()));
+  p2p_combine_kernel<T><<<grid, 256, 0, st>>>(slots, slot_ld, G, flags, seq, y_out, plen, beta, is_zero(beta) ? 1 : 0,
+                                              consumed, counter);
+  launched();
+  return code(cudaGetLastError());
+}
+
 }  // namespace
 
 // ====================================================================
@@ -1130,6 +1181,31 @@ int kblas_p2p_wait_async(const unsigned long long *flag, unsigned long long seq,
   p2p_wait_kernel<<<1, 32, 0, stream>>>(flag, seq);
   launched();
   return code(cudaGetLastError());
+}
+
+int kblas_mv_mgpu_partial_p2p_async(char prec, char kind, char op, int m, int n, const void *alpha,
+                                    const void *dA_local, int lda, const void *dx, int ngpus, int gpu, int nb,
+                                    int hermitian, void *slots, long long slot_ld, unsigned long long *flags,
+                                    unsigned long long *consumed, unsigned *counter, unsigned long long seq,
+                                    const void *beta, const void *y_in, void *y_out, cudaStream_t stream) {
+  const bool is_gemv = (kind | 0x20) == 'g';
+  const char o = (char)(op | 0x20);
+  if (ngpus < 1 || ngpus > kMaxGpus || gpu < 0 || gpu >= ngpus || nb < 1 || m < 0 || n < 0) return -1;
+  if (slots == nullptr || flags == nullptr || consumed == nullptr || seq < 1) return -1;
+  if (gpu == 0 && (y_out == nullptr || counter == nullptr)) return -1;
+  switch (prec | 0x20) {
+#define KB_PP(CH, T, H)                                                                                         \
+  case CH:                                                                                                      \
+    return partial_p2p<T>(is_gemv, o, H, m, n, *(const T *)alpha, (const T *)dA_local, lda, (const T *)dx,        \
+                          ngpus, gpu, nb, (T *)slots, slot_ld, flags, consumed, counter, seq, *(const T *)beta,   \
+                          (const T *)y_in, (T *)y_out, stream);
+    KB_PP('s', float, false)
+    KB_PP('d', double, false)
+    KB_PP('c', float2, hermitian != 0)
+    KB_PP('z', double2, hermitian != 0)
+#undef KB_PP
+  }
+  return -1;
 }
 
 int kblas_p2p_combine_async(char prec, int nranks, const void *slots, long long slot_ld,

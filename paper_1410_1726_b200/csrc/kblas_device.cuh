@@ -219,6 +219,25 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// system-scope acquire/release flags (cross-process peer-memory handshake)
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// bounded spin: a peer that never arrives turns into a kernel error
+// (~30 s) instead of a hung GPU
+__device__ __forceinline__ void spin_until(const unsigned long long *flag, unsigned long long seq) {
+  for (unsigned long long it = 0; ld_acquire_sys(flag) < seq; ++it) {
+    __nanosleep(256);
+    if (it > (1ull << 27)) __trap();
+  }
+}
+
 // ---------------------------------------------------------------------------
 // stream-K split: `total` equal work items over P CTAs; CTA c owns
 // [sk_start(c), sk_start(c+1)).  sk_owner(i) is the CTA owning item i.

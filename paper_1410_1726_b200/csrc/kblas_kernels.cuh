@@ -774,9 +774,30 @@ __global__ void __launch_bounds__(EW * 32) gemv_t_epilogue(T *y, const T *__rest
 // summation order is fixed and results are bit-reproducible); the tile
 // record is fetched alongside the t1 loads, so a call costs about two L2
 // round trips.  Warp 0 then adds the EW parts in order.
+// Peer-memory exchange fused into the epilogue of a one-process-per-GPU
+// mgpu call (dist.P2PExchange): G == 0 disables it.  A non-root rank's y
+// is its slot in the root's HBM; its last CTA publishes flags[rank] = seq.
+// The root adds the other ranks' slots to its own partial in rank order,
+// then beta*y_in, and its last CTA publishes consumed = seq.
+struct Xchg {
+  int G, rank;
+  const void *slots;  // root's slot array (this rank's mapping of it)
+  long long slot_ld;
+  unsigned long long *flags, *consumed;
+  unsigned *counter;  // local arrival counter, zero between calls
+  unsigned long long seq;
+  const void *y_in;   // root: the caller's y (beta != 0)
+};
+
 template <class T, bool LOWER, int EW>
-__global__ void __launch_bounds__(EW * 32) symv_epilogue(T *y, const SymParams p, T alpha, T beta, int beta_zero) {
+__global__ void __launch_bounds__(EW * 32) symv_epilogue(T *y, const SymParams p, T alpha, T beta, int beta_zero,
+                                                         const Xchg xg) {
   griddep_wait();
+  if (xg.G > 0 && xg.rank != 0 && xg.seq > 1) {
+    // this rank's slot is free once the root consumed the previous call
+    if (threadIdx.x == 0) spin_until(xg.consumed, xg.seq - 1);
+    __syncthreads();
+  }
   __shared__ T part[EW][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const long long i = min((long long)blockIdx.x * 32 + lane, (long long)p.d - 1);
@@ -828,11 +849,48 @@ __global__ void __launch_bounds__(EW * 32) symv_epilogue(T *y, const SymParams p
   }
   part[warp][lane] = acc;
   __syncthreads();
-  if (warp != 0 || !valid) return;
-  T s = part[0][lane];
+  if (xg.G == 0) {
+    if (warp != 0 || !valid) return;
+    T s = part[0][lane];
 #pragma unroll
-  for (int w = 1; w < EW; ++w) s = add_(s, part[w][lane]);
-  store_axpby(y, i, alpha, s, beta, beta_zero);
+    for (int w = 1; w < EW; ++w) s = add_(s, part[w][lane]);
+    store_axpby(y, i, alpha, s, beta, beta_zero);
+    return;
+  }
+  if (warp == 0) {
+    T s = part[0][lane];
+#pragma unroll
+    for (int w = 1; w < EW; ++w) s = add_(s, part[w][lane]);
+    T r = mul_(alpha, s);  // this rank's partial (multidevice.py:224-276)
+    if (xg.rank == 0) {
+      // the other ranks' slots, in rank order (multidevice.py:276), then
+      // beta * y (282-283)
+      if (lane == 0)
+        for (int g = 1; g < xg.G; ++g) spin_until(xg.flags + g, xg.seq);
+      __syncwarp();
+      const T *slots = static_cast<const T *>(xg.slots);
+      if (valid) {
+        for (int g = 1; g < xg.G; ++g) r = add_(r, __ldcv(slots + g * xg.slot_ld + i));
+        if (!beta_zero) r = fma_(beta, static_cast<const T *>(xg.y_in)[i], r);
+        y[i] = r;
+      }
+    } else if (valid) {
+      y[i] = r;  // a store into the root's HBM
+    }
+  }
+  // the last CTA to finish publishes this rank's arrival (or, on the root,
+  // that every slot has been consumed)
+  __shared__ bool last;
+  if (xg.rank == 0) __threadfence(); else __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    last = atomicAdd(xg.counter, 1u) == gridDim.x - 1;
+    if (last) {
+      *xg.counter = 0u;
+      __threadfence_system();
+      st_release_sys(xg.rank == 0 ? xg.consumed : xg.flags + xg.rank, xg.seq);
+    }
+  }
 }
 
 // y <- beta * y (beta == 0: zero fill); run_scal semantics (kernels.py:127-146)
@@ -868,24 +926,6 @@ __global__ void mgpu_combine_kernel(T *y, PartList<T> parts, int G, long long n,
 // beta*y (282-283), and its last CTA publishes `consumed` so ranks may
 // reuse their slots.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
-// bounded spin: a peer that never arrives turns into a kernel error
-// (~30 s) instead of a hung GPU
-__device__ __forceinline__ void spin_until(const unsigned long long *flag, unsigned long long seq) {
-  for (unsigned long long it = 0; ld_acquire_sys(flag) < seq; ++it) {
-    __nanosleep(256);
-    if (it > (1ull << 27)) __trap();
-  }
-}
-
 // rank side: its partial (written by the preceding kernels on this stream)
 // becomes visible system-wide, then flags[rank] = seq
 __global__ void p2p_signal_kernel(unsigned long long *flag, unsigned long long seq) {

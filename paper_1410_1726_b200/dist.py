@@ -73,17 +73,15 @@ def gpu_partial(prec):
 class P2PExchange:
     """Peer-memory exchange of the per-rank partials (no NCCL on the data
     path): the root (rank 0) owns a slot per rank plus flags in HBM and
-    shares them with CUDA IPC; each rank's partial kernels write straight
-    into its slot (NVLink stores when ranks are on different GPUs), a
-    signal kernel publishes the call's sequence number, and the root's
-    combine kernel sums the slots in rank order with beta*y fused
-    (multidevice.py:276,282-283: the device-order sum, so the result does
-    not depend on arrival order).  All synchronisation is on the device;
-    the process group is used once, to exchange the IPC handles.
-
-    Usage per call:  out = ex.slot()  -> partial kernels write `out`;
-    res = ex.combine(y, beta)  (the result on rank 0, None elsewhere).
-    """
+    shares them with CUDA IPC.  Each rank's partial goes straight into its
+    slot (NVLink stores when ranks are on different GPUs) and its arrival
+    is published with a system-scope release; the root sums the slots in
+    rank order with beta*y (multidevice.py:276,282-283: the device-order
+    sum, so the result does not depend on arrival order) and releases the
+    slots for the next call.  For SYMV/HEMV all of this happens inside the
+    partial's epilogue kernel.  Synchronisation is on the device; the
+    process group is used once, to exchange the IPC handles.  One call:
+    `p2p_mv(..., ex)`."""
 
     def __init__(self, n: int, dtype: torch.dtype, group=None):
         import ctypes
@@ -142,40 +140,6 @@ class P2PExchange:
             raise RuntimeError(f"cuMemGetAddressRange failed ({rc})")
         return base.value
 
-    def slot_ptr(self) -> int:
-        """Device address (on this rank) of its slot for the next call; waits
-        on the stream until the root has consumed the previous call."""
-        from . import _lib
-
-        st = self._stream(self.dev)
-        if self.seq > 0 and self.rank != 0:
-            _lib.check(self._lib.kblas_p2p_wait_async(self.consumed_ptr, self.seq, st), "kblas_p2p_wait_async")
-        return self.slots_ptr + self.rank * self.ld * self._esize
-
-    def combine(self, y: torch.Tensor | None, beta, prec_tag: str):
-        """Publish this rank's partial; on rank 0 wait for all and return
-        beta*y + sum of the slots (rank order) in a fresh tensor."""
-        import ctypes
-
-        from . import _lib
-
-        self.seq += 1
-        st = self._stream(self.dev)
-        if self.rank != 0:
-            _lib.check(self._lib.kblas_p2p_signal_async(self.flags_ptr + 8 * self.rank, self.seq, st),
-                       "kblas_p2p_signal_async")
-            return None
-        _lib.check(self._lib.kblas_p2p_signal_async(self.flags_ptr, self.seq, st), "kblas_p2p_signal_async")
-        out = torch.empty(self.n, dtype=self.dtype, device=self.dev)
-        bz = complex(beta) == 0
-        if not bz:
-            out.copy_(y)
-        b = _lib.scalar(prec_tag, beta)
-        _lib.check(self._lib.kblas_p2p_combine_async(
-            prec_tag.encode(), self.world, self.slots_ptr, self.ld, self.flags_ptr, self.seq, ctypes.addressof(b),
-            out.data_ptr(), self.n, self.consumed_ptr, self.counter_ptr, st), "kblas_p2p_combine_async")
-        return out
-
     def close(self):
         for p in self._opened:
             self._lib.kblas_ipc_close(p)
@@ -185,8 +149,10 @@ class P2PExchange:
 def p2p_mv(prec, kind: str, op: str, m: int, n: int, alpha, panel, x: torch.Tensor, beta, y, nb: int,
            ex: P2PExchange, hermitian: bool = False):
     """Distributed y = alpha * op(A) x + beta * y with the peer-memory
-    exchange: this rank's partial kernels write into its root slot, the
-    root combines on the device.  Returns the result on rank 0."""
+    exchange (kblas_mv_mgpu_partial_p2p_async): this rank's partial goes
+    into its slot in rank 0's HBM, rank 0 adds the slots in rank order with
+    beta*y.  For SYMV/HEMV the exchange runs inside the partial's epilogue
+    kernel.  Returns the result on rank 0, None elsewhere."""
     import ctypes
 
     from . import _lib
@@ -197,10 +163,20 @@ def p2p_mv(prec, kind: str, op: str, m: int, n: int, alpha, panel, x: torch.Tens
     if panel is not None:
         a_ptr = panel.data.data_ptr() + panel.linear_index(0, 0) * prec.element_bytes
         lda = panel.ld
-    dst = ex.slot_ptr()
-    al = _lib.scalar(prec.tag, alpha)
-    rc = lib.kblas_mv_mgpu_partial_async(prec.tag.encode(), kind.encode(), op.encode(), m, n,
-                                         ctypes.addressof(al), a_ptr, lda, x.data_ptr(), dst, ex.world, ex.rank,
-                                         nb, 1 if hermitian else 0, stream_handle(x.device))
-    _lib.check(rc, "kblas_mv_mgpu_partial_async")
-    return ex.combine(y, beta, prec.tag)
+    ex.seq += 1
+    plen = m if (kind == "g" and op == "n") else n
+    root = ex.rank == 0
+    out = torch.empty(plen, dtype=x.dtype, device=x.device) if root else None
+    bz = complex(beta) == 0
+    if root and not bz:
+        if y is None or y.numel() != plen:
+            raise ValueError(f"y must be a vector of length {plen}")
+        y = y.to(device=x.device, dtype=x.dtype).contiguous()
+    al, be = _lib.scalar(prec.tag, alpha), _lib.scalar(prec.tag, beta)
+    rc = lib.kblas_mv_mgpu_partial_p2p_async(
+        prec.tag.encode(), kind.encode(), op.encode(), m, n, ctypes.addressof(al), a_ptr, lda, x.data_ptr(),
+        ex.world, ex.rank, nb, 1 if hermitian else 0, ex.slots_ptr, ex.ld, ex.flags_ptr, ex.consumed_ptr,
+        ex.counter_ptr, ex.seq, ctypes.addressof(be), y.data_ptr() if (root and not bz) else None,
+        out.data_ptr() if root else None, stream_handle(x.device))
+    _lib.check(rc, "kblas_mv_mgpu_partial_p2p_async")
+    return out
