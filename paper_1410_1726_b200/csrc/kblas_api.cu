@@ -620,9 +620,9 @@ cudaError_t dispatch_gemv(char trans, const Path<T> &pa, long long lda, int m, i
   if (trans == 'c' && is_cplx<T>())                                                                          \
     return run_gemv_t<T, C::V, NW, CW, R, true, MB>(pa, lda, m, n, nglob, x, cm, y, alpha, beta, beta_zero, st);   \
   return run_gemv_t<T, C::V, NW, CW, R, false, MB>(pa, lda, m, n, nglob, x, cm, y, alpha, beta, beta_zero, st);
+    // (variants 1 = 4x4x1 at 4 CTAs/SM and 2 = 8x2x2 were measured and
+    // dropped: profiles/r1j_tune_gemv_*.jsonl)
     switch (gv) {
-      case 1: KB_GV(4, 4, 1, 4)
-      case 2: KB_GV(8, 2, 2, 2)
       case 3: KB_GV(4, 4, 2, 2)
       default: KB_GV(16, 4, 1, 1)
     }
@@ -656,16 +656,11 @@ cudaError_t dispatch_symv_h(bool lower, const Path<T> &pa, long long lda, int d,
     if constexpr (sizeof(T) == 16) {
       switch (g_symv_variant < 0 ? default_variant<T>() : g_symv_variant) {
         case 1: KB_TMA(8, 8, 2, 3);
-        case 2: KB_TMA(16, 8, 1, 3);
-        case 3: KB_TMA(8, 16, 1, 3);
         default: KB_TMA(16, 4, 1, 5);
       }
     } else {
       switch (g_symv_variant < 0 ? default_variant<T>() : g_symv_variant) {
         case 1: KB_TMA(16, 8, 1, 5);
-        case 2: KB_TMA(8, 8, 4, 3);
-        case 3: KB_TMA(16, 8, 4, 1);
-        case 4: KB_TMA(8, 16, 2, 3);
         default: KB_TMA(16, 8, 2, 3);
       }
     }
@@ -685,16 +680,10 @@ cudaError_t dispatch_symv_h(bool lower, const Path<T> &pa, long long lda, int d,
   // there are enough items to occupy every SM
   int v = g_symv_variant;
   if (v < 100 && d <= g_symv_narrow_max) v = 103;
+  // (variants 101/102/104/108 and the column-rolling / split-barrier
+  // kernels were measured and dropped: profiles/r1h_tune_symv_*.jsonl)
   switch (v) {
-    case 101: KB_REG(C::V, 16, (sizeof(T) == 16 ? 4 : 4), 2);  // 2 KiB column segments
-    case 102: KB_REG(C::V, 8, (sizeof(T) == 16 ? 8 : 16), 1);  // 8 warps, wider per-warp column sets
     case 103: KB_REG(C::V, 8, 4, 1);                           // 8 warps x 4 columns (small operands)
-    case 104: KB_REG(C::V, 8, 8, 1);                           // 8 warps x 8 columns
-    case 108:                                                  // 16 warps x 8 columns, x_col in shared memory
-      return lower ? run_symv<T, C::V, 16, 8, 1, true, HERM, 1, true>(pa, lda, d, x, cm, ncols_local, y, alpha,
-                                                                      beta, beta_zero, st)
-                   : run_symv<T, C::V, 16, 8, 1, false, HERM, 1, true>(pa, lda, d, x, cm, ncols_local, y, alpha,
-                                                                       beta, beta_zero, st);
     case 105:                                                  // 8 warps x 8 columns, 2 CTAs per SM
       return lower ? run_symv<T, C::V, 8, (sizeof(T) == 16 ? 4 : 8), 1, true, HERM, 2>(
                          pa, lda, d, x, cm, ncols_local, y, alpha, beta, beta_zero, st)

@@ -28,7 +28,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--ops", default="dsymv,zhemv,ssymv,chemv")
     ap.add_argument("--sizes", default="8192,16384,32768")
-    ap.add_argument("--variants", default="0,1,2,3,4")
+    ap.add_argument("--variants", default="0,1,103,105")
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--out", default=None)
     args = ap.parse_args()
