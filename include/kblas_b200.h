@@ -251,6 +251,46 @@ int kblas_zsymv_mgpu(char uplo, int n, cuDoubleComplex alpha, cuDoubleComplex *c
                      int lda, cuDoubleComplex *const *dx, int incx, cuDoubleComplex beta,
                      cuDoubleComplex *const *dy, int incy, int ngpus, int nb,
                      const int *device_ids);
+/* _async forms (every routine has one): streams[g] is */
+/* the stream on GPU g; the root's combine runs on streams[0] after     */
+/* events from the others; nothing is waited for on the host.  A       */
+/* non-NULL streams array is required (last argument index).           */
+int kblas_sgemv_mgpu_async(char trans, int m, int n, float alpha, float *const *dA, int lda,
+                           float *const *dx, int incx, float beta, float *const *dy, int incy,
+                           int ngpus, int nb, const int *device_ids, cudaStream_t const *streams);
+int kblas_dgemv_mgpu_async(char trans, int m, int n, double alpha, double *const *dA, int lda,
+                           double *const *dx, int incx, double beta, double *const *dy, int incy,
+                           int ngpus, int nb, const int *device_ids, cudaStream_t const *streams);
+int kblas_cgemv_mgpu_async(char trans, int m, int n, cuFloatComplex alpha,
+                           cuFloatComplex *const *dA, int lda, cuFloatComplex *const *dx, int incx,
+                           cuFloatComplex beta, cuFloatComplex *const *dy, int incy, int ngpus,
+                           int nb, const int *device_ids, cudaStream_t const *streams);
+int kblas_zgemv_mgpu_async(char trans, int m, int n, cuDoubleComplex alpha,
+                           cuDoubleComplex *const *dA, int lda, cuDoubleComplex *const *dx,
+                           int incx, cuDoubleComplex beta, cuDoubleComplex *const *dy, int incy,
+                           int ngpus, int nb, const int *device_ids, cudaStream_t const *streams);
+int kblas_ssymv_mgpu_async(char uplo, int n, float alpha, float *const *dA, int lda,
+                           float *const *dx, int incx, float beta, float *const *dy, int incy,
+                           int ngpus, int nb, const int *device_ids, cudaStream_t const *streams);
+int kblas_dsymv_mgpu_async(char uplo, int n, double alpha, double *const *dA, int lda,
+                           double *const *dx, int incx, double beta, double *const *dy, int incy,
+                           int ngpus, int nb, const int *device_ids, cudaStream_t const *streams);
+int kblas_chemv_mgpu_async(char uplo, int n, cuFloatComplex alpha, cuFloatComplex *const *dA,
+                           int lda, cuFloatComplex *const *dx, int incx, cuFloatComplex beta,
+                           cuFloatComplex *const *dy, int incy, int ngpus, int nb,
+                           const int *device_ids, cudaStream_t const *streams);
+int kblas_zhemv_mgpu_async(char uplo, int n, cuDoubleComplex alpha, cuDoubleComplex *const *dA,
+                           int lda, cuDoubleComplex *const *dx, int incx, cuDoubleComplex beta,
+                           cuDoubleComplex *const *dy, int incy, int ngpus, int nb,
+                           const int *device_ids, cudaStream_t const *streams);
+int kblas_csymv_mgpu_async(char uplo, int n, cuFloatComplex alpha, cuFloatComplex *const *dA,
+                           int lda, cuFloatComplex *const *dx, int incx, cuFloatComplex beta,
+                           cuFloatComplex *const *dy, int incy, int ngpus, int nb,
+                           const int *device_ids, cudaStream_t const *streams);
+int kblas_zsymv_mgpu_async(char uplo, int n, cuDoubleComplex alpha, cuDoubleComplex *const *dA,
+                           int lda, cuDoubleComplex *const *dx, int incx, cuDoubleComplex beta,
+                           cuDoubleComplex *const *dy, int incy, int ngpus, int nb,
+                           const int *device_ids, cudaStream_t const *streams);
 
 /* Per-device partial only (no cross-device reduction, no beta): the    */
 /* building block for one-process-per-GPU deployments, where the       */
@@ -311,6 +351,19 @@ int kblas_p2p_combine_async(char prec, int nranks, const void *slots, long long 
 /* ------------------------------------------------------------------ */
 int kblas_mgpu_local_cols(int n, int nb, int ngpus, int gpu);
 int kblas_mgpu_local_ld(int m);
+/* Allocate (free) every GPU's local panel for an m x n matrix in the   */
+/* cyclic layout, ld = kblas_mgpu_local_ld(m) returned in *ldda; an     */
+/* idle GPU gets NULL (multidevice.py:81-93).  "KBLAS provides          */
+/* functions that allocate the necessary memory space on each GPU"      */
+/* (PAPER.md:425-427).                                                  */
+int kblas_malloc_mgpu_1d(int m, int n, size_t esize, void **dA, int *ldda, int ngpus, int nb,
+                         const int *device_ids);
+int kblas_free_mgpu(void **dA, int ngpus, const int *device_ids);
+/* The distribution block width to use with the mgpu routines for this */
+/* precision and kind ('g' gemv, 's' symv/hemv): the SYMV tile width,  */
+/* so tiles never straddle a block ("KBLAS exposes   */
+/* such values through another set of functions").                     */
+int kblas_mgpu_block_size(char prec, char kind);
 /* Copy the global host matrix into (pre-allocated) local panels, and   */
 /* back (blockmv.distribute / gather, multidevice.py:72-110).  esize is */
 /* the element size in bytes.                                          */

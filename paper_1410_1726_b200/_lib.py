@@ -89,6 +89,8 @@ def load():
                 f.restype = c_int
             getattr(lib, f"kblas_{tag}gemv_mgpu").argtypes = _mgpu_argtypes("gemv", tag)
             getattr(lib, f"kblas_{tag}gemv_mgpu").restype = c_int
+            getattr(lib, f"kblas_{tag}gemv_mgpu_async").argtypes = _mgpu_argtypes("gemv", tag) + [POINTER(c_void_p)]
+            getattr(lib, f"kblas_{tag}gemv_mgpu_async").restype = c_int
             for name in SYMV_NAMES[tag]:
                 for suffix, extra in (
                     ("", ()),
@@ -101,6 +103,9 @@ def load():
                     f.restype = c_int
                 getattr(lib, f"kblas_{name}_mgpu").argtypes = _mgpu_argtypes("symv", tag)
                 getattr(lib, f"kblas_{name}_mgpu").restype = c_int
+                getattr(lib, f"kblas_{name}_mgpu_async").argtypes = (_mgpu_argtypes("symv", tag)
+                                                                     + [POINTER(c_void_p)])
+                getattr(lib, f"kblas_{name}_mgpu_async").restype = c_int
         lib.kblas_mv_mgpu_partial_async.argtypes = [
             c_char, c_char, c_char, c_int, c_int, c_void_p, c_void_p, c_int, c_void_p, c_void_p,
             c_int, c_int, c_int, c_int, c_void_p,
@@ -128,6 +133,13 @@ def load():
         lib.kblas_mv_hostvec.restype = c_int
         lib.kblas_mgpu_local_cols.argtypes = [c_int, c_int, c_int, c_int]
         lib.kblas_mgpu_local_cols.restype = c_int
+        lib.kblas_malloc_mgpu_1d.argtypes = [c_int, c_int, c_size_t, POINTER(c_void_p), POINTER(c_int), c_int,
+                                             c_int, POINTER(c_int)]
+        lib.kblas_malloc_mgpu_1d.restype = c_int
+        lib.kblas_free_mgpu.argtypes = [POINTER(c_void_p), c_int, POINTER(c_int)]
+        lib.kblas_free_mgpu.restype = c_int
+        lib.kblas_mgpu_block_size.argtypes = [c_char, c_char]
+        lib.kblas_mgpu_block_size.restype = c_int
         lib.kblas_mgpu_local_ld.argtypes = [c_int]
         lib.kblas_mgpu_local_ld.restype = c_int
         for name in ("kblas_setmatrix_mgpu_1d", "kblas_getmatrix_mgpu_1d"):

@@ -796,33 +796,38 @@ int partial_entry(bool is_gemv, char op, bool herm, int m, int n, T alpha, const
   return code(dispatch_symv<T>(op == 'l', herm, pa, lda, n, dx, cm, (int)lc, dpart, alpha, zero<T>(), true, st));
 }
 
+// streams: one per GPU (the _async entry points) or
+// null for each device's legacy default stream plus a final wait
 template <class T>
 int mgpu_entry(bool is_gemv, char op, bool herm, int m, int n, T alpha, T *const *dA, int lda, T *const *dx,
-               T beta, T *const *dy, int ngpus, int nb, const int *device_ids) {
+               T beta, T *const *dy, int ngpus, int nb, const int *device_ids, cudaStream_t const *streams = nullptr) {
   if (ngpus < 1 || ngpus > kMaxGpus) return -13;
   if (nb < 1) return -14;
   DevGuard guard;
   auto devof = [&](int g) { return device_ids ? device_ids[g] : g; };
+  auto stof = [&](int g) { return streams ? streams[g] : (cudaStream_t)0; };
+  const bool sync = streams == nullptr;
   const long long ylen = is_gemv ? ((op == 'n') ? m : n) : n;
   const int root = devof(0);
+  const cudaStream_t rst = stof(0);
   cudaError_t e;
   if (ylen == 0) return 0;
   if (is_zero(alpha) && is_one(beta)) return 0;
   if (is_zero(alpha) || (is_gemv && (m == 0 || n == 0))) {
     cudaSetDevice(root);
-    int rc = scal_only(dy[0], ylen, beta, 0);
+    int rc = scal_only(dy[0], ylen, beta, rst);
     if (rc) return rc;
-    return code(cudaStreamSynchronize(0));
+    return sync ? code(cudaStreamSynchronize(rst)) : 0;
   }
   // root's own partial lives in a workspace slot (dy[0] holds the input y)
   cudaSetDevice(root);
   void *rootbuf = nullptr;
-  // separate from the kernel workspace: allocate once per device
+  // separate from the kernel workspace: allocated once per (device, root stream)
   static std::mutex mu;
-  static std::map<int, WsBuf> rootbufs;
+  static std::map<std::pair<int, cudaStream_t>, WsBuf> rootbufs;
   {
     std::lock_guard<std::mutex> lk(mu);
-    WsBuf &b = rootbufs[root];
+    WsBuf &b = rootbufs[{root, rst}];
     const size_t need = (size_t)ylen * sizeof(T) * (ngpus + 1);
     if (b.bytes < need) {
       if (b.ptr) { cudaDeviceSynchronize(); cudaFree(b.ptr); }
@@ -838,16 +843,16 @@ int mgpu_entry(bool is_gemv, char op, bool herm, int m, int n, T alpha, T *const
     const int dev = devof(g);
     if ((e = cudaSetDevice(dev)) != cudaSuccess) return code(e);
     T *out = (g == 0) ? root_part : dy[g];
-    int rc = partial_entry<T>(is_gemv, op, herm, m, n, alpha, dA[g], lda, dx[g], out, ngpus, g, nb, 0);
+    int rc = partial_entry<T>(is_gemv, op, herm, m, n, alpha, dA[g], lda, dx[g], out, ngpus, g, nb, stof(g));
     if (rc) return rc;
     cudaEventCreateWithFlags(&done[g], cudaEventDisableTiming);
-    cudaEventRecord(done[g], 0);
+    cudaEventRecord(done[g], stof(g));
   }
   cudaSetDevice(root);
   PartList<T> parts{};
   for (int g = 0; g < ngpus; ++g) {
     const int dev = devof(g);
-    cudaStreamWaitEvent(0, done[g], 0);
+    cudaStreamWaitEvent(rst, done[g], 0);
     if (g == 0 || dev == root) {
       parts.p[g] = (g == 0) ? root_part : dy[g];
       continue;
@@ -863,16 +868,38 @@ int mgpu_entry(bool is_gemv, char op, bool herm, int m, int n, T alpha, T *const
       parts.p[g] = dy[g];  // NVLink peer load inside the combine kernel
     } else {
       T *slot = root_part + (size_t)ylen * g;
-      if ((e = cudaMemcpyPeerAsync(slot, root, dy[g], dev, ylen * sizeof(T), 0)) != cudaSuccess) return code(e);
+      if ((e = cudaMemcpyPeerAsync(slot, root, dy[g], dev, ylen * sizeof(T), rst)) != cudaSuccess) return code(e);
       parts.p[g] = slot;
     }
   }
-  mgpu_combine_kernel<T><<<(unsigned)cdiv(ylen, 256), 256>>>(dy[0], parts, ngpus, ylen, beta, is_zero(beta) ? 1 : 0);
+  mgpu_combine_kernel<T><<<(unsigned)cdiv(ylen, 256), 256, 0, rst>>>(dy[0], parts, ngpus, ylen, beta,
+                                                                     is_zero(beta) ? 1 : 0);
   launched();
   e = cudaGetLastError();
-  if (e == cudaSuccess) e = cudaStreamSynchronize(0);
-  for (auto ev : done) if (ev) cudaEventDestroy(ev);
+  if (e == cudaSuccess && sync) e = cudaStreamSynchronize(rst);
+  for (auto ev : done) if (ev) cudaEventDestroy(ev);  // released once complete
   return code(e);
+}
+
+// per-GPU panels of the 1D block-column-cyclic layout
+int malloc_mgpu(int m, int n, size_t esize, void **dA, int *ldda, int ngpus, int nb, const int *device_ids) {
+  if (m < 0 || n < 0 || esize == 0 || dA == nullptr || ngpus < 1 || nb < 1) return -1;
+  DevGuard guard;
+  const long long ld = cdiv(std::max(m, 1), 32) * 32;
+  if (ldda) *ldda = (int)ld;
+  for (int g = 0; g < ngpus; ++g) {
+    dA[g] = nullptr;
+    const long long lc = local_cols(n, nb, ngpus, g);
+    if (lc == 0) continue;  // idle GPU (multidevice.py:81-83)
+    cudaError_t e = cudaSetDevice(device_ids ? device_ids[g] : g);
+    if (e == cudaSuccess) e = cudaMalloc(&dA[g], (size_t)ld * lc * esize);
+    if (e != cudaSuccess) {
+      for (int h = 0; h < g; ++h)
+        if (dA[h]) { cudaSetDevice(device_ids ? device_ids[h] : h); cudaFree(dA[h]); dA[h] = nullptr; }
+      return (int)e;
+    }
+  }
+  return 0;
 }
 
 // Host-vector call: x (and y when beta != 0) are host arrays, A is in HBM.
@@ -1012,6 +1039,19 @@ extern "C" {
     if (incx != 1) return -8;                                                                                  \
     if (incy != 1) return -11;                                                                                 \
     return mgpu_entry<T>(true, t, false, m, n, alpha, dA, lda, dx, beta, dy, ngpus, nb, device_ids);          \
+  }                                                                                                            \
+  int kblas_##P##gemv_mgpu_async(char trans, int m, int n, T alpha, T *const *dA, int lda, T *const *dx,      \
+                                 int incx, T beta, T *const *dy, int incy, int ngpus, int nb,                 \
+                                 const int *device_ids, cudaStream_t const *streams) {                        \
+    char t = (char)(trans | 0x20);                                                                             \
+    if (t != 'n' && t != 't' && t != 'c') return -1;                                                           \
+    if (m < 0) return -2;                                                                                      \
+    if (n < 0) return -3;                                                                                      \
+    if (lda < std::max(1, m)) return -6;                                                                       \
+    if (incx != 1) return -8;                                                                                  \
+    if (incy != 1) return -11;                                                                                 \
+    if (streams == nullptr) return -16;                                                                        \
+    return mgpu_entry<T>(true, t, false, m, n, alpha, dA, lda, dx, beta, dy, ngpus, nb, device_ids, streams); \
   }
 
 #define KB_SYMV(NAME, T, HERM)                                                                                \
@@ -1040,6 +1080,18 @@ extern "C" {
     if (incx != 1) return -7;                                                                                  \
     if (incy != 1) return -10;                                                                                 \
     return mgpu_entry<T>(false, u, HERM, n, n, alpha, dA, lda, dx, beta, dy, ngpus, nb, device_ids);          \
+  }                                                                                                            \
+  int kblas_##NAME##_mgpu_async(char uplo, int n, T alpha, T *const *dA, int lda, T *const *dx, int incx,      \
+                                T beta, T *const *dy, int incy, int ngpus, int nb, const int *device_ids,     \
+                                cudaStream_t const *streams) {                                                 \
+    const char u = (char)(uplo | 0x20);                                                                        \
+    if (u != 'l' && u != 'u') return -1;                                                                       \
+    if (n < 0) return -2;                                                                                      \
+    if (lda < std::max(1, n)) return -5;                                                                       \
+    if (incx != 1) return -7;                                                                                  \
+    if (incy != 1) return -10;                                                                                 \
+    if (streams == nullptr) return -14;                                                                        \
+    return mgpu_entry<T>(false, u, HERM, n, n, alpha, dA, lda, dx, beta, dy, ngpus, nb, device_ids, streams); \
   }
 
 KB_GEMV(s, float)
@@ -1074,6 +1126,33 @@ int kblas_mgpu_local_cols(int n, int nb, int ngpus, int gpu) {
 }
 
 int kblas_mgpu_local_ld(int m) { return (int)(cdiv(std::max(m, 1), 32) * 32); }
+
+int kblas_malloc_mgpu_1d(int m, int n, size_t esize, void **dA, int *ldda, int ngpus, int nb,
+                         const int *device_ids) {
+  return malloc_mgpu(m, n, esize, dA, ldda, ngpus, nb, device_ids);
+}
+
+int kblas_free_mgpu(void **dA, int ngpus, const int *device_ids) {
+  if (dA == nullptr || ngpus < 1) return -1;
+  DevGuard guard;
+  for (int g = 0; g < ngpus; ++g) {
+    if (!dA[g]) continue;
+    cudaSetDevice(device_ids ? device_ids[g] : g);
+    cudaError_t e = cudaFree(dA[g]);
+    if (e != cudaSuccess) return (int)e;
+    dA[g] = nullptr;
+  }
+  return 0;
+}
+
+// the SYMV/HEMV tile width: a distribution block of this width (or a
+// multiple) keeps every tile inside one block, so no tile is cut short
+int kblas_mgpu_block_size(char prec, char kind) {
+  const char p = (char)(prec | 0x20), k = (char)(kind | 0x20);
+  if (p != 's' && p != 'd' && p != 'c' && p != 'z') return -1;
+  if (k != 'g' && k != 's') return -2;
+  return 128;
+}
 
 static int copy_mgpu(bool to_dev, int m, int n, size_t esize, const void *hA_c, void *hA, int ldha,
                      void *const *dA, int ldda, int ngpus, int nb, const int *device_ids) {

@@ -326,6 +326,55 @@ class TestCAbi:
         check(ys[0], want, "d", 0.5, np.abs(naive.dense_from_triangle(a, "l", False)), x, -1.0, y)
 
 
+    @pytest.mark.parametrize("kind", ["zhemv", "sgemv_t", "dgemv_n"])
+    def test_mgpu_async_c_entries_and_allocation(self, kind):
+        """kblas_malloc_mgpu_1d + kblas_setmatrix_mgpu_1d + the _mgpu_async
+        entry on user streams (every logical GPU on device 0), checked against
+        the oracle; then kblas_free_mgpu."""
+        lib = _lib.load()
+        tag = kind[0]
+        rng = np.random.default_rng(43)
+        m = n = 700
+        G = 3
+        nb = lib.kblas_mgpu_block_size(tag.encode(), b"s" if "mv" in kind and "gemv" not in kind else b"g")
+        assert nb == 128
+        a = naive.fill(rng, (m, n), tag)
+        a_f = np.asfortranarray(a)
+        esize = a.dtype.itemsize
+        arr = ctypes.c_void_p * G
+        dA = arr()
+        ldda = ctypes.c_int(0)
+        ids = (ctypes.c_int * G)(*([0] * G))
+        assert lib.kblas_malloc_mgpu_1d(m, n, esize, dA, ctypes.byref(ldda), G, nb, ids) == 0
+        assert ldda.value == 704 and all(dA[g] for g in range(G))
+        assert lib.kblas_setmatrix_mgpu_1d(m, n, esize, a_f.ctypes.data, m, dA, ldda.value, G, nb, ids) == 0
+        dt = DT[tag]
+        trans = kind.split("_")[1] if "_" in kind else None
+        xl, yl = (n, m) if trans in (None, "n") else (m, n)
+        x, y = naive.fill(rng, xl, tag), naive.fill(rng, yl, tag)
+        xs = [dvec(x) for _ in range(G)]
+        ys = [dvec(y)] + [torch.empty(yl, dtype=dt, device="cuda") for _ in range(G - 1)]
+        streams = [torch.cuda.Stream() for _ in range(G)]
+        pst = arr(*[s.cuda_stream for s in streams])
+        px, py = arr(*[t.data_ptr() for t in xs]), arr(*[t.data_ptr() for t in ys])
+        torch.cuda.synchronize()
+        al, be = _lib.scalar(tag, 0.5), _lib.scalar(tag, -1.0)
+        if kind == "zhemv":
+            rc = lib.kblas_zhemv_mgpu_async(b"L", n, al, dA, ldda.value, px, 1, be, py, 1, G, nb, ids, pst)
+            want = naive.naive_symv_hemv(0.5, np.tril(a), "l", x, -1.0, y, hermitian=True)
+            dense = np.abs(naive.dense_from_triangle(np.tril(a), "l", True))
+        else:
+            f = getattr(lib, f"kblas_{tag}gemv_mgpu_async")
+            rc = f(trans.encode(), m, n, al, dA, ldda.value, px, 1, be, py, 1, G, nb, ids, pst)
+            want = naive.naive_gemv(trans, 0.5, a, x, -1.0, y)
+            dense = np.abs(a) if trans == "n" else np.abs(a).T
+        assert rc == 0
+        streams[0].synchronize()
+        check(ys[0], want, tag, 0.5, dense, x, -1.0, y)
+        assert lib.kblas_free_mgpu(dA, G, ids) == 0
+        assert not any(dA[g] for g in range(G))
+
+
 class TestLarge:
     """Sizes the numpy oracle cannot hold comfortably: the streamed C oracle
     (all host threads) and size-independent properties."""
