@@ -428,6 +428,11 @@ int kblas_set_gemv_split(int mode);
 /* (warps, columns per warp, vectors per lane, CTAs per SM); 0 = tuned   */
 /* default.  Returns the previous variant.                               */
 int kblas_set_gemv_variant(int variant);
+/* Select the GEMV-T/C form: -1 (default) = automatic (column-owning    */
+/* CTAs, one kernel, for operands up to max_bytes with >= 2 CTAs per SM; */
+/* stream-K otherwise), 1 = always, 0 = never.  max_bytes <= 0 keeps    */
+/* the current threshold.  Returns the previous mode.                   */
+int kblas_set_gemv_tc(int mode, long long max_bytes);
 /* Register SYMV/HEMV kernel: orders up to max_order use narrow column */
 /* tiles (more work items for small operands).  Returns the previous   */
 /* threshold (default 2048).                                           */

@@ -316,9 +316,52 @@ cudaError_t run_gemv_n(const Path<T> &pa, long long lda, int m, int n, const T *
 }
 
 // ============================================================= GEMV-T/C
+// column-owning form (gemv_tc_kernel) choice: -1 auto, 0 never, 1 always
+int g_gemv_tc = -1;
+long long g_gemv_tc_max_bytes = 80LL << 20;
+
+template <class T, int V, int NW, int CB, bool CONJ>
+cudaError_t run_gemv_tc(const Path<T> &pa, long long lda, int m, int n, long long nglob, const T *x, ColMap cm,
+                        T *y, T alpha, T beta, bool beta_zero, cudaStream_t st) {
+  auto kfn = gemv_tc_kernel<T, V, NW, CB, CONJ>;
+  if (cm.G > 1) {
+    // mgpu partial: columns this GPU does not own stay zero
+    cudaError_t e = cudaMemsetAsync(y, 0, (size_t)nglob * sizeof(T), st);
+    if (e != cudaSuccess) return e;
+  }
+  const long long P = cdiv(n, CB);
+  GemvParams p{pa.base, lda, m, n, pa.lead, x, nullptr, 0, 0, (int)P, 0, cm,
+               y, nullptr, widen(alpha), widen(beta), beta_zero ? 1 : 0, nglob};
+  {
+    TimedScope ts(st);
+    kfn<<<(unsigned)P, NW * 32, 0, st>>>(p);
+  }
+  launched(1);
+  char buf[256];
+  snprintf(buf, sizeof buf, "gemv_tc %s %s%s lead=%d m=%d n=%d H=%d CB=%d P=%lld slots=1", tname<T>(),
+           V > 1 ? "v256" : "scalar", CONJ ? " conj" : "", pa.lead, m, n, 32 * V, CB, P);
+  g_last_plan = buf;
+  return cudaGetLastError();
+}
+
 template <class T, int V, int NW, int CW, int R, bool CONJ, int MINB = 2>
 cudaError_t run_gemv_t(const Path<T> &pa, long long lda, int m, int n, long long nglob, const T *x,
                        ColMap cm, T *y, T alpha, T beta, bool beta_zero, cudaStream_t st) {
+  {
+    // whole columns per CTA, one kernel with no cross-CTA reduction
+    // (profiles/r1p_tune_gemv_tc.jsonl): wins for every operand up to
+    // 80 MB, and at every size for d and z, as long as the grid is not cut
+    // badly by the wave count; s and c stay on stream-K above 80 MB
+    constexpr int CBc = 4;
+    const long long Pc = cdiv(n, CBc);
+    const long long slots = (long long)dev_sms() * 2;
+    const double eff = (double)Pc / (double)(cdiv(Pc, slots) * slots);
+    const bool enough = Pc >= dev_sms() / 2;
+    const bool small = (long long)m * n * (long long)sizeof(T) <= g_gemv_tc_max_bytes;
+    const bool any_size = (sizeof(T) == 16 || (sizeof(T) == 8 && !is_cplx<T>())) && eff >= 0.8;
+    if (g_gemv_tc == 1 || (g_gemv_tc == -1 && enough && (small || any_size)))
+      return run_gemv_tc<T, V, 8, CBc, CONJ>(pa, lda, m, n, nglob, x, cm, y, alpha, beta, beta_zero, st);
+  }
   constexpr int H = 32 * V * R, CBW = NW * CW;
   auto kfn = gemv_t_kernel<T, V, NW, CW, R, CONJ, MINB>;
   const long long ncb = cdiv(n, CBW);
@@ -1352,6 +1395,13 @@ int kblas_set_symv_narrow(int max_order) {
 int kblas_set_gemv_variant(int v) {
   const int prev = g_gemv_variant;
   g_gemv_variant = v;
+  return prev;
+}
+
+int kblas_set_gemv_tc(int mode, long long max_bytes) {
+  const int prev = g_gemv_tc;
+  g_gemv_tc = mode < 0 ? -1 : (mode ? 1 : 0);
+  if (max_bytes > 0) g_gemv_tc_max_bytes = max_bytes;
   return prev;
 }
 

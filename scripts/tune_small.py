@@ -52,6 +52,14 @@ def forms(family, op, tag):
     if family == "gemv" and op == "n":
         return {"auto": lambda: _lib.set_gemv_split(-1), "split": lambda: _lib.set_gemv_split(1),
                 "stacked": lambda: _lib.set_gemv_split(0)}
+    if family == "gemv":
+        return {"auto": lambda: _lib.load().kblas_set_gemv_tc(-1, 80 << 20),
+                "tc": lambda: _lib.load().kblas_set_gemv_tc(1, 0),
+                "streamk": lambda: _lib.load().kblas_set_gemv_tc(0, 0)}
+    if family == "gemv":
+        return {"auto": lambda: _lib.load().kblas_set_gemv_tc(-1, 80 << 20),
+                "tc": lambda: _lib.load().kblas_set_gemv_tc(1, 0),
+                "streamk": lambda: _lib.load().kblas_set_gemv_tc(0, 0)}
     if family == "symv":
         big = 1 << 30
         f = {"auto": lambda: reset(),
@@ -68,6 +76,7 @@ DEFAULTS = {}
 
 def reset():
     _lib.set_gemv_split(-1)
+    _lib.load().kblas_set_gemv_tc(-1, 80 << 20)
     _lib.set_tma(-1)
     if not DEFAULTS:  # the library's built-in thresholds
         DEFAULTS["narrow"] = _lib.set_symv_narrow(0)

@@ -643,3 +643,42 @@ class TestHostVectorPath:
                                     x.ctypes.data, ctypes.addressof(one), y.ctypes.data, y.ctypes.data, None) == -2
         assert lib.kblas_mv_hostvec(b"d", b"g", b"n", 0, 4, 4, ctypes.addressof(one), v.data.data_ptr(), 300, 0, 0,
                                     None, ctypes.addressof(one), y.ctypes.data, y.ctypes.data, None) == -1
+
+
+@pytest.fixture(params=["tc", "streamk"])
+def gemv_t_form(request):
+    """GEMV-T/C in the column-owning form (whole columns per CTA) and in
+    the stream-K form (split rows, cross-CTA partials)."""
+    lib = _lib.load()
+    prev = lib.kblas_set_gemv_tc(1 if request.param == "tc" else 0, 0)
+    yield request.param
+    lib.kblas_set_gemv_tc(prev, 0)
+
+
+class TestGemvTForms:
+    @pytest.mark.parametrize("tag", "sdcz")
+    def test_oracle_both_forms(self, gemv_t_form, tag):
+        rng = np.random.default_rng(161)
+        for m, n in [(1, 1), (7, 5), (65, 33), (3000, 100), (37, 1000), (2049, 1537)]:
+            for ld, ro in ((-(-m // 32) * 32 + 32, 0), (m + 11, 5), (m + 40, 3)):
+                host = np.full(ld * n, np.nan, dtype=naive.DTYPES[tag])
+                win = naive.window(host, ld, ro + m, n)
+                a = naive.fill(rng, (m, n), tag)
+                win[ro:ro + m, :] = a
+                v = kb.MatrixView(torch.from_numpy(host).cuda(), ro + m, n, ld, kb.precision(tag)).submatrix(
+                    ro, 0, m, n)
+                for trans in "tc":
+                    x, y = naive.fill(rng, m, tag), naive.fill(rng, n, tag)
+                    rep = kb.gemv(trans, 0.7, v, dvec(x), -0.3, dvec(y))
+                    if gemv_t_form == "tc":
+                        assert rep.plan.startswith("gemv_tc"), rep.plan
+                    assert torch.isfinite(rep.y_out).all()
+                    dense = np.abs(a).T
+                    check(rep.y_out, naive.naive_gemv(trans, 0.7, a, x, -0.3, y), tag, 0.7, dense, x, -0.3, y)
+
+    def test_mgpu_partial_tc(self, gemv_t_form):
+        rng = np.random.default_rng(162)
+        v, a = dev_matrix(rng, 900, 1300, "z")
+        x, y = naive.fill(rng, 900, "z"), naive.fill(rng, 1300, "z")
+        merged, _ = kb.gemv_mgpu("c", 1.1, kb.distribute(v, 64, 3), x, 0.4, y)
+        check(merged.y_out, naive.naive_gemv("c", 1.1, a, x, 0.4, y), "z", 1.1, np.abs(a).T, x, 0.4, y)
