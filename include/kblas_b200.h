@@ -433,6 +433,9 @@ int kblas_set_gemv_variant(int variant);
 /* stream-K otherwise), 1 = always, 0 = never.  max_bytes <= 0 keeps    */
 /* the current threshold.  Returns the previous mode.                   */
 int kblas_set_gemv_tc(int mode, long long max_bytes);
+/* Split-form GEMV-N grid: CTAs per row block sized for this many waves */
+/* of the GPU (>= 1).  Returns the previous value.                      */
+int kblas_set_gemv_split_waves(int waves);
 /* Register SYMV/HEMV kernel: orders up to max_order use narrow column */
 /* tiles (more work items for small operands).  Returns the previous   */
 /* threshold (default 2048).                                           */

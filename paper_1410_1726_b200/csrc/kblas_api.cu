@@ -238,6 +238,7 @@ template <class T> struct Cfg {
 // (kblas_set_gemv_split, for the tuner).
 int g_gemv_split = -1;
 int g_gemv_variant = 0;  // 0: tuned default shape (kblas_set_gemv_variant)
+int g_split_waves = 1;   // split-form GEMV-N: CTAs per row block sized for this many waves
 constexpr long long kSplitMaxSlots = 64;
 
 template <class T, int V, int NW, int CW>
@@ -284,11 +285,20 @@ cudaError_t run_gemv_n(const Path<T> &pa, long long lda, int m, int n, const T *
     constexpr int NWs = 8, CWs = 4, RBs = 32 * V;
     const long long nrb_s = cdiv((long long)pa.lead + m, RBs);
     const long long Ps = (long long)dev_sms() * occupancy((const void *)gemv_ns_kernel<T, V, NWs, CWs>, NWs * 32);
-    const long long S = std::max<long long>(
-        1, std::min<long long>({cdiv(Ps, nrb_s), kSplitMaxSlots, std::max<long long>(1, n / (NWs * CWs))}));
+    const long long S = std::max<long long>(1, std::min<long long>({cdiv((long long)g_split_waves * Ps, nrb_s),
+                                                                     kSplitMaxSlots,
+                                                                     std::max<long long>(1, n / (NWs * CWs))}));
     const bool fills = nrb_s * S >= dev_sms();
     const bool small = (long long)m * n * (long long)sizeof(T) <= (80LL << 20);
-    if (g_gemv_split == 1 || (g_gemv_split == -1 && !fused && fills && small))
+    // large operands: when at most 2 CTAs share a row block (little or no
+    // partial traffic) and the grid fills >= 85 % of its waves, the split
+    // form beats stream-K (profiles/r1q_tune_gemv_nforms.jsonl: Z N=32768
+    // 6.8 -> 7.3 TB/s, D/C +2-3 %)
+    const long long Pg = nrb_s * S;
+    const double eff = (double)Pg / (double)(cdiv(Pg, Ps) * Ps);
+    const bool large_ok = S <= 2 && eff >= 0.85 && fills;
+    const bool half_fills = 2 * nrb_s * S >= dev_sms();  // small calls are latency-bound anyway
+    if (g_gemv_split == 1 || (g_gemv_split == -1 && ((!fused && half_fills && small) || large_ok)))
       return run_gemv_ns<T, V, NWs, CWs>(pa, lda, m, n, x, cm, y, alpha, beta, beta_zero, st, S, nrb_s);
   }
   void *ws = nullptr;
@@ -1395,6 +1405,12 @@ int kblas_set_symv_narrow(int max_order) {
 int kblas_set_gemv_variant(int v) {
   const int prev = g_gemv_variant;
   g_gemv_variant = v;
+  return prev;
+}
+
+int kblas_set_gemv_split_waves(int waves) {
+  const int prev = g_split_waves;
+  if (waves >= 1) g_split_waves = waves;
   return prev;
 }
 

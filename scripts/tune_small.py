@@ -50,8 +50,11 @@ def measure_graph(fn, reps, ncopies):
 
 def forms(family, op, tag):
     if family == "gemv" and op == "n":
-        return {"auto": lambda: _lib.set_gemv_split(-1), "split": lambda: _lib.set_gemv_split(1),
-                "stacked": lambda: _lib.set_gemv_split(0)}
+        lib = _lib.load()
+        f = {"auto": lambda: reset(), "stacked": lambda: _lib.set_gemv_split(0)}
+        for w in (1, 2, 4, 8):
+            f[f"split_w{w}"] = (lambda w=w: (_lib.set_gemv_split(1), lib.kblas_set_gemv_split_waves(w)))
+        return f
     if family == "gemv":
         return {"auto": lambda: _lib.load().kblas_set_gemv_tc(-1, 80 << 20),
                 "tc": lambda: _lib.load().kblas_set_gemv_tc(1, 0),
@@ -76,6 +79,7 @@ DEFAULTS = {}
 
 def reset():
     _lib.set_gemv_split(-1)
+    _lib.load().kblas_set_gemv_split_waves(1)
     _lib.load().kblas_set_gemv_tc(-1, 80 << 20)
     _lib.set_tma(-1)
     if not DEFAULTS:  # the library's built-in thresholds
