@@ -436,6 +436,11 @@ int kblas_set_gemv_tc(int mode, long long max_bytes);
 /* Split-form GEMV-N grid: CTAs per row block sized for this many waves */
 /* of the GPU (>= 1).  Returns the previous value.                      */
 int kblas_set_gemv_split_waves(int waves);
+/* Split-form GEMV-N cross-CTA step: -1 (default) = automatic (thread-  */
+/* block clusters reduced through distributed shared memory for small  */
+/* operands), 1 = always clusters, 0 = global partial slots.  Returns   */
+/* the previous mode.                                                  */
+int kblas_set_gemv_cluster(int mode);
 /* Register SYMV/HEMV kernel: orders up to max_order use narrow column */
 /* tiles (more work items for small operands).  Returns the previous   */
 /* threshold (default 2048).                                           */

@@ -161,6 +161,8 @@ def load():
         lib.kblas_set_symv_variant.restype = c_int
         lib.kblas_set_tma.argtypes = [c_int]
         lib.kblas_set_tma.restype = c_int
+        lib.kblas_set_gemv_cluster.argtypes = [c_int]
+        lib.kblas_set_gemv_cluster.restype = c_int
         lib.kblas_set_gemv_split_waves.argtypes = [c_int]
         lib.kblas_set_gemv_split_waves.restype = c_int
         lib.kblas_set_gemv_tc.argtypes = [c_int, ctypes.c_longlong]

@@ -265,6 +265,49 @@ cudaError_t run_gemv_ns(const Path<T> &pa, long long lda, int m, int n, const T 
   return cudaGetLastError();
 }
 
+// cluster split form (gemv_nc_kernel): -1 auto, 0 never, 1 always
+int g_gemv_cluster = -1;
+
+template <class T, int V, int NW, int CW>
+cudaError_t run_gemv_nc(const Path<T> &pa, long long lda, int m, int n, const T *x, ColMap cm, T *y, T alpha,
+                        T beta, bool beta_zero, cudaStream_t st, int S, long long nrb) {
+  constexpr int RB = 32 * V;
+  auto kfn = gemv_nc_kernel<T, V, NW, CW>;
+  {
+    static std::once_flag once;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(once, [&] {
+      attr_err = cudaFuncSetAttribute((const void *)kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    });
+    if (attr_err != cudaSuccess) return attr_err;
+  }
+  GemvParams p{pa.base, lda, m, n, pa.lead, x, nullptr, 0, nrb * S, (int)(nrb * S), S, cm,
+               y, nullptr, widen(alpha), widen(beta), beta_zero ? 1 : 0, (long long)m};
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(nrb * S));
+  cfg.blockDim = dim3(NW * 32);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)S;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e;
+  {
+    TimedScope ts(st);
+    e = cudaLaunchKernelEx(&cfg, kfn, p);
+  }
+  if (e != cudaSuccess) return e;
+  launched(1);
+  char buf[256];
+  snprintf(buf, sizeof buf, "gemv_nc %s %s lead=%d m=%d n=%d RB=%d cluster=%d P=%lld slots=1", tname<T>(),
+           V > 1 ? "v256" : "scalar", pa.lead, m, n, RB, S, nrb * S);
+  g_last_plan = buf;
+  return cudaGetLastError();
+}
+
 template <class T, int V, int NW, int CW, int R, int MINB = 2>
 cudaError_t run_gemv_n(const Path<T> &pa, long long lda, int m, int n, const T *x, ColMap cm, T *y,
                        T alpha, T beta, bool beta_zero, cudaStream_t st) {
@@ -298,8 +341,16 @@ cudaError_t run_gemv_n(const Path<T> &pa, long long lda, int m, int n, const T *
     const double eff = (double)Pg / (double)(cdiv(Pg, Ps) * Ps);
     const bool large_ok = S <= 2 && eff >= 0.85 && fills;
     const bool half_fills = 2 * nrb_s * S >= dev_sms();  // small calls are latency-bound anyway
-    if (g_gemv_split == 1 || (g_gemv_split == -1 && ((!fused && half_fills && small) || large_ok)))
+    if (g_gemv_split == 1 || (g_gemv_split == -1 && ((!fused && half_fills && small) || large_ok))) {
+      // the CTAs of a row block as one cluster, reduced through DSMEM
+      // (cluster sizes 2..16; 16 is the opt-in non-portable maximum)
+      int Sc = 1;
+      while (Sc < 16 && Sc < S) Sc *= 2;
+      const bool cl_ok = S > 1 && n / Sc >= NWs * CWs && 2 * nrb_s * Sc >= dev_sms();
+      if (g_gemv_cluster == 1 || (g_gemv_cluster == -1 && cl_ok && small))
+        return run_gemv_nc<T, V, NWs, CWs>(pa, lda, m, n, x, cm, y, alpha, beta, beta_zero, st, Sc, nrb_s);
       return run_gemv_ns<T, V, NWs, CWs>(pa, lda, m, n, x, cm, y, alpha, beta, beta_zero, st, S, nrb_s);
+    }
   }
   void *ws = nullptr;
   cudaError_t e = workspace(align256((size_t)maxslots * m * sizeof(T)), st, &ws);
@@ -1405,6 +1456,12 @@ int kblas_set_symv_narrow(int max_order) {
 int kblas_set_gemv_variant(int v) {
   const int prev = g_gemv_variant;
   g_gemv_variant = v;
+  return prev;
+}
+
+int kblas_set_gemv_cluster(int mode) {
+  const int prev = g_gemv_cluster;
+  g_gemv_cluster = mode < 0 ? -1 : (mode ? 1 : 0);
   return prev;
 }
 

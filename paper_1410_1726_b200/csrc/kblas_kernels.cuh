@@ -24,6 +24,8 @@
 // lane, 1 KiB per warp per column); the warp's CW column loads are all
 // issued before any FMA so CW x 32 B per lane are in flight.
 #pragma once
+#include <cooperative_groups.h>
+
 #include "kblas_device.cuh"
 
 namespace kb {
@@ -329,6 +331,86 @@ __global__ void __launch_bounds__(NW * 32, 2) gemv_ns_kernel(const GemvParams p)
   if (p.KS > 1 && arrive_last(p.counters + rb, p.KS))
     cta_slot_sum<T, NW * 32>(ws, p.ws_ld, i0, (int)(i1 - i0), p.KS,
                              [&](int k, T sum) { axpby_out(y, i0 + k, p, sum); });
+}
+
+// ---------------------------------------------------------------------------
+// GEMV-N split form over a thread-block cluster.  The S CTAs sharing a
+// 32*V-row block form one cluster (S = cluster size, up to 16): each CTA
+// reduces its warps in shared memory as gemv_ns_kernel does, then the
+// cluster exchanges the S partial row blocks through distributed shared
+// memory (CTA rank r sums rows [r*RB/S, (r+1)*RB/S) over ranks 0..S-1 in
+// order and writes y).  No global slots, fences or atomics: the cross-CTA
+// step is two cluster barriers and on-chip DSMEM reads.
+// ---------------------------------------------------------------------------
+template <class T, int V, int NW, int CW>
+__global__ void __launch_bounds__(NW * 32, 2) gemv_nc_kernel(const GemvParams p) {
+  namespace cg = cooperative_groups;
+  constexpr int RB = 32 * V;
+  __shared__ T red[NW][RB];
+  __shared__ T part[RB];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int S = (int)cluster.num_blocks();
+  const int split = (int)cluster.block_rank();
+  const T *__restrict__ A = static_cast<const T *>(p.A);
+  const T *__restrict__ x = static_cast<const T *>(p.x);
+  T *y = static_cast<T *>(p.y);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint64_t pol = policy_evict_first();
+  const long long rb = blockIdx.x / S;
+  const int c0 = (int)((long long)split * p.n / S), c1 = (int)((long long)(split + 1) * p.n / S);
+  const long long pw = rb * RB;
+  const bool rok = pw + lane * V < (long long)p.lead + p.m;
+  T acc[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) acc[v] = zero<T>();
+  auto load = [&](int g, Pack<T, V> (&a)[CW], T (&xv)[CW]) {
+#pragma unroll
+    for (int j = 0; j < CW; ++j) {
+      const int col = g + j;
+      const bool cok = col < c1;
+      xv[j] = cok ? __ldg(x + map_col(p.cm, col)) : zero<T>();
+      ld_pack(a[j], A + (long long)col * p.lda + pw + lane * V, cok && rok, pol);
+    }
+  };
+  auto fma_group = [&](const Pack<T, V> (&a)[CW], const T (&xv)[CW]) {
+#pragma unroll
+    for (int j = 0; j < CW; ++j)
+#pragma unroll
+      for (int v = 0; v < V; ++v) acc[v] = fma_(a[j].v(v), xv[j], acc[v]);
+  };
+  constexpr int STEP = NW * CW;
+  Pack<T, V> a0[CW], a1[CW];
+  T x0[CW], x1[CW];
+  int g = c0 + warp * CW;
+  if (g < c1) load(g, a0, x0);
+  while (g < c1) {
+    const bool more = g + STEP < c1;
+    if (more) load(g + STEP, a1, x1);
+    fma_group(a0, x0);
+    if (!more) break;
+    if (g + 2 * STEP < c1) load(g + 2 * STEP, a0, x0);
+    fma_group(a1, x1);
+    g += 2 * STEP;
+  }
+#pragma unroll
+  for (int v = 0; v < V; ++v) red[warp][lane * V + v] = acc[v];
+  __syncthreads();
+  for (int t = threadIdx.x; t < RB; t += NW * 32) {
+    T sum = red[0][t];
+#pragma unroll
+    for (int w = 1; w < NW; ++w) sum = add_(sum, red[w][t]);
+    part[t] = sum;
+  }
+  cluster.sync();  // every CTA's partial row block is in its shared memory
+  const int t0 = RB * split / S, t1 = RB * (split + 1) / S;
+  for (int t = t0 + (int)threadIdx.x; t < t1; t += NW * 32) {
+    const long long i = pw + t - p.lead;
+    if (i < 0 || i >= p.m) continue;
+    T sum = *cluster.map_shared_rank(part + t, 0);
+    for (int q = 1; q < S; ++q) sum = add_(sum, *cluster.map_shared_rank(part + t, q));
+    axpby_out(y, i, p, sum);
+  }
+  cluster.sync();  // keep the partials alive until every rank has read them
 }
 
 // ---------------------------------------------------------------------------

@@ -51,9 +51,9 @@ def measure_graph(fn, reps, ncopies):
 def forms(family, op, tag):
     if family == "gemv" and op == "n":
         lib = _lib.load()
-        f = {"auto": lambda: reset(), "stacked": lambda: _lib.set_gemv_split(0)}
-        for w in (1, 2, 4, 8):
-            f[f"split_w{w}"] = (lambda w=w: (_lib.set_gemv_split(1), lib.kblas_set_gemv_split_waves(w)))
+        f = {"auto": lambda: reset(), "stacked": lambda: _lib.set_gemv_split(0),
+             "split_slots": lambda: (_lib.set_gemv_split(1), lib.kblas_set_gemv_cluster(0)),
+             "split_cluster": lambda: (_lib.set_gemv_split(1), lib.kblas_set_gemv_cluster(1))}
         return f
     if family == "gemv":
         return {"auto": lambda: _lib.load().kblas_set_gemv_tc(-1, 80 << 20),
@@ -79,6 +79,7 @@ DEFAULTS = {}
 
 def reset():
     _lib.set_gemv_split(-1)
+    _lib.load().kblas_set_gemv_cluster(-1)
     _lib.load().kblas_set_gemv_split_waves(1)
     _lib.load().kblas_set_gemv_tc(-1, 80 << 20)
     _lib.set_tma(-1)

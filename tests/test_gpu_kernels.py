@@ -523,7 +523,7 @@ class TestGemvNForms:
                 x, y = naive.fill(rng, n, tag), naive.fill(rng, m, tag)
                 rep = kb.gemv("n", 0.7, v, dvec(x), -0.3, dvec(y))
                 if gemv_form == "split":
-                    assert rep.plan.startswith("gemv_ns"), rep.plan
+                    assert rep.plan.startswith(("gemv_ns", "gemv_nc")), rep.plan
                 got = rep.y_out
                 assert torch.isfinite(got).all()
                 check(got, naive.naive_gemv("n", 0.7, a, x, -0.3, y), tag, 0.7, np.abs(a), x, -0.3, y)
@@ -546,7 +546,7 @@ class TestGemvNForms:
             v, a = dev_matrix(rng, 1024, 1024, "d")
             x, y = naive.fill(rng, 1024, "d"), naive.fill(rng, 1024, "d")
             rep = kb.gemv("n", 1.0, v, dvec(x), 1.0, dvec(y))
-            assert rep.plan.startswith("gemv_ns"), rep.plan
+            assert rep.plan.startswith(("gemv_ns", "gemv_nc")), rep.plan
             check(rep.y_out, naive.naive_gemv("n", 1.0, a, x, 1.0, y), "d", 1.0, np.abs(a), x, 1.0, y)
         finally:
             _lib.set_gemv_split(prev)
@@ -682,3 +682,44 @@ class TestGemvTForms:
         x, y = naive.fill(rng, 900, "z"), naive.fill(rng, 1300, "z")
         merged, _ = kb.gemv_mgpu("c", 1.1, kb.distribute(v, 64, 3), x, 0.4, y)
         check(merged.y_out, naive.naive_gemv("c", 1.1, a, x, 0.4, y), "z", 1.1, np.abs(a).T, x, 0.4, y)
+
+
+@pytest.fixture(params=["cluster", "slots"])
+def gemv_n_xcta(request):
+    """Split-form GEMV-N with the cross-CTA step through a thread-block
+    cluster's distributed shared memory, or through global partial slots."""
+    lib = _lib.load()
+    prev_s = _lib.set_gemv_split(1)
+    prev_c = lib.kblas_set_gemv_cluster(1 if request.param == "cluster" else 0)
+    yield request.param
+    lib.kblas_set_gemv_cluster(prev_c)
+    _lib.set_gemv_split(prev_s)
+
+
+class TestGemvNCluster:
+    @pytest.mark.parametrize("tag", "sdcz")
+    def test_oracle_cluster_and_slots(self, gemv_n_xcta, tag):
+        rng = np.random.default_rng(171)
+        for m, n in [(65, 33), (100, 3000), (1000, 37), (2049, 1537), (700, 5000)]:
+            for ld, ro in ((-(-m // 32) * 32 + 32, 0), (m + 11, 5)):
+                host = np.full(ld * n, np.nan, dtype=naive.DTYPES[tag])
+                win = naive.window(host, ld, ro + m, n)
+                a = naive.fill(rng, (m, n), tag)
+                win[ro:ro + m, :] = a
+                v = kb.MatrixView(torch.from_numpy(host).cuda(), ro + m, n, ld, kb.precision(tag)).submatrix(
+                    ro, 0, m, n)
+                x, y = naive.fill(rng, n, tag), naive.fill(rng, m, tag)
+                r1 = kb.gemv("n", 0.7, v, dvec(x), -0.3, dvec(y))
+                r2 = kb.gemv("n", 0.7, v, dvec(x), -0.3, dvec(y))
+                assert torch.equal(r1.y_out, r2.y_out)
+                if gemv_n_xcta == "cluster" and n >= 512:
+                    assert r1.plan.startswith("gemv_nc"), r1.plan
+                assert torch.isfinite(r1.y_out).all()
+                check(r1.y_out, naive.naive_gemv("n", 0.7, a, x, -0.3, y), tag, 0.7, np.abs(a), x, -0.3, y)
+
+    def test_mgpu_partial_cluster(self, gemv_n_xcta):
+        rng = np.random.default_rng(172)
+        v, a = dev_matrix(rng, 1100, 1500, "d")
+        x, y = naive.fill(rng, 1500, "d"), naive.fill(rng, 1100, "d")
+        merged, _ = kb.gemv_mgpu("n", 1.1, kb.distribute(v, 64, 3), x, 0.4, y)
+        check(merged.y_out, naive.naive_gemv("n", 1.1, a, x, 0.4, y), "d", 1.1, np.abs(a), x, 0.4, y)
