@@ -1,0 +1,89 @@
+#!/usr/bin/env python
+"""One small call of every kernel family (and form) for compute-sanitizer:
+
+    compute-sanitizer --tool memcheck python scripts/sanitize_probe.py
+    compute-sanitizer --tool racecheck python scripts/sanitize_probe.py
+    compute-sanitizer --tool synccheck python scripts/sanitize_probe.py
+
+Ragged sizes and a misaligned submatrix start so predicated edges run.
+Exits non-zero if any result is non-finite."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+import paper_1410_1726_b200 as kb  # noqa: E402
+from paper_1410_1726_b200 import _lib  # noqa: E402
+
+lib = _lib.load()
+torch.manual_seed(0)
+bad = 0
+
+
+def mat(tag, m, n, ld, ro):
+    p = kb.precision(tag)
+    buf = torch.empty(ld * (n + 1), dtype=p.torch_dtype, device="cuda")
+    (torch.view_as_real(buf) if p.is_complex else buf).uniform_(-1, 1)
+    return kb.MatrixView(buf, ro + m, n + 1, ld, p).submatrix(ro, 1, m, n)
+
+
+def vec(tag, n):
+    p = kb.precision(tag)
+    v = torch.empty(n, dtype=p.torch_dtype, device="cuda")
+    (torch.view_as_real(v) if p.is_complex else v).uniform_(-1, 1)
+    return v
+
+
+def ok(name, t):
+    global bad
+    torch.cuda.synchronize()
+    if not torch.isfinite(t).all():
+        print("non-finite:", name)
+        bad += 1
+
+
+forms = [
+    ("default", lambda: None),
+    ("split-slots", lambda: (_lib.set_gemv_split(1), lib.kblas_set_gemv_cluster(0))),
+    ("split-cluster", lambda: (_lib.set_gemv_split(1), lib.kblas_set_gemv_cluster(1))),
+    ("stacked", lambda: (_lib.set_gemv_split(0), lib.kblas_set_gemv_cluster(-1))),
+    ("t-streamk", lambda: (_lib.set_gemv_split(-1), lib.kblas_set_gemv_tc(0, 0))),
+    ("t-colown", lambda: lib.kblas_set_gemv_tc(1, 0)),
+]
+for tag in "sdcz":
+    for m, n, ld, ro in ((333, 517, 352, 3), (1025, 300, 1056, 0)):
+        A = mat(tag, m, n, ld, ro)
+        for fname, setf in forms:
+            setf()
+            for trans in "ntc":
+                xl, yl = (n, m) if trans == "n" else (m, n)
+                r = kb.gemv(trans, 0.5, A, vec(tag, xl), 0.25, vec(tag, yl)).y_out
+                ok(f"gemv {tag} {trans} {fname}", r)
+        _lib.set_gemv_split(-1)
+        lib.kblas_set_gemv_cluster(-1)
+        lib.kblas_set_gemv_tc(-1, 0)
+    d, ld, ro = 700, 736, 5
+    A = mat(tag, d + 1, d + 1, ld, ro).submatrix(0, 0, d, d)
+    herm = tag in "cz"
+    for uplo in "lu":
+        for narrow in (0, 1 << 30):
+            _lib.set_symv_narrow(narrow)
+            r = kb.symv_hemv(uplo, 0.5, kb.HermitianView(A, uplo), vec(tag, d), 0.25, vec(tag, d),
+                             hermitian=herm).y_out
+            ok(f"symv {tag} {uplo} narrow={narrow}", r)
+        _lib.set_symv_narrow(2048)
+        prev = _lib.set_tma(1)
+        r = kb.symv_hemv(uplo, 0.5, kb.HermitianView(A, uplo), vec(tag, d), 0.25, vec(tag, d), hermitian=herm).y_out
+        ok(f"symv-tma {tag} {uplo}", r)
+        _lib.set_tma(prev)
+    dist = kb.distribute(kb.view_of(torch.rand(600, 600, device="cuda", dtype=kb.precision(tag).torch_dtype).T),
+                         64, 3)
+    r = kb.symv_hemv_mgpu("l", 1.0, dist, vec(tag, 600), 0.5, vec(tag, 600), kb.KernelConfig(64, 2),
+                          hermitian=herm)[0].y_out
+    ok(f"symv mgpu {tag}", r)
+    r = kb.gemv_mgpu("n", 1.0, dist, vec(tag, 600), 0.5, vec(tag, 600))[0].y_out
+    ok(f"gemv mgpu {tag}", r)
+print("sanitize probe done, bad =", bad)
+sys.exit(1 if bad else 0)
