@@ -1054,10 +1054,24 @@ int hostvec_entry(bool is_gemv, char op, bool herm, int m, int n, T alpha, const
   if (!bz && ylen > 0 &&
       (e = cudaMemcpyAsync(dy, hy_in, ylen * sizeof(T), cudaMemcpyHostToDevice, st)) != cudaSuccess)
     return (int)e;
-  const int rc = is_gemv ? gemv_entry<T>(o, m, n, alpha, dA, lda, dx, 1, beta, dy, 1, off_r, off_c, st)
-                         : symv_entry<T>(o, herm, n, alpha, dA, lda, dx, 1, beta, dy, 1, off_r, st);
+  // a page-locked result buffer (e.g. from torch's pinned allocator) is
+  // mapped into the device address space: with beta == 0 the kernels write
+  // y straight into it over PCIe, overlapping the transfer with the last
+  // kernel instead of a D2H copy after it
+  T *dyk = dy;
+  if (bz && ylen > 0) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, hy_out) == cudaSuccess && at.type == cudaMemoryTypeHost &&
+        at.devicePointer != nullptr)
+      dyk = static_cast<T *>(at.devicePointer);
+    else
+      cudaGetLastError();
+  }
+  const int rc = is_gemv ? gemv_entry<T>(o, m, n, alpha, dA, lda, dx, 1, beta, dyk, 1, off_r, off_c, st)
+                         : symv_entry<T>(o, herm, n, alpha, dA, lda, dx, 1, beta, dyk, 1, off_r, st);
   if (rc != 0) return rc;
-  if (ylen > 0 && (e = cudaMemcpyAsync(hy_out, dy, ylen * sizeof(T), cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+  if (dyk == dy && ylen > 0 &&
+      (e = cudaMemcpyAsync(hy_out, dy, ylen * sizeof(T), cudaMemcpyDeviceToHost, st)) != cudaSuccess)
     return (int)e;
   return code(cudaStreamSynchronize(st));
 }
