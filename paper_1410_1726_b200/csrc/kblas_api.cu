@@ -34,9 +34,7 @@ using namespace kb;
 namespace {
 
 std::atomic<unsigned long long> g_launches{0};
-// peer-memory exchange for the SYMV epilogue of the current call on this
-// thread (set by kblas_mv_mgpu_partial_p2p_async only; G == 0 otherwise)
-thread_local kb::Xchg g_xchg{};
+
 int g_symv_narrow_max = 2048;  // register SYMV: narrow tiles up to this order (kblas_set_symv_narrow)
 thread_local std::string g_last_plan;
 
@@ -587,7 +585,7 @@ cudaError_t run_symv(const Path<T> &pa, long long lda, int d, const T *x, ColMap
     kfn<<<(unsigned)P, NW * 32, smem, st>>>(p);
   }
   launch_pdl(symv_epilogue<T, LOWER, 16>, (unsigned)cdiv(d, 32), 512, st, y, p, alpha, beta, (int)beta_zero,
-             g_xchg);
+             cm.xg ? *cm.xg : kb::Xchg{});
   launched(2);
   char buf[256];
   snprintf(buf, sizeof buf, "symv %s %s %s%s lead=%d d=%d W=%d H=%d tiles=%d items=%lld P=%lld slots=%lld",
@@ -696,7 +694,7 @@ cudaError_t run_symv_tma(const T *A00, long long lda, int d, const T *x, ColMap 
     kfn<<<(unsigned)P, (NC + 2) * 32, smem, st>>>(map, tp);
   }
   launch_pdl(symv_epilogue<T, LOWER, 16>, (unsigned)cdiv(d, 32), 512, st, y, tp.sp, alpha, beta,
-             (int)beta_zero, g_xchg);
+             (int)beta_zero, cm.xg ? *cm.xg : kb::Xchg{});
   launched(2);
   char buf[256];
   snprintf(buf, sizeof buf, "symv_tma %s %s%s lead=%d d=%d W=%d H=%d S=%d tiles=%d items=%lld P=%lld slots=%lld smem=%zu",
@@ -1089,16 +1087,15 @@ int partial_p2p(bool is_gemv, char op, bool herm, int m, int n, T alpha, const T
     unsigned *cnt = nullptr;
     cudaError_t e = counters(1, st, &cnt);
     if (e != cudaSuccess) return (int)e;
-    g_xchg = kb::Xchg{G, g, slots, slot_ld, flags, consumed, cnt, seq, y_in};
+    const kb::Xchg xg{G, g, slots, slot_ld, flags, consumed, cnt, seq, y_in};
     // root: epilogue writes y_out = beta*y_in + sum; others: their slot
     T *dst = (g == 0) ? y_out : slots + (long long)g * slot_ld;
     const bool bz = g != 0 || is_zero(beta);
     Path<T> pa;
     int rc = make_path(dA, lda, &pa) != 0 ? -5 : 0;
     if (rc == 0)
-      rc = code(dispatch_symv<T>(op == 'l', herm, pa, lda, n, dx, ColMap{G, g, nb}, (int)local_cols(n, nb, G, g),
+      rc = code(dispatch_symv<T>(op == 'l', herm, pa, lda, n, dx, ColMap{G, g, nb, &xg}, (int)local_cols(n, nb, G, g),
                                  dst, alpha, g == 0 ? beta : zero<T>(), bz, st));
-    g_xchg = kb::Xchg{};
     return rc;
   }
   // general path: wait for the slot, partial into it, signal; root combines

@@ -253,8 +253,10 @@ __host__ __device__ __forceinline__ int sk_owner(long long i, long long total, l
 
 // 1D block-column-cyclic column map (multidevice.py:33-35, 72-93): local
 // column p of GPU g is global column (g + (p / nb) * G) * nb + p % nb.
+struct Xchg;  // peer-memory exchange of a one-process-per-GPU call (kblas_kernels.cuh)
 struct ColMap {
   int G, g, nb;
+  const Xchg *xg = nullptr;  // host side only: set for a p2p mgpu partial (SYMV/HEMV epilogue)
 };
 __host__ __device__ __forceinline__ long long map_col(const ColMap &cm, long long p) {
   if (cm.G == 1) return p;
