@@ -13,20 +13,20 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libkblas_b200.so")
-SOURCES = [os.path.join(CSRC, "kblas_api.cu")]
-DEPS = SOURCES + [
-    os.path.join(CSRC, "kblas_kernels.cuh"),
-    os.path.join(CSRC, "kblas_device.cuh"),
-    os.path.join(os.path.dirname(HERE), "include", "kblas_b200.h"),
-]
+# one translation unit per precision plus the precision-independent part,
+# compiled in parallel and linked into one shared library
+SOURCES = [os.path.join(CSRC, f) for f in ("kblas_runtime.cu", "kblas_s.cu", "kblas_d.cu", "kblas_c.cu",
+                                           "kblas_z.cu")]
+HEADERS = [os.path.join(CSRC, f) for f in ("kblas_impl.cuh", "kblas_entry_macros.cuh", "kblas_kernels.cuh",
+                                           "kblas_device.cuh", "kblas_symv_tma.cuh")]
+DEPS = SOURCES + HEADERS + [os.path.join(os.path.dirname(HERE), "include", "kblas_b200.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
-    "-Xcompiler", "-fPIC", "-shared",
+    "-Xcompiler", "-fPIC",
     "-Xptxas", "-v",
 ]
-
 
 def nvcc() -> str:
     for cand in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", "nvcc"):
@@ -45,15 +45,34 @@ def up_to_date() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return LIB
+    objs, procs = [], []
+    for src in SOURCES:
+        obj = os.path.join(CSRC, os.path.basename(src)[:-3] + ".o")
+        objs.append(obj)
+        cmd = [nvcc(), *NVCC_FLAGS, "-c", src, "-o", obj]
+        procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
+    reports = []
+    failed = None
+    for cmd, pr in procs:
+        out, err = pr.communicate()
+        reports.append(err)
+        if pr.returncode != 0 and failed is None:
+            failed = (cmd, pr.returncode, out + err)
+    if failed:
+        cmd, rc, log = failed
+        sys.stderr.write(log)
+        raise RuntimeError(f"nvcc failed ({rc}): {' '.join(cmd)}")
+    with open(os.path.join(CSRC, "ptxas_report.txt"), "w") as fh:
+        fh.write("".join(reports))
     tmp = LIB + ".tmp"
-    cmd = [nvcc(), *NVCC_FLAGS, *SOURCES, "-o", tmp]
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    link = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", *objs, "-o", tmp]
+    res = subprocess.run(link, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
-        raise RuntimeError(f"nvcc failed ({res.returncode}): {' '.join(cmd)}")
-    with open(os.path.join(HERE, "csrc", "ptxas_report.txt"), "w") as fh:
-        fh.write(res.stderr)
+        raise RuntimeError(f"nvcc link failed ({res.returncode}): {' '.join(link)}")
     os.replace(tmp, LIB)
+    for obj in objs:
+        os.remove(obj)
     if verbose:
         print(f"built {LIB}")
     return LIB

@@ -1,0 +1,18 @@
+// kblas_d.cu — double precision: the C entry points of include/kblas_b200.h
+// for this precision and every kernel instantiation they need.  One
+// translation unit per precision so the library builds in parallel.
+#include "kblas_entry_macros.cuh"
+
+using namespace kb;
+using namespace kbi;
+
+namespace kbi {
+KBI_ENTRY_TEMPLATES(, double)
+}  // namespace kbi
+
+extern "C" {
+
+KB_GEMV(d, double)
+KB_SYMV(dsymv, double, false)
+
+}  // extern "C"

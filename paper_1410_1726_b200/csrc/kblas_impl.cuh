@@ -1,4 +1,6 @@
-// kblas_api.cu — C ABI (include/kblas_b200.h) over the sm_100a kernels.
+// kblas_impl.cuh — host-side planning and launch code shared by the
+// translation units of the library (kblas_runtime.cu and one kblas_<p>.cu
+// per precision, compiled in parallel).
 //
 // Planning per call: pick the load path (256-bit vectors when the column
 // stride is 32-byte aligned, else one element per lane), realign the
@@ -8,6 +10,7 @@
 // caller's stream.  Workspace for cross-CTA partials is cached per
 // (device, stream) and grows only; tile tables for SYMV/HEMV are cached per
 // shape.  No allocation happens on the steady-state path.
+#pragma once
 #include <cuda_runtime.h>
 
 #include <atomic>
@@ -31,18 +34,18 @@
 
 using namespace kb;
 
-namespace {
+namespace kbi {
 
-std::atomic<unsigned long long> g_launches{0};
+inline std::atomic<unsigned long long> g_launches{0};
 
-int g_symv_narrow_max = 2048;  // register SYMV: narrow tiles up to this order (kblas_set_symv_narrow)
-thread_local std::string g_last_plan;
+inline int g_symv_narrow_max = 2048;  // register SYMV: narrow tiles up to this order (kblas_set_symv_narrow)
+inline thread_local std::string g_last_plan;
 
 // ------------------------------------------------------------- timing hook
-std::mutex g_tmu;
-bool g_timing = false;
+inline std::mutex g_tmu;
+inline bool g_timing = false;
 struct EvPair { cudaEvent_t a, b; int dev; };
-std::vector<EvPair> g_events;
+inline std::vector<EvPair> g_events;
 
 struct TimedScope {
   bool on = false;
@@ -65,11 +68,11 @@ struct TimedScope {
 };
 
 // ------------------------------------------------------ device properties
-std::mutex g_mu;
-std::map<int, int> g_sms;
-std::map<const void *, int> g_occ;
+inline std::mutex g_mu;
+inline std::map<int, int> g_sms;
+inline std::map<const void *, int> g_occ;
 
-int dev_sms() {
+inline int dev_sms() {
   int dev = 0;
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lk(g_mu);
@@ -82,7 +85,7 @@ int dev_sms() {
   return sms;
 }
 
-int occupancy(const void *fn, int threads, size_t smem = 0) {
+inline int occupancy(const void *fn, int threads, size_t smem = 0) {
   {
     std::lock_guard<std::mutex> lk(g_mu);
     auto it = g_occ.find(fn);
@@ -98,9 +101,9 @@ int occupancy(const void *fn, int threads, size_t smem = 0) {
 
 // --------------------------------------------------------------- workspace
 struct WsBuf { void *ptr = nullptr; size_t bytes = 0; };
-std::map<std::pair<int, cudaStream_t>, WsBuf> g_ws;
+inline std::map<std::pair<int, cudaStream_t>, WsBuf> g_ws;
 
-cudaError_t workspace(size_t bytes, cudaStream_t st, void **out) {
+inline cudaError_t workspace(size_t bytes, cudaStream_t st, void **out) {
   int dev = 0;
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lk(g_mu);
@@ -124,9 +127,9 @@ cudaError_t workspace(size_t bytes, cudaStream_t st, void **out) {
 // Arrival counters for the fused GEMV epilogue: one per row/column block,
 // zero between calls (the finishing CTA resets its counter), zeroed when
 // (re)allocated.  Cached per (device, stream) like the workspace.
-std::map<std::pair<int, cudaStream_t>, WsBuf> g_cnt;
+inline std::map<std::pair<int, cudaStream_t>, WsBuf> g_cnt;
 
-cudaError_t counters(size_t n, cudaStream_t st, unsigned **out) {
+inline cudaError_t counters(size_t n, cudaStream_t st, unsigned **out) {
   int dev = 0;
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lk(g_mu);
@@ -157,15 +160,15 @@ inline size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
 
 // ------------------------------------------------------------ scalar utils
 template <class T> bool is_zero(T v);
-template <> bool is_zero(float v) { return v == 0.f; }
-template <> bool is_zero(double v) { return v == 0.0; }
-template <> bool is_zero(float2 v) { return v.x == 0.f && v.y == 0.f; }
-template <> bool is_zero(double2 v) { return v.x == 0.0 && v.y == 0.0; }
+template <> inline bool is_zero(float v) { return v == 0.f; }
+template <> inline bool is_zero(double v) { return v == 0.0; }
+template <> inline bool is_zero(float2 v) { return v.x == 0.f && v.y == 0.f; }
+template <> inline bool is_zero(double2 v) { return v.x == 0.0 && v.y == 0.0; }
 template <class T> bool is_one(T v);
-template <> bool is_one(float v) { return v == 1.f; }
-template <> bool is_one(double v) { return v == 1.0; }
-template <> bool is_one(float2 v) { return v.x == 1.f && v.y == 0.f; }
-template <> bool is_one(double2 v) { return v.x == 1.0 && v.y == 0.0; }
+template <> inline bool is_one(float v) { return v == 1.f; }
+template <> inline bool is_one(double v) { return v == 1.0; }
+template <> inline bool is_one(float2 v) { return v.x == 1.f && v.y == 0.f; }
+template <> inline bool is_one(double2 v) { return v.x == 1.0 && v.y == 0.0; }
 template <class T> constexpr bool is_cplx() { return Elem<T>::cplx; }
 inline double2 widen(float v) { return make_double2(v, 0.0); }
 inline double2 widen(double v) { return make_double2(v, 0.0); }
@@ -173,10 +176,10 @@ inline double2 widen(float2 v) { return make_double2(v.x, v.y); }
 inline double2 widen(double2 v) { return v; }
 
 template <class T> const char *tname();
-template <> const char *tname<float>() { return "s"; }
-template <> const char *tname<double>() { return "d"; }
-template <> const char *tname<float2>() { return "c"; }
-template <> const char *tname<double2>() { return "z"; }
+template <> inline const char *tname<float>() { return "s"; }
+template <> inline const char *tname<double>() { return "d"; }
+template <> inline const char *tname<float2>() { return "c"; }
+template <> inline const char *tname<double2>() { return "z"; }
 
 inline int launched(int n = 1) { g_launches += n; return 0; }
 
@@ -234,9 +237,9 @@ template <class T> struct Cfg {
 // ============================================================= GEMV-N
 // Split-form GEMV-N (gemv_ns_kernel) choice: -1 auto, 0 never, 1 always
 // (kblas_set_gemv_split, for the tuner).
-int g_gemv_split = -1;
-int g_gemv_variant = 0;  // 0: tuned default shape (kblas_set_gemv_variant)
-int g_split_waves = 1;   // split-form GEMV-N: CTAs per row block sized for this many waves
+inline int g_gemv_split = -1;
+inline int g_gemv_variant = 0;  // 0: tuned default shape (kblas_set_gemv_variant)
+inline int g_split_waves = 1;   // split-form GEMV-N: CTAs per row block sized for this many waves
 constexpr long long kSplitMaxSlots = 64;
 
 template <class T, int V, int NW, int CW>
@@ -264,7 +267,7 @@ cudaError_t run_gemv_ns(const Path<T> &pa, long long lda, int m, int n, const T 
 }
 
 // cluster split form (gemv_nc_kernel): -1 auto, 0 never, 1 always
-int g_gemv_cluster = -1;
+inline int g_gemv_cluster = -1;
 
 template <class T, int V, int NW, int CW>
 cudaError_t run_gemv_nc(const Path<T> &pa, long long lda, int m, int n, const T *x, ColMap cm, T *y, T alpha,
@@ -376,8 +379,8 @@ cudaError_t run_gemv_n(const Path<T> &pa, long long lda, int m, int n, const T *
 
 // ============================================================= GEMV-T/C
 // column-owning form (gemv_tc_kernel) choice: -1 auto, 0 never, 1 always
-int g_gemv_tc = -1;
-long long g_gemv_tc_max_bytes = 80LL << 20;
+inline int g_gemv_tc = -1;
+inline long long g_gemv_tc_max_bytes = 80LL << 20;
 
 template <class T, int V, int NW, int CB, bool CONJ>
 cudaError_t run_gemv_tc(const Path<T> &pa, long long lda, int m, int n, long long nglob, const T *x, ColMap cm,
@@ -470,13 +473,13 @@ struct TileTable {
   long long total = 0;
   long long maxslots = 0;
 };
-std::map<std::vector<long long>, TileTable> g_tiles;
+inline std::map<std::vector<long long>, TileTable> g_tiles;
 
 // Tiles for the local panel of GPU g under the block-cyclic layout (G=1,
 // nb=d for a single GPU): every owned block column is cut into W-wide tiles.
 // exact: chunks start at each tile's first stored row (TMA path); else on
 // the physical H-row grid (vector-load path, 32-byte granules).
-cudaError_t tile_table(int d, int lead, bool lower, int W, int H, ColMap cm, int ncols_local, long long P,
+inline cudaError_t tile_table(int d, int lead, bool lower, int W, int H, ColMap cm, int ncols_local, long long P,
                        TileTable *out, bool exact = false) {
   int dev = 0;
   cudaGetDevice(&dev);
@@ -596,7 +599,7 @@ cudaError_t run_symv(const Path<T> &pa, long long lda, int d, const T *x, ColMap
 }
 
 // ---------------------------------------------------------- SYMV via TMA
-PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+inline PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
   std::call_once(once, [] {
@@ -612,16 +615,16 @@ PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 // SYMV/HEMV kernel choice: -1 auto (per-precision default from the
 // empirical tuning in profiles/r1_tune_symv_*.jsonl), 0 register-load
 // kernel, 1 TMA kernel.  KBLAS_NO_TMA=1 forces 0 at load.
-int g_use_tma = -2;
-int g_symv_variant = -1;  // -1: per-precision default variant
-int tma_mode() {
+inline int g_use_tma = -2;
+inline int g_symv_variant = -1;  // -1: per-precision default variant
+inline int tma_mode() {
   if (g_use_tma == -2) {
     const char *e = getenv("KBLAS_NO_TMA");
     g_use_tma = (e && e[0] == '1') ? 0 : -1;
   }
   return g_use_tma;
 }
-bool use_tma() { return tma_mode() != 0; }
+inline bool use_tma() { return tma_mode() != 0; }
 // tuned defaults (profiles/r1_tune_symv_v3.jsonl): the software-pipelined
 // register kernel wins for every precision and size except SSYMV at
 // N <= 8192, where the TMA kernel (variant 1: 16 consumers x 8 columns,
@@ -867,7 +870,7 @@ int symv_entry(char uplo, bool herm, int n, T alpha, const T *dA, int lda, const
 }
 
 // ------------------------------------------------------------------ mgpu
-long long local_cols(long long n, long long nb, long long G, long long g) {
+inline long long local_cols(long long n, long long nb, long long G, long long g) {
   long long total = 0;
   const long long nblk = cdiv(n, nb);
   for (long long j = g; j < nblk; j += G) total += std::min(n, (j + 1) * nb) - j * nb;
@@ -984,7 +987,7 @@ int mgpu_entry(bool is_gemv, char op, bool herm, int m, int n, T alpha, T *const
 }
 
 // per-GPU panels of the 1D block-column-cyclic layout
-int malloc_mgpu(int m, int n, size_t esize, void **dA, int *ldda, int ngpus, int nb, const int *device_ids) {
+inline int malloc_mgpu(int m, int n, size_t esize, void **dA, int *ldda, int ngpus, int nb, const int *device_ids) {
   if (m < 0 || n < 0 || esize == 0 || dA == nullptr || ngpus < 1 || nb < 1) return -1;
   DevGuard guard;
   const long long ld = cdiv(std::max(m, 1), 32) * 32;
@@ -1009,9 +1012,9 @@ int malloc_mgpu(int m, int n, size_t esize, void **dA, int *ldda, int ngpus, int
 // pair, the kernels, and the D2H of the result, then waits for the stream.
 // This is the path the Python API takes for numpy vectors (one crossing of
 // the FFI per call instead of a handful of tensor operations).
-std::map<std::pair<int, cudaStream_t>, WsBuf> g_vecs;
+inline std::map<std::pair<int, cudaStream_t>, WsBuf> g_vecs;
 
-cudaError_t vec_staging(size_t bytes, cudaStream_t st, void **out) {
+inline cudaError_t vec_staging(size_t bytes, cudaStream_t st, void **out) {
   int dev = 0;
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lk(g_mu);
@@ -1119,388 +1122,20 @@ int partial_p2p(bool is_gemv, char op, bool herm, int m, int n, T alpha, const T
   return code(cudaGetLastError());
 }
 
-}  // namespace
 
-// ====================================================================
-// extern "C" surface
-// ====================================================================
-extern "C" {
+// Entry templates instantiated once per precision in kblas_<p>.cu and
+// referenced from kblas_runtime.cu's precision-switching C functions.
+#define KBI_ENTRY_TEMPLATES(EXT, T)                                                                          \
+  EXT template int partial_entry<T>(bool, char, bool, int, int, T, const T *, int, const T *, T *, int, int, int, \
+                                    cudaStream_t);                                                            \
+  EXT template int hostvec_entry<T>(bool, char, bool, int, int, T, const T *, int, int, int, const T *, T,       \
+                                    const T *, T *, cudaStream_t);                                            \
+  EXT template int partial_p2p<T>(bool, char, bool, int, int, T, const T *, int, const T *, int, int, int, T *,   \
+                                  long long, unsigned long long *, unsigned long long *, unsigned *,           \
+                                  unsigned long long, T, const T *, T *, cudaStream_t);
+KBI_ENTRY_TEMPLATES(extern, float)
+KBI_ENTRY_TEMPLATES(extern, double)
+KBI_ENTRY_TEMPLATES(extern, float2)
+KBI_ENTRY_TEMPLATES(extern, double2)
 
-#define KB_GEMV(P, T)                                                                                        \
-  int kblas_##P##gemv(char trans, int m, int n, T alpha, const T *dA, int lda, const T *dx, int incx, T beta,   \
-                      T *dy, int incy) {                                                                       \
-    return gemv_entry<T>(trans, m, n, alpha, dA, lda, dx, incx, beta, dy, incy, 0, 0, 0);                      \
-  }                                                                                                            \
-  int kblas_##P##gemv_async(char trans, int m, int n, T alpha, const T *dA, int lda, const T *dx, int incx,    \
-                            T beta, T *dy, int incy, cudaStream_t s) {                                         \
-    return gemv_entry<T>(trans, m, n, alpha, dA, lda, dx, incx, beta, dy, incy, 0, 0, s);                      \
-  }                                                                                                            \
-  int kblas_##P##gemv_offset(char trans, int m, int n, T alpha, const T *dA, int lda, const T *dx, int incx,   \
-                             T beta, T *dy, int incy, int offset_r, int offset_c) {                            \
-    return gemv_entry<T>(trans, m, n, alpha, dA, lda, dx, incx, beta, dy, incy, offset_r, offset_c, 0);        \
-  }                                                                                                            \
-  int kblas_##P##gemv_offset_async(char trans, int m, int n, T alpha, const T *dA, int lda, const T *dx,       \
-                                   int incx, T beta, T *dy, int incy, int offset_r, int offset_c,             \
-                                   cudaStream_t s) {                                                           \
-    return gemv_entry<T>(trans, m, n, alpha, dA, lda, dx, incx, beta, dy, incy, offset_r, offset_c, s);        \
-  }                                                                                                            \
-  int kblas_##P##gemv_mgpu(char trans, int m, int n, T alpha, T *const *dA, int lda, T *const *dx, int incx,   \
-                           T beta, T *const *dy, int incy, int ngpus, int nb, const int *device_ids) {         \
-    char t = (char)(trans | 0x20);                                                                             \
-    if (t != 'n' && t != 't' && t != 'c') return -1;                                                           \
-    if (m < 0) return -2;                                                                                      \
-    if (n < 0) return -3;                                                                                      \
-    if (lda < std::max(1, m)) return -6;                                                                       \
-    if (incx != 1) return -8;                                                                                  \
-    if (incy != 1) return -11;                                                                                 \
-    return mgpu_entry<T>(true, t, false, m, n, alpha, dA, lda, dx, beta, dy, ngpus, nb, device_ids);          \
-  }                                                                                                            \
-  int kblas_##P##gemv_mgpu_async(char trans, int m, int n, T alpha, T *const *dA, int lda, T *const *dx,      \
-                                 int incx, T beta, T *const *dy, int incy, int ngpus, int nb,                 \
-                                 const int *device_ids, cudaStream_t const *streams) {                        \
-    char t = (char)(trans | 0x20);                                                                             \
-    if (t != 'n' && t != 't' && t != 'c') return -1;                                                           \
-    if (m < 0) return -2;                                                                                      \
-    if (n < 0) return -3;                                                                                      \
-    if (lda < std::max(1, m)) return -6;                                                                       \
-    if (incx != 1) return -8;                                                                                  \
-    if (incy != 1) return -11;                                                                                 \
-    if (streams == nullptr) return -16;                                                                        \
-    return mgpu_entry<T>(true, t, false, m, n, alpha, dA, lda, dx, beta, dy, ngpus, nb, device_ids, streams); \
-  }
-
-#define KB_SYMV(NAME, T, HERM)                                                                                \
-  int kblas_##NAME(char uplo, int n, T alpha, const T *dA, int lda, const T *dx, int incx, T beta, T *dy,      \
-                   int incy) {                                                                                 \
-    return symv_entry<T>(uplo, HERM, n, alpha, dA, lda, dx, incx, beta, dy, incy, 0, 0);                       \
-  }                                                                                                            \
-  int kblas_##NAME##_async(char uplo, int n, T alpha, const T *dA, int lda, const T *dx, int incx, T beta,     \
-                           T *dy, int incy, cudaStream_t s) {                                                  \
-    return symv_entry<T>(uplo, HERM, n, alpha, dA, lda, dx, incx, beta, dy, incy, 0, s);                       \
-  }                                                                                                            \
-  int kblas_##NAME##_offset(char uplo, int n, T alpha, const T *dA, int lda, const T *dx, int incx, T beta,    \
-                            T *dy, int incy, int offset) {                                                     \
-    return symv_entry<T>(uplo, HERM, n, alpha, dA, lda, dx, incx, beta, dy, incy, offset, 0);                  \
-  }                                                                                                            \
-  int kblas_##NAME##_offset_async(char uplo, int n, T alpha, const T *dA, int lda, const T *dx, int incx,      \
-                                  T beta, T *dy, int incy, int offset, cudaStream_t s) {                       \
-    return symv_entry<T>(uplo, HERM, n, alpha, dA, lda, dx, incx, beta, dy, incy, offset, s);                  \
-  }                                                                                                            \
-  int kblas_##NAME##_mgpu(char uplo, int n, T alpha, T *const *dA, int lda, T *const *dx, int incx, T beta,    \
-                          T *const *dy, int incy, int ngpus, int nb, const int *device_ids) {                  \
-    const char u = (char)(uplo | 0x20);                                                                        \
-    if (u != 'l' && u != 'u') return -1;                                                                       \
-    if (n < 0) return -2;                                                                                      \
-    if (lda < std::max(1, n)) return -5;                                                                       \
-    if (incx != 1) return -7;                                                                                  \
-    if (incy != 1) return -10;                                                                                 \
-    return mgpu_entry<T>(false, u, HERM, n, n, alpha, dA, lda, dx, beta, dy, ngpus, nb, device_ids);          \
-  }                                                                                                            \
-  int kblas_##NAME##_mgpu_async(char uplo, int n, T alpha, T *const *dA, int lda, T *const *dx, int incx,      \
-                                T beta, T *const *dy, int incy, int ngpus, int nb, const int *device_ids,     \
-                                cudaStream_t const *streams) {                                                 \
-    const char u = (char)(uplo | 0x20);                                                                        \
-    if (u != 'l' && u != 'u') return -1;                                                                       \
-    if (n < 0) return -2;                                                                                      \
-    if (lda < std::max(1, n)) return -5;                                                                       \
-    if (incx != 1) return -7;                                                                                  \
-    if (incy != 1) return -10;                                                                                 \
-    if (streams == nullptr) return -14;                                                                        \
-    return mgpu_entry<T>(false, u, HERM, n, n, alpha, dA, lda, dx, beta, dy, ngpus, nb, device_ids, streams); \
-  }
-
-KB_GEMV(s, float)
-KB_GEMV(d, double)
-KB_GEMV(c, cuFloatComplex)
-KB_GEMV(z, cuDoubleComplex)
-KB_SYMV(ssymv, float, false)
-KB_SYMV(dsymv, double, false)
-KB_SYMV(chemv, cuFloatComplex, true)
-KB_SYMV(zhemv, cuDoubleComplex, true)
-KB_SYMV(csymv, cuFloatComplex, false)
-KB_SYMV(zsymv, cuDoubleComplex, false)
-
-int kblas_mv_mgpu_partial_async(char prec, char kind, char op, int m, int n, const void *alpha,
-                                const void *dA_local, int lda, const void *dx, void *dy_partial, int ngpus,
-                                int gpu, int nb, int hermitian, cudaStream_t stream) {
-  const bool is_gemv = (kind | 0x20) == 'g';
-  const char o = (char)(op | 0x20);
-  if (ngpus < 1 || gpu < 0 || gpu >= ngpus || nb < 1 || m < 0 || n < 0) return -1;
-  switch (prec | 0x20) {
-    case 's': return partial_entry<float>(is_gemv, o, false, m, n, *(const float *)alpha, (const float *)dA_local, lda, (const float *)dx, (float *)dy_partial, ngpus, gpu, nb, stream);
-    case 'd': return partial_entry<double>(is_gemv, o, false, m, n, *(const double *)alpha, (const double *)dA_local, lda, (const double *)dx, (double *)dy_partial, ngpus, gpu, nb, stream);
-    case 'c': return partial_entry<float2>(is_gemv, o, hermitian != 0, m, n, *(const float2 *)alpha, (const float2 *)dA_local, lda, (const float2 *)dx, (float2 *)dy_partial, ngpus, gpu, nb, stream);
-    case 'z': return partial_entry<double2>(is_gemv, o, hermitian != 0, m, n, *(const double2 *)alpha, (const double2 *)dA_local, lda, (const double2 *)dx, (double2 *)dy_partial, ngpus, gpu, nb, stream);
-  }
-  return -1;
-}
-
-int kblas_mgpu_local_cols(int n, int nb, int ngpus, int gpu) {
-  if (n < 0 || nb < 1 || ngpus < 1 || gpu < 0 || gpu >= ngpus) return -1;
-  return (int)local_cols(n, nb, ngpus, gpu);
-}
-
-int kblas_mgpu_local_ld(int m) { return (int)(cdiv(std::max(m, 1), 32) * 32); }
-
-int kblas_malloc_mgpu_1d(int m, int n, size_t esize, void **dA, int *ldda, int ngpus, int nb,
-                         const int *device_ids) {
-  return malloc_mgpu(m, n, esize, dA, ldda, ngpus, nb, device_ids);
-}
-
-int kblas_free_mgpu(void **dA, int ngpus, const int *device_ids) {
-  if (dA == nullptr || ngpus < 1) return -1;
-  DevGuard guard;
-  for (int g = 0; g < ngpus; ++g) {
-    if (!dA[g]) continue;
-    cudaSetDevice(device_ids ? device_ids[g] : g);
-    cudaError_t e = cudaFree(dA[g]);
-    if (e != cudaSuccess) return (int)e;
-    dA[g] = nullptr;
-  }
-  return 0;
-}
-
-// the SYMV/HEMV tile width: a distribution block of this width (or a
-// multiple) keeps every tile inside one block, so no tile is cut short
-int kblas_mgpu_block_size(char prec, char kind) {
-  const char p = (char)(prec | 0x20), k = (char)(kind | 0x20);
-  if (p != 's' && p != 'd' && p != 'c' && p != 'z') return -1;
-  if (k != 'g' && k != 's') return -2;
-  return 128;
-}
-
-static int copy_mgpu(bool to_dev, int m, int n, size_t esize, const void *hA_c, void *hA, int ldha,
-                     void *const *dA, int ldda, int ngpus, int nb, const int *device_ids) {
-  if (m < 0 || n < 0 || ngpus < 1 || nb < 1 || ldha < std::max(1, m) || ldda < std::max(1, m)) return -1;
-  DevGuard guard;
-  const long long nblk = cdiv(n, nb);
-  for (long long j = 0; j < nblk; ++j) {
-    const int g = (int)(j % ngpus);
-    const long long b = j / ngpus;
-    const long long c0 = j * nb, w = std::min<long long>(n, c0 + nb) - c0;
-    cudaSetDevice(device_ids ? device_ids[g] : g);
-    char *dp = static_cast<char *>(dA[g]) + (size_t)(b * nb) * ldda * esize;
-    cudaError_t e;
-    if (to_dev)
-      e = cudaMemcpy2D(dp, (size_t)ldda * esize, static_cast<const char *>(hA_c) + (size_t)c0 * ldha * esize,
-                       (size_t)ldha * esize, (size_t)m * esize, (size_t)w, cudaMemcpyHostToDevice);
-    else
-      e = cudaMemcpy2D(static_cast<char *>(hA) + (size_t)c0 * ldha * esize, (size_t)ldha * esize, dp,
-                       (size_t)ldda * esize, (size_t)m * esize, (size_t)w, cudaMemcpyDeviceToHost);
-    if (e != cudaSuccess) return (int)e;
-  }
-  return 0;
-}
-
-int kblas_setmatrix_mgpu_1d(int m, int n, size_t esize, const void *hA, int ldha, void *const *dA, int ldda,
-                            int ngpus, int nb, const int *device_ids) {
-  return copy_mgpu(true, m, n, esize, hA, nullptr, ldha, dA, ldda, ngpus, nb, device_ids);
-}
-
-int kblas_getmatrix_mgpu_1d(int m, int n, size_t esize, void *const *dA, int ldda, void *hA, int ldha, int ngpus,
-                            int nb, const int *device_ids) {
-  return copy_mgpu(false, m, n, esize, nullptr, hA, ldha, dA, ldda, ngpus, nb, device_ids);
-}
-
-int kblas_setmatrix_async(int rows, int cols, size_t esize, const void *hA, int ldha, void *dA, int ldda,
-                          cudaStream_t stream) {
-  if (rows < 0 || cols < 0 || ldha < std::max(1, rows) || ldda < std::max(1, rows)) return -1;
-  if (rows == 0 || cols == 0) return 0;
-  return code(cudaMemcpy2DAsync(dA, (size_t)ldda * esize, hA, (size_t)ldha * esize, (size_t)rows * esize,
-                                (size_t)cols, cudaMemcpyHostToDevice, stream));
-}
-
-int kblas_getmatrix_async(int rows, int cols, size_t esize, const void *dA, int ldda, void *hA, int ldha,
-                          cudaStream_t stream) {
-  if (rows < 0 || cols < 0 || ldha < std::max(1, rows) || ldda < std::max(1, rows)) return -1;
-  if (rows == 0 || cols == 0) return 0;
-  return code(cudaMemcpy2DAsync(hA, (size_t)ldha * esize, dA, (size_t)ldda * esize, (size_t)rows * esize,
-                                (size_t)cols, cudaMemcpyDeviceToHost, stream));
-}
-
-int kblas_mv_hostvec(char prec, char kind, char op, int hermitian, int m, int n, const void *alpha,
-                     const void *dA, int lda, int offset_r, int offset_c, const void *hx, const void *beta,
-                     const void *hy_in, void *hy_out, cudaStream_t stream) {
-  const bool g = (kind | 0x20) == 'g';
-  if (!g && (kind | 0x20) != 's') return -2;
-  if (!g && offset_r != offset_c) return -11;
-  switch (prec | 0x20) {
-    case 's': return hostvec_entry<float>(g, op, false, m, n, *(const float *)alpha, (const float *)dA, lda, offset_r, offset_c, (const float *)hx, *(const float *)beta, (const float *)hy_in, (float *)hy_out, stream);
-    case 'd': return hostvec_entry<double>(g, op, false, m, n, *(const double *)alpha, (const double *)dA, lda, offset_r, offset_c, (const double *)hx, *(const double *)beta, (const double *)hy_in, (double *)hy_out, stream);
-    case 'c': return hostvec_entry<float2>(g, op, hermitian != 0, m, n, *(const float2 *)alpha, (const float2 *)dA, lda, offset_r, offset_c, (const float2 *)hx, *(const float2 *)beta, (const float2 *)hy_in, (float2 *)hy_out, stream);
-    case 'z': return hostvec_entry<double2>(g, op, hermitian != 0, m, n, *(const double2 *)alpha, (const double2 *)dA, lda, offset_r, offset_c, (const double2 *)hx, *(const double2 *)beta, (const double2 *)hy_in, (double2 *)hy_out, stream);
-  }
-  return -1;
-}
-
-// ------------------------------------------------ peer-memory exchange
-int kblas_ipc_get_handle(const void *dptr, void *handle_out) {
-  if (dptr == nullptr || handle_out == nullptr) return -1;
-  cudaIpcMemHandle_t h;
-  cudaError_t e = cudaIpcGetMemHandle(&h, const_cast<void *>(dptr));
-  if (e != cudaSuccess) return (int)e;
-  memcpy(handle_out, &h, sizeof h);
-  return 0;
-}
-
-int kblas_ipc_open_handle(const void *handle, void **dptr_out) {
-  if (handle == nullptr || dptr_out == nullptr) return -1;
-  cudaIpcMemHandle_t h;
-  memcpy(&h, handle, sizeof h);
-  return code(cudaIpcOpenMemHandle(dptr_out, h, cudaIpcMemLazyEnablePeerAccess));
-}
-
-int kblas_ipc_close(void *dptr) { return code(cudaIpcCloseMemHandle(dptr)); }
-
-int kblas_p2p_signal_async(unsigned long long *flag, unsigned long long seq, cudaStream_t stream) {
-  if (flag == nullptr) return -1;
-  p2p_signal_kernel<<<1, 32, 0, stream>>>(flag, seq);
-  launched();
-  return code(cudaGetLastError());
-}
-
-int kblas_p2p_wait_async(const unsigned long long *flag, unsigned long long seq, cudaStream_t stream) {
-  if (flag == nullptr) return -1;
-  p2p_wait_kernel<<<1, 32, 0, stream>>>(flag, seq);
-  launched();
-  return code(cudaGetLastError());
-}
-
-int kblas_mv_mgpu_partial_p2p_async(char prec, char kind, char op, int m, int n, const void *alpha,
-                                    const void *dA_local, int lda, const void *dx, int ngpus, int gpu, int nb,
-                                    int hermitian, void *slots, long long slot_ld, unsigned long long *flags,
-                                    unsigned long long *consumed, unsigned *counter, unsigned long long seq,
-                                    const void *beta, const void *y_in, void *y_out, cudaStream_t stream) {
-  const bool is_gemv = (kind | 0x20) == 'g';
-  const char o = (char)(op | 0x20);
-  if (ngpus < 1 || ngpus > kMaxGpus || gpu < 0 || gpu >= ngpus || nb < 1 || m < 0 || n < 0) return -1;
-  if (slots == nullptr || flags == nullptr || consumed == nullptr || seq < 1) return -1;
-  if (gpu == 0 && (y_out == nullptr || counter == nullptr)) return -1;
-  switch (prec | 0x20) {
-#define KB_PP(CH, T, H)                                                                                         \
-  case CH:                                                                                                      \
-    return partial_p2p<T>(is_gemv, o, H, m, n, *(const T *)alpha, (const T *)dA_local, lda, (const T *)dx,        \
-                          ngpus, gpu, nb, (T *)slots, slot_ld, flags, consumed, counter, seq, *(const T *)beta,   \
-                          (const T *)y_in, (T *)y_out, stream);
-    KB_PP('s', float, false)
-    KB_PP('d', double, false)
-    KB_PP('c', float2, hermitian != 0)
-    KB_PP('z', double2, hermitian != 0)
-#undef KB_PP
-  }
-  return -1;
-}
-
-int kblas_p2p_combine_async(char prec, int nranks, const void *slots, long long slot_ld,
-                            const unsigned long long *flags, unsigned long long seq, const void *beta, void *y,
-                            long long n, unsigned long long *consumed, unsigned *counter, cudaStream_t stream) {
-  if (nranks < 1 || slots == nullptr || flags == nullptr || y == nullptr || consumed == nullptr ||
-      counter == nullptr || n < 0 || slot_ld < n)
-    return -1;
-  const unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>(cdiv(n, 256), 4LL * dev_sms()));
-  switch (prec | 0x20) {
-#define KB_P2P(CH, T)                                                                                         \
-  case CH: {                                                                                                  \
-    const T b = *static_cast<const T *>(beta);                                                                \
-    p2p_combine_kernel<T><<<grid, 256, 0, stream>>>(static_cast<const T *>(slots), slot_ld, nranks, flags, seq, \
-                                                    static_cast<T *>(y), n, b, is_zero(b) ? 1 : 0, consumed,      \
-                                                    counter);                                                 \
-    break;                                                                                                    \
-  }
-    KB_P2P('s', float)
-    KB_P2P('d', double)
-    KB_P2P('c', float2)
-    KB_P2P('z', double2)
-#undef KB_P2P
-    default: return -1;
-  }
-  launched();
-  return code(cudaGetLastError());
-}
-
-unsigned long long kblas_launch_count(void) { return g_launches.load(); }
-
-int kblas_timing_enable(int enable) {
-  std::lock_guard<std::mutex> lk(g_tmu);
-  g_timing = enable != 0;
-  return 0;
-}
-
-int kblas_timing_read(double *total_ms, int *launches) {
-  std::vector<EvPair> evs;
-  {
-    std::lock_guard<std::mutex> lk(g_tmu);
-    evs.swap(g_events);
-  }
-  DevGuard guard;
-  double tot = 0.0;
-  int rc = 0;
-  for (auto &ev : evs) {
-    cudaSetDevice(ev.dev);
-    float ms = 0.f;
-    cudaError_t e = cudaEventSynchronize(ev.b);
-    if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, ev.a, ev.b);
-    if (e != cudaSuccess) rc = (int)e;
-    tot += ms;
-    cudaEventDestroy(ev.a);
-    cudaEventDestroy(ev.b);
-  }
-  if (total_ms) *total_ms = tot;
-  if (launches) *launches = (int)evs.size();
-  return rc;
-}
-
-const char *kblas_last_plan(void) { return g_last_plan.c_str(); }
-
-int kblas_set_symv_variant(int v) {
-  const int prev = g_symv_variant;
-  g_symv_variant = v;
-  return prev;
-}
-
-int kblas_set_symv_narrow(int max_order) {
-  const int prev = g_symv_narrow_max;
-  g_symv_narrow_max = max_order;
-  return prev;
-}
-
-int kblas_set_gemv_variant(int v) {
-  const int prev = g_gemv_variant;
-  g_gemv_variant = v;
-  return prev;
-}
-
-int kblas_set_gemv_cluster(int mode) {
-  const int prev = g_gemv_cluster;
-  g_gemv_cluster = mode < 0 ? -1 : (mode ? 1 : 0);
-  return prev;
-}
-
-int kblas_set_gemv_split_waves(int waves) {
-  const int prev = g_split_waves;
-  if (waves >= 1) g_split_waves = waves;
-  return prev;
-}
-
-int kblas_set_gemv_tc(int mode, long long max_bytes) {
-  const int prev = g_gemv_tc;
-  g_gemv_tc = mode < 0 ? -1 : (mode ? 1 : 0);
-  if (max_bytes > 0) g_gemv_tc_max_bytes = max_bytes;
-  return prev;
-}
-
-int kblas_set_gemv_split(int mode) {
-  const int prev = g_gemv_split;
-  g_gemv_split = mode < 0 ? -1 : (mode ? 1 : 0);
-  return prev;
-}
-
-int kblas_set_tma(int mode) {
-  const int prev = tma_mode();
-  g_use_tma = mode < 0 ? -1 : (mode ? 1 : 0);
-  return prev;
-}
-
-const char *kblas_version(void) { return "kblas-b200 0.1.0 (sm_100a)"; }
-
-}  // extern "C"
+}  // namespace kbi

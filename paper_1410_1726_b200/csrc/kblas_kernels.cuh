@@ -1086,7 +1086,7 @@ __global__ void mgpu_combine_kernel(T *y, PartList<T> parts, int G, long long n,
 // ---------------------------------------------------------------------------
 // rank side: its partial (written by the preceding kernels on this stream)
 // becomes visible system-wide, then flags[rank] = seq
-__global__ void p2p_signal_kernel(unsigned long long *flag, unsigned long long seq) {
+static __global__ void p2p_signal_kernel(unsigned long long *flag, unsigned long long seq) {
   if (threadIdx.x == 0) {
     __threadfence_system();
     st_release_sys(flag, seq);
@@ -1094,7 +1094,7 @@ __global__ void p2p_signal_kernel(unsigned long long *flag, unsigned long long s
 }
 
 // wait until *flag >= seq (e.g. the root has consumed the previous call)
-__global__ void p2p_wait_kernel(const unsigned long long *flag, unsigned long long seq) {
+static __global__ void p2p_wait_kernel(const unsigned long long *flag, unsigned long long seq) {
   if (threadIdx.x == 0) spin_until(flag, seq);
   __syncthreads();
 }

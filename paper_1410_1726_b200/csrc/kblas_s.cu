@@ -1,0 +1,18 @@
+// kblas_s.cu — single precision: the C entry points of include/kblas_b200.h
+// for this precision and every kernel instantiation they need.  One
+// translation unit per precision so the library builds in parallel.
+#include "kblas_entry_macros.cuh"
+
+using namespace kb;
+using namespace kbi;
+
+namespace kbi {
+KBI_ENTRY_TEMPLATES(, float)
+}  // namespace kbi
+
+extern "C" {
+
+KB_GEMV(s, float)
+KB_SYMV(ssymv, float, false)
+
+}  // extern "C"

@@ -3,7 +3,7 @@
 `KernelConfig` keeps the reference's validation (partition.py:25-36) so
 existing call sites construct it unchanged.  On B200 the triple is a
 tuning hint only: the kernels pick their own tile shape for sm_100a
-(csrc/kblas_api.cu, `Cfg`), and the cooperating-TB split-K of the paper
+(csrc/kblas_impl.cuh, `Cfg`), and the cooperating-TB split-K of the paper
 (Y-bar) is replaced by stream-K over equal work items.  `block_size` still
 matters for the mgpu SYMV/HEMV distribution check (multidevice.py:205-208).
 """
