@@ -347,7 +347,7 @@ cudaError_t run_gemv_n(const Path<T> &pa, long long lda, int m, int n, const T *
       // (cluster sizes 2..16; 16 is the opt-in non-portable maximum)
       int Sc = 1;
       while (Sc < 16 && Sc < S) Sc *= 2;
-      const bool cl_ok = S > 1 && n / Sc >= NWs * CWs && 2 * nrb_s * Sc >= dev_sms();
+      const bool cl_ok = S > 1 && n / Sc >= NWs * CWs && 4 * nrb_s * Sc >= dev_sms();
       if (g_gemv_cluster == 1 || (g_gemv_cluster == -1 && cl_ok && small))
         return run_gemv_nc<T, V, NWs, CWs>(pa, lda, m, n, x, cm, y, alpha, beta, beta_zero, st, Sc, nrb_s);
       return run_gemv_ns<T, V, NWs, CWs>(pa, lda, m, n, x, cm, y, alpha, beta, beta_zero, st, S, nrb_s);
