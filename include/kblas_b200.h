@@ -445,6 +445,10 @@ int kblas_set_gemv_cluster(int mode);
 /* tiles (more work items for small operands).  Returns the previous   */
 /* threshold (default 2048).                                           */
 int kblas_set_symv_narrow(int max_order);
+/* Register SYMV/HEMV kernel, s/d/c: orders above the narrow threshold  */
+/* and up to max_order use 8-warp CTAs at 2 per SM.  Returns the        */
+/* previous threshold (default 12288).                                  */
+int kblas_set_symv_mid(int max_order);
 /* Description of the last plan chosen for a call on this thread      */
 /* (kernel family, grid, items, workspace bytes) as a NUL-terminated   */
 /* string; for reports and tests.                                      */

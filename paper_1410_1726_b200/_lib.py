@@ -171,6 +171,8 @@ def load():
         lib.kblas_set_gemv_variant.restype = c_int
         lib.kblas_set_gemv_split.argtypes = [c_int]
         lib.kblas_set_gemv_split.restype = c_int
+        lib.kblas_set_symv_mid.argtypes = [c_int]
+        lib.kblas_set_symv_mid.restype = c_int
         lib.kblas_set_symv_narrow.argtypes = [c_int]
         lib.kblas_set_symv_narrow.restype = c_int
         lib.kblas_last_plan.restype = ctypes.c_char_p

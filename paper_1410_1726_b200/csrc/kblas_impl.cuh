@@ -38,6 +38,7 @@ namespace kbi {
 
 inline std::atomic<unsigned long long> g_launches{0};
 
+inline int g_symv_mid_max = 12288;  // register SYMV: 2-CTA/SM variant up to this order (s, d, c)
 inline int g_symv_narrow_max = 2048;  // register SYMV: narrow tiles up to this order (kblas_set_symv_narrow)
 inline thread_local std::string g_last_plan;
 
@@ -785,6 +786,10 @@ cudaError_t dispatch_symv_h(bool lower, const Path<T> &pa, long long lda, int d,
   // there are enough items to occupy every SM
   int v = g_symv_variant;
   if (v < 100 && d <= g_symv_narrow_max) v = 103;
+  // mid orders (s, d, c): 8 warps x 8 columns at 2 CTAs/SM ramps up faster
+  // than one 16-warp CTA per SM (+2-10 % at d = 4096-12288,
+  // profiles/r1v_tune_symv_mid.jsonl); z keeps the wide default
+  else if (v < 100 && sizeof(T) <= 8 && d <= g_symv_mid_max) v = 105;
   // (variants 101/102/104/108 and the column-rolling / split-barrier
   // kernels were measured and dropped: profiles/r1h_tune_symv_*.jsonl)
   switch (v) {

@@ -251,6 +251,12 @@ int kblas_set_symv_variant(int v) {
   return prev;
 }
 
+int kblas_set_symv_mid(int max_order) {
+  const int prev = g_symv_mid_max;
+  g_symv_mid_max = max_order;
+  return prev;
+}
+
 int kblas_set_symv_narrow(int max_order) {
   const int prev = g_symv_narrow_max;
   g_symv_narrow_max = max_order;

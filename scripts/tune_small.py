@@ -65,9 +65,11 @@ def forms(family, op, tag):
                 "streamk": lambda: _lib.load().kblas_set_gemv_tc(0, 0)}
     if family == "symv":
         big = 1 << 30
+        lib = _lib.load()
         f = {"auto": lambda: reset(),
              "narrow": lambda: (_lib.set_symv_narrow(big), _lib.set_tma(0)),
-             "wide": lambda: (_lib.set_symv_narrow(0), _lib.set_tma(0))}
+             "mid": lambda: (_lib.set_symv_narrow(0), lib.kblas_set_symv_mid(big), _lib.set_tma(0)),
+             "wide": lambda: (_lib.set_symv_narrow(0), lib.kblas_set_symv_mid(0), _lib.set_tma(0))}
         if tag == "s":
             f["tma"] = lambda: (_lib.set_symv_narrow(0), _lib.set_tma(1))
         return f
@@ -85,7 +87,9 @@ def reset():
     _lib.set_tma(-1)
     if not DEFAULTS:  # the library's built-in thresholds
         DEFAULTS["narrow"] = _lib.set_symv_narrow(0)
+        DEFAULTS["mid"] = _lib.load().kblas_set_symv_mid(0)
     _lib.set_symv_narrow(DEFAULTS["narrow"])
+    _lib.load().kblas_set_symv_mid(DEFAULTS["mid"])
 
 
 def main():

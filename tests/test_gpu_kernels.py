@@ -552,13 +552,17 @@ class TestGemvNForms:
             _lib.set_gemv_split(prev)
 
 
-@pytest.fixture(params=["narrow", "wide"])
+@pytest.fixture(params=["narrow", "mid", "wide"])
 def symv_tiles(request):
-    """Register SYMV/HEMV kernel with narrow (small-operand) and wide tiles."""
+    """Register SYMV/HEMV kernel shapes: narrow tiles (small operands),
+    8-warp CTAs at 2 per SM (mid orders) and the wide 16-warp default."""
+    lib = _lib.load()
     prev_n = _lib.set_symv_narrow((1 << 30) if request.param == "narrow" else 0)
+    prev_m = lib.kblas_set_symv_mid((1 << 30) if request.param == "mid" else 0)
     prev_t = _lib.set_tma(0)
     yield request.param
     _lib.set_symv_narrow(prev_n)
+    lib.kblas_set_symv_mid(prev_m)
     _lib.set_tma(prev_t)
 
 
