@@ -400,6 +400,11 @@ int kblas_mv_hostvec(char prec, char kind, char op, int hermitian, int m, int n,
                      const void *alpha, const void *dA, int lda, int offset_r,
                      int offset_c, const void *x, const void *beta,
                      const void *y_in, void *y_out, cudaStream_t stream);
+/* Free every cached device buffer (per-stream workspaces, counters,   */
+/* vector staging, mgpu root buffers, SYMV tile tables) after waiting   */
+/* for the devices that own them.  The next call re-creates what it     */
+/* needs.  For long-running processes that used many streams / shapes.  */
+int kblas_clear_cache(void);
 /* Number of kernels this library has launched since load.             */
 unsigned long long kblas_launch_count(void);
 /* When enabled, the library brackets every main (matrix-streaming)    */

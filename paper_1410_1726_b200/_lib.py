@@ -151,6 +151,8 @@ def load():
         for name in ("kblas_setmatrix_async", "kblas_getmatrix_async"):
             getattr(lib, name).argtypes = [c_int, c_int, c_size_t, c_void_p, c_int, c_void_p, c_int, c_void_p]
             getattr(lib, name).restype = c_int
+        lib.kblas_clear_cache.argtypes = []
+        lib.kblas_clear_cache.restype = c_int
         lib.kblas_launch_count.restype = c_ulonglong
         lib.kblas_launch_count.argtypes = []
         lib.kblas_timing_enable.argtypes = [c_int]

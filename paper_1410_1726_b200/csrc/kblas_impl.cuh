@@ -129,6 +129,8 @@ inline cudaError_t workspace(size_t bytes, cudaStream_t st, void **out) {
 // zero between calls (the finishing CTA resets its counter), zeroed when
 // (re)allocated.  Cached per (device, stream) like the workspace.
 inline std::map<std::pair<int, cudaStream_t>, WsBuf> g_cnt;
+// mgpu root partial buffers (kblas_x*_mgpu), per (root device, stream)
+inline std::map<std::pair<int, cudaStream_t>, WsBuf> g_rootbufs;
 
 inline cudaError_t counters(size_t n, cudaStream_t st, unsigned **out) {
   int dev = 0;
@@ -933,11 +935,9 @@ int mgpu_entry(bool is_gemv, char op, bool herm, int m, int n, T alpha, T *const
   cudaSetDevice(root);
   void *rootbuf = nullptr;
   // separate from the kernel workspace: allocated once per (device, root stream)
-  static std::mutex mu;
-  static std::map<std::pair<int, cudaStream_t>, WsBuf> rootbufs;
   {
-    std::lock_guard<std::mutex> lk(mu);
-    WsBuf &b = rootbufs[{root, rst}];
+    std::lock_guard<std::mutex> lk(g_mu);
+    WsBuf &b = g_rootbufs[{root, rst}];
     const size_t need = (size_t)ylen * sizeof(T) * (ngpus + 1);
     if (b.bytes < need) {
       if (b.ptr) { cudaDeviceSynchronize(); cudaFree(b.ptr); }

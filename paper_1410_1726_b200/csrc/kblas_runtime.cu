@@ -211,6 +211,35 @@ int kblas_p2p_combine_async(char prec, int nranks, const void *slots, long long 
   return code(cudaGetLastError());
 }
 
+int kblas_clear_cache(void) {
+  // every cached buffer (workspaces, counters, staging, mgpu root buffers,
+  // tile tables); waits for the devices that own them first
+  std::lock_guard<std::mutex> lk(g_mu);
+  DevGuard guard;
+  int rc = 0;
+  auto release = [&](std::map<std::pair<int, cudaStream_t>, WsBuf> &m) {
+    for (auto &kv : m) {
+      if (!kv.second.ptr) continue;
+      cudaSetDevice(kv.first.first);
+      cudaDeviceSynchronize();
+      if (cudaFree(kv.second.ptr) != cudaSuccess) rc = 1;
+    }
+    m.clear();
+  };
+  release(g_ws);
+  release(g_cnt);
+  release(g_vecs);
+  release(g_rootbufs);
+  for (auto &kv : g_tiles) {
+    if (!kv.second.dev) continue;
+    cudaSetDevice((int)kv.first[0]);
+    cudaDeviceSynchronize();
+    if (cudaFree(kv.second.dev) != cudaSuccess) rc = 1;
+  }
+  g_tiles.clear();
+  return rc;
+}
+
 unsigned long long kblas_launch_count(void) { return g_launches.load(); }
 
 int kblas_timing_enable(int enable) {

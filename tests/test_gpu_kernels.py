@@ -727,3 +727,21 @@ class TestGemvNCluster:
         x, y = naive.fill(rng, 1500, "d"), naive.fill(rng, 1100, "d")
         merged, _ = kb.gemv_mgpu("n", 1.1, kb.distribute(v, 64, 3), x, 0.4, y)
         check(merged.y_out, naive.naive_gemv("n", 1.1, a, x, 0.4, y), "d", 1.1, np.abs(a), x, 0.4, y)
+
+
+def test_clear_cache_and_reuse():
+    """kblas_clear_cache frees every cached buffer; later calls re-create
+    them and give bit-identical results."""
+    lib = _lib.load()
+    rng = np.random.default_rng(181)
+    v, a = dev_matrix(rng, 1500, 1500, "d")
+    x, y = dvec(naive.fill(rng, 1500, "d")), dvec(naive.fill(rng, 1500, "d"))
+    s1 = kb.symv_hemv("l", 1.0, kb.HermitianView(v, "l"), x, 0.5, y).y_out
+    g1 = kb.gemv("n", 1.0, v, x, 0.5, y).y_out
+    m1 = kb.symv_hemv_mgpu("l", 1.0, kb.distribute(v, 128, 2), x, 0.5, y, kb.KernelConfig(128, 2))[0].y_out
+    torch.cuda.synchronize()
+    assert lib.kblas_clear_cache() == 0
+    s2 = kb.symv_hemv("l", 1.0, kb.HermitianView(v, "l"), x, 0.5, y).y_out
+    g2 = kb.gemv("n", 1.0, v, x, 0.5, y).y_out
+    m2 = kb.symv_hemv_mgpu("l", 1.0, kb.distribute(v, 128, 2), x, 0.5, y, kb.KernelConfig(128, 2))[0].y_out
+    assert torch.equal(s1, s2) and torch.equal(g1, g2) and torch.equal(m1, m2)
