@@ -557,8 +557,8 @@ def main():
         except Exception:
             pass
         line = {
-            "metric": "achieved HBM GB/s (DSYMV lower, algorithmic bytes)" if family == "symv"
-            else "achieved HBM GB/s (GEMV, algorithmic bytes)",
+            "metric": "achieved HBM GB/s (DSYMV lower, algorithmic bytes)" if opname == "dsymv"
+            else f"achieved HBM GB/s ({opname.upper()}, algorithmic bytes)",
             "value": round(res["gbs"], 2),
             "unit": "GB/s",
             "n_gpus": world,
