@@ -745,3 +745,31 @@ def test_clear_cache_and_reuse():
     g2 = kb.gemv("n", 1.0, v, x, 0.5, y).y_out
     m2 = kb.symv_hemv_mgpu("l", 1.0, kb.distribute(v, 128, 2), x, 0.5, y, kb.KernelConfig(128, 2))[0].y_out
     assert torch.equal(s1, s2) and torch.equal(g1, g2) and torch.equal(m1, m2)
+
+
+def test_cuda_graph_capture_after_warmup():
+    """After one warm-up call on a stream (which creates that stream's
+    workspace and the shape's tile table), the async entry points can be
+    captured into a CUDA graph and replayed: same results, no host work."""
+    rng = np.random.default_rng(191)
+    v, a = dev_matrix(rng, 3000, 3000, "d")
+    x = dvec(naive.fill(rng, 3000, "d"))
+    y = torch.empty(3000, dtype=torch.float64, device="cuda")
+    g_out = torch.empty(3000, dtype=torch.float64, device="cuda")
+    s = torch.cuda.Stream()
+    hv = kb.HermitianView(v, "l")
+    with torch.cuda.stream(s):
+        kb.symv_hemv("l", 1.0, hv, x, 0.0, y, inplace=True)
+        kb.gemv("t", 1.0, v, x, 0.0, g_out, inplace=True)
+        s.synchronize()
+        want_s, want_g = y.clone(), g_out.clone()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=s):
+            kb.symv_hemv("l", 1.0, hv, x, 0.0, y, inplace=True)
+            kb.gemv("t", 1.0, v, x, 0.0, g_out, inplace=True)
+    y.zero_()
+    g_out.zero_()
+    for _ in range(3):
+        graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(y, want_s) and torch.equal(g_out, want_g)
