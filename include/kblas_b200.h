@@ -446,6 +446,33 @@ int kblas_set_gemv_split_waves(int waves);
 /* operands), 1 = always clusters, 0 = global partial slots.  Returns   */
 /* the previous mode.                                                  */
 int kblas_set_gemv_cluster(int mode);
+/* Empirical tuning table (written by paper_1410_1726_b200/tuner.py,    */
+/* the on-device replacement of the reference's analytic tuner,         */
+/* tuner.py:168-235).  Calls of precision prec ('s','d','c','z') and    */
+/* operation op whose order key lies in [n_lo, n_hi] run with the given  */
+/* choices; the key is round(sqrt(m*n)) for GEMV and d for SYMV/HEMV.   */
+/* Single-GPU calls only; an explicit kblas_set_* value wins over the    */
+/* table, the table over the built-in rules.  The latest matching entry  */
+/* wins; an entry with the same (prec, op, n_lo, n_hi) is replaced.      */
+/*   op 'n': shape 0 auto | 3 (4 warps x 4 cols x 2 vectors, 2 CTAs/SM)  */
+/*           | 4 (16 x 4 x 1, 1 CTA/SM) | 5 (8 x 4 x 1, 2 CTAs/SM);       */
+/*           form -1 auto | 0 stacked-rows stream-K | 1 split form with   */
+/*           global partial slots | 2 split form reduced in a cluster;    */
+/*           waves 0 = default, else split-form grid in waves (1..64).   */
+/*   op 't'/'c': shape as for 'n' (stream-K form); form -1 auto |        */
+/*           0 stream-K | 1 column-owning; waves must be 0.              */
+/*   op 'l'/'u': shape -1 auto | 100 wide tiles (16 warps x 8 columns) | */
+/*           103 narrow (8 x 4) | 105 mid (8 x 8, 2 CTAs/SM); form -1,   */
+/*           waves 0.                                                    */
+/* Returns 0, or -k for an invalid argument k.                          */
+int kblas_tune_set(char prec, char op, long long n_lo, long long n_hi, int shape, int form, int waves);
+/* Remove every tuning-table entry. */
+int kblas_tune_clear(void);
+/* Number of tuning-table entries. */
+int kblas_tune_count(void);
+/* Read entry i (0-based) of the tuning table; -1 if out of range. */
+int kblas_tune_get(int i, char *prec, char *op, long long *n_lo, long long *n_hi, int *shape, int *form,
+                   int *waves);
 /* Register SYMV/HEMV kernel: orders up to max_order use narrow column */
 /* tiles (more work items for small operands).  Returns the previous   */
 /* threshold (default 2048).                                           */

@@ -177,12 +177,40 @@ def load():
         lib.kblas_set_symv_mid.restype = c_int
         lib.kblas_set_symv_narrow.argtypes = [c_int]
         lib.kblas_set_symv_narrow.restype = c_int
+        LL = ctypes.c_longlong
+        lib.kblas_tune_set.argtypes = [c_char, c_char, LL, LL, c_int, c_int, c_int]
+        lib.kblas_tune_set.restype = c_int
+        lib.kblas_tune_clear.argtypes = []
+        lib.kblas_tune_clear.restype = c_int
+        lib.kblas_tune_count.argtypes = []
+        lib.kblas_tune_count.restype = c_int
+        lib.kblas_tune_get.argtypes = [c_int, ctypes.c_char_p, ctypes.c_char_p, POINTER(LL), POINTER(LL),
+                                       POINTER(c_int), POINTER(c_int), POINTER(c_int)]
+        lib.kblas_tune_get.restype = c_int
         lib.kblas_last_plan.restype = ctypes.c_char_p
         lib.kblas_last_plan.argtypes = []
         lib.kblas_version.restype = ctypes.c_char_p
         lib.kblas_version.argtypes = []
         _lib = lib
+        path = os.environ.get("KBLAS_TUNING_FILE")
+        if path:
+            _load_tuning(lib, path)
         return lib
+
+
+def _load_tuning(lib, path: str):
+    """Install the tuning table saved at `path` (paper_1410_1726_b200.tuner
+    .save format); a bad file raises rather than running untuned silently."""
+    import json
+
+    with open(path) as fh:
+        doc = json.load(fh)
+    if doc.get("format") != "kblas-b200-tuning/1":
+        raise ValueError(f"{path}: not a kblas-b200 tuning table")
+    for e in doc["entries"]:
+        rc = lib.kblas_tune_set(e["prec"].encode(), e["op"].encode(), int(e["n_lo"]), int(e["n_hi"]),
+                                int(e["shape"]), int(e.get("form", -1)), int(e.get("waves", 0)))
+        check(rc, f"{path}: kblas_tune_set", ["prec", "op", "n_lo", "n_hi", "shape", "form", "waves"])
 
 
 def header_symbols() -> list[str]:

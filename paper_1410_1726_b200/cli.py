@@ -256,6 +256,49 @@ def cmd_run(args) -> int:
     return 0
 
 
+def cmd_tune(args) -> int:
+    """Measured coarse/fine search (reference cli.py:295-331): CSV of every
+    timed point, the winners on stderr, optionally applied and saved as a
+    tuning table (--save; load it with $KBLAS_TUNING_FILE)."""
+    from . import tuner
+    from .core import precision
+
+    try:
+        sizes = [int(s) for s in args.sizes.split(",") if s]
+        if not sizes or min(sizes) <= 0:
+            raise ValueError("--sizes needs positive orders")
+        prec = precision(args.prec)
+        tuner._check_kernel(args.kernel, prec)
+    except ValueError as e:
+        print(f"error: {e}", file=sys.stderr)
+        return 2
+    import torch
+
+    if not torch.cuda.is_available():
+        print("error: tune needs a CUDA device (the tuner times the sm_100a kernels)", file=sys.stderr)
+        return 2
+    coarse, fine = tuner.tune(args.kernel, args.prec, sizes, uplo=args.uplo, reps=args.reps,
+                              min_gain=args.min_gain)
+    fh = open(args.csv, "w", newline="") if args.csv else sys.stdout
+    try:
+        tuner.write_sweep_csv(coarse.points + fine.points, fh)
+    finally:
+        if fh is not sys.stdout:
+            fh.close()
+    print(f"coarse winner: {coarse.winner.label()}; fine recommendation: {fine.recommended.label()}",
+          file=sys.stderr)
+    for size in sorted(fine.per_size):
+        print(f"  size {size}: {fine.per_size[size].label()}", file=sys.stderr)
+    if args.save:
+        rows = tuner.entries_for(fine)
+        if args.merge and os.path.exists(args.save):
+            tuner.load(args.save)
+        tuner.apply(fine)
+        tuner.save(args.save, device=torch.cuda.get_device_name())
+        print(f"saved {len(rows)} tuned range(s) to {args.save}", file=sys.stderr)
+    return 0
+
+
 def build_parser() -> argparse.ArgumentParser:
     parser = argparse.ArgumentParser(
         prog="python -m paper_1410_1726_b200",
@@ -284,6 +327,19 @@ def build_parser() -> argparse.ArgumentParser:
     p.add_argument("--verify-max", type=int, default=16384)
     p.add_argument("--csv", help="write the report here instead of stdout")
     p.set_defaults(func=cmd_run)
+
+    p = sub.add_parser("tune", help="measured coarse/fine configuration search on the GPU")
+    p.add_argument("--kernel", choices=KERNEL_CHOICES, required=True)
+    p.add_argument("--prec", choices="sdcz", default="d")
+    p.add_argument("--sizes", default="1024,2048,4096,8192")
+    p.add_argument("--uplo", choices=("l", "u"), default="l")
+    p.add_argument("--reps", type=int, default=20)
+    p.add_argument("--min-gain", type=float, default=0.01,
+                   help="fraction a candidate must beat the built-in choice by")
+    p.add_argument("--csv", help="write the sweep here instead of stdout")
+    p.add_argument("--save", help="apply the result and save the tuning table (JSON) here")
+    p.add_argument("--merge", action="store_true", help="keep the entries already in --save")
+    p.set_defaults(func=cmd_tune)
     return parser
 
 

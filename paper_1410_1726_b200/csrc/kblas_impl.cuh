@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -237,12 +238,75 @@ template <class T> struct Cfg {
 
 };
 
-// ============================================================= GEMV-N
+// ============================================================= knobs
 // Split-form GEMV-N (gemv_ns_kernel) choice: -1 auto, 0 never, 1 always
 // (kblas_set_gemv_split, for the tuner).
 inline int g_gemv_split = -1;
 inline int g_gemv_variant = 0;  // 0: tuned default shape (kblas_set_gemv_variant)
 inline int g_split_waves = 1;   // split-form GEMV-N: CTAs per row block sized for this many waves
+// cluster split form (gemv_nc_kernel): -1 auto, 0 never, 1 always
+inline int g_gemv_cluster = -1;
+// column-owning form (gemv_tc_kernel) choice: -1 auto, 0 never, 1 always
+inline int g_gemv_tc = -1;
+inline int g_symv_variant = -1;  // -1: per-precision default variant
+
+// The knobs one call runs with: the process-wide setters above (tuning
+// hooks; a non-default value wins) over the empirical tuning table
+// (kblas_tune_set, written by paper_1410_1726_b200/tuner.py) over the
+// built-in rules.  Resolved once per call at dispatch, read by the run_*
+// functions on the same thread.
+struct Knobs {
+  int gsplit = -1, gcluster = -1, gwaves = 1, gtc = -1, gvariant = 0, svariant = -1;
+};
+inline thread_local Knobs t_k;
+
+// one row of the tuning table: calls of precision `prec` and operation
+// `op` ('n', 't', 'c' GEMV; 'l', 'u' SYMV/HEMV) whose order key lies in
+// [lo, hi] (GEMV: round(sqrt(m n)); SYMV: d) use these choices
+struct TuneEntry {
+  char prec, op;
+  long long lo, hi;
+  int shape, form, waves;
+};
+inline std::mutex g_tune_mu;
+inline std::vector<TuneEntry> g_tune;
+inline std::atomic<int> g_tune_n{0};
+
+template <class T>
+Knobs resolve_knobs(char op, long long key) {
+  Knobs k;
+  k.gsplit = g_gemv_split;
+  k.gcluster = g_gemv_cluster;
+  k.gwaves = g_split_waves;
+  k.gtc = g_gemv_tc;
+  k.gvariant = g_gemv_variant;
+  k.svariant = g_symv_variant;
+  if (key < 0 || g_tune_n.load(std::memory_order_acquire) == 0) return k;
+  if (op == 'c' && !is_cplx<T>()) op = 't';
+  std::lock_guard<std::mutex> lk(g_tune_mu);
+  for (auto it = g_tune.rbegin(); it != g_tune.rend(); ++it) {  // latest entry wins
+    const TuneEntry &e = *it;
+    if (e.prec != tname<T>()[0] || e.op != op || key < e.lo || key > e.hi) continue;
+    if (op == 'l' || op == 'u') {
+      if (k.svariant == -1 && e.shape >= 100) k.svariant = e.shape;
+    } else {
+      if (k.gvariant == 0 && e.shape > 0) k.gvariant = e.shape;
+      if (op == 'n') {
+        if (k.gsplit == -1 && k.gcluster == -1 && e.form >= 0) {
+          k.gsplit = e.form >= 1 ? 1 : 0;
+          k.gcluster = e.form == 2 ? 1 : (e.form == 1 ? 0 : -1);
+        }
+        if (k.gwaves == 1 && e.waves > 0) k.gwaves = e.waves;
+      } else if (k.gtc == -1 && e.form >= 0) {
+        k.gtc = e.form ? 1 : 0;
+      }
+    }
+    break;
+  }
+  return k;
+}
+
+// ============================================================= GEMV-N
 constexpr long long kSplitMaxSlots = 64;
 
 template <class T, int V, int NW, int CW>
@@ -268,9 +332,6 @@ cudaError_t run_gemv_ns(const Path<T> &pa, long long lda, int m, int n, const T 
   g_last_plan = buf;
   return cudaGetLastError();
 }
-
-// cluster split form (gemv_nc_kernel): -1 auto, 0 never, 1 always
-inline int g_gemv_cluster = -1;
 
 template <class T, int V, int NW, int CW>
 cudaError_t run_gemv_nc(const Path<T> &pa, long long lda, int m, int n, const T *x, ColMap cm, T *y, T alpha,
@@ -332,7 +393,7 @@ cudaError_t run_gemv_n(const Path<T> &pa, long long lda, int m, int n, const T *
     constexpr int NWs = 8, CWs = 4, RBs = 32 * V;
     const long long nrb_s = cdiv((long long)pa.lead + m, RBs);
     const long long Ps = (long long)dev_sms() * occupancy((const void *)gemv_ns_kernel<T, V, NWs, CWs>, NWs * 32);
-    const long long S = std::max<long long>(1, std::min<long long>({cdiv((long long)g_split_waves * Ps, nrb_s),
+    const long long S = std::max<long long>(1, std::min<long long>({cdiv((long long)t_k.gwaves * Ps, nrb_s),
                                                                      kSplitMaxSlots,
                                                                      std::max<long long>(1, n / (NWs * CWs))}));
     const bool fills = nrb_s * S >= dev_sms();
@@ -345,13 +406,13 @@ cudaError_t run_gemv_n(const Path<T> &pa, long long lda, int m, int n, const T *
     const double eff = (double)Pg / (double)(cdiv(Pg, Ps) * Ps);
     const bool large_ok = S <= 2 && eff >= 0.85 && fills;
     const bool half_fills = 2 * nrb_s * S >= dev_sms();  // small calls are latency-bound anyway
-    if (g_gemv_split == 1 || (g_gemv_split == -1 && ((!fused && half_fills && small) || large_ok))) {
+    if (t_k.gsplit == 1 || (t_k.gsplit == -1 && ((!fused && half_fills && small) || large_ok))) {
       // the CTAs of a row block as one cluster, reduced through DSMEM
       // (cluster sizes 2..16; 16 is the opt-in non-portable maximum)
       int Sc = 1;
       while (Sc < 16 && Sc < S) Sc *= 2;
       const bool cl_ok = S > 1 && n / Sc >= NWs * CWs && 4 * nrb_s * Sc >= dev_sms();
-      if (g_gemv_cluster == 1 || (g_gemv_cluster == -1 && cl_ok && small))
+      if (t_k.gcluster == 1 || (t_k.gcluster == -1 && cl_ok && small))
         return run_gemv_nc<T, V, NWs, CWs>(pa, lda, m, n, x, cm, y, alpha, beta, beta_zero, st, Sc, nrb_s);
       return run_gemv_ns<T, V, NWs, CWs>(pa, lda, m, n, x, cm, y, alpha, beta, beta_zero, st, S, nrb_s);
     }
@@ -381,8 +442,6 @@ cudaError_t run_gemv_n(const Path<T> &pa, long long lda, int m, int n, const T *
 }
 
 // ============================================================= GEMV-T/C
-// column-owning form (gemv_tc_kernel) choice: -1 auto, 0 never, 1 always
-inline int g_gemv_tc = -1;
 inline long long g_gemv_tc_max_bytes = 80LL << 20;
 
 template <class T, int V, int NW, int CB, bool CONJ>
@@ -424,7 +483,7 @@ cudaError_t run_gemv_t(const Path<T> &pa, long long lda, int m, int n, long long
     const bool enough = Pc >= dev_sms() / 2;
     const bool small = (long long)m * n * (long long)sizeof(T) <= g_gemv_tc_max_bytes;
     const bool any_size = (sizeof(T) == 16 || (sizeof(T) == 8 && !is_cplx<T>())) && eff >= 0.8;
-    if (g_gemv_tc == 1 || (g_gemv_tc == -1 && enough && (small || any_size)))
+    if (t_k.gtc == 1 || (t_k.gtc == -1 && enough && (small || any_size)))
       return run_gemv_tc<T, V, 8, CBc, CONJ>(pa, lda, m, n, nglob, x, cm, y, alpha, beta, beta_zero, st);
   }
   constexpr int H = 32 * V * R, CBW = NW * CW;
@@ -619,7 +678,6 @@ inline PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 // empirical tuning in profiles/r1_tune_symv_*.jsonl), 0 register-load
 // kernel, 1 TMA kernel.  KBLAS_NO_TMA=1 forces 0 at load.
 inline int g_use_tma = -2;
-inline int g_symv_variant = -1;  // -1: per-precision default variant
 inline int tma_mode() {
   if (g_use_tma == -2) {
     const char *e = getenv("KBLAS_NO_TMA");
@@ -715,12 +773,15 @@ template <class T>
 cudaError_t dispatch_gemv(char trans, const Path<T> &pa, long long lda, int m, int n, long long nglob,
                           const T *x, ColMap cm, T *y, T alpha, T beta, bool beta_zero, cudaStream_t st) {
   using C = Cfg<T>;
+  // single-GPU calls look up the tuning table by order; mgpu partials (and
+  // any call under an explicit setter) keep the process-wide knobs
+  t_k = resolve_knobs<T>(trans, cm.G == 1 ? std::llround(std::sqrt((double)m * (double)n)) : -1);
   // tuned per-precision shapes (profiles/r1j_tune_gemv_*.jsonl): S uses 16
   // warps at 1 CTA/SM (variant 4), Z GEMV-N 4 warps x 4 columns x 2 vectors
-  // per lane (variant 3); D, C and Z-T/C keep the 8 x 4 x 1 default
-  int gv = g_gemv_variant;
-  if (gv == 0) gv = sizeof(T) == 4 ? 4 : (sizeof(T) == 16 && trans == 'n') ? 3 : 0;
-  if (pa.vec && gv > 0) {
+  // per lane (variant 3); D, C and Z-T/C keep the 8 x 4 x 1 default (5)
+  int gv = t_k.gvariant;
+  if (gv == 0) gv = sizeof(T) == 4 ? 4 : (sizeof(T) == 16 && trans == 'n') ? 3 : 5;
+  if (pa.vec && (gv == 3 || gv == 4)) {
     // tuning variants (kblas_set_gemv_variant): (warps, columns per warp,
     // vectors per lane per column, CTAs per SM)
 #define KB_GV(NW, CW, R, MB)                                                                                  \
@@ -752,6 +813,7 @@ template <class T, bool HERM>
 cudaError_t dispatch_symv_h(bool lower, const Path<T> &pa, long long lda, int d, const T *x, ColMap cm,
                             int ncols_local, T *y, T alpha, T beta, bool beta_zero, cudaStream_t st) {
   using C = Cfg<T>;
+  t_k = resolve_knobs<T>(lower ? 'l' : 'u', cm.G == 1 ? d : -1);
   const T *A00 = pa.base + pa.lead;
   if (tma_ok(A00, lda, d)) {
 #define KB_TMA(NC, CW, RS, S)                                                                                 \
@@ -762,12 +824,12 @@ cudaError_t dispatch_symv_h(bool lower, const Path<T> &pa, long long lda, int d,
     // tuning variants (kblas_set_symv_variant); 0 is the default
     // (consumer warps, columns per warp, rows per lane, stages)
     if constexpr (sizeof(T) == 16) {
-      switch (g_symv_variant < 0 ? default_variant<T>() : g_symv_variant) {
+      switch (t_k.svariant < 0 ? default_variant<T>() : t_k.svariant) {
         case 1: KB_TMA(8, 8, 2, 3);
         default: KB_TMA(16, 4, 1, 5);
       }
     } else {
-      switch (g_symv_variant < 0 ? default_variant<T>() : g_symv_variant) {
+      switch (t_k.svariant < 0 ? default_variant<T>() : t_k.svariant) {
         case 1: KB_TMA(16, 8, 1, 5);
         default: KB_TMA(16, 8, 2, 3);
       }
@@ -786,7 +848,7 @@ cudaError_t dispatch_symv_h(bool lower, const Path<T> &pa, long long lda, int d,
   // register-kernel tuning variants (kblas_set_symv_variant 100+); small
   // operands use narrow tiles (variant 103, W = 32 columns, 16 for z) so
   // there are enough items to occupy every SM
-  int v = g_symv_variant;
+  int v = t_k.svariant;
   if (v < 100 && d <= g_symv_narrow_max) v = 103;
   // mid orders (s, d, c): 8 warps x 8 columns at 2 CTAs/SM ramps up faster
   // than one 16-warp CTA per SM (+2-10 % at d = 4096-12288,

@@ -3,6 +3,8 @@
 // host-vector calls, the peer-memory exchange), mgpu allocation and
 // layout helpers, panel copies, timing / tuning hooks and the version.
 // The per-precision templates are instantiated in kblas_<p>.cu.
+#include <cctype>
+#include <cstring>
 #include "kblas_impl.cuh"
 
 using namespace kb;
@@ -321,6 +323,56 @@ int kblas_set_gemv_split(int mode) {
   const int prev = g_gemv_split;
   g_gemv_split = mode < 0 ? -1 : (mode ? 1 : 0);
   return prev;
+}
+
+int kblas_tune_set(char prec, char op, long long n_lo, long long n_hi, int shape, int form, int waves) {
+  prec = (char)std::tolower((unsigned char)prec);
+  op = (char)std::tolower((unsigned char)op);
+  if (!std::strchr("sdcz", prec) || prec == 0) return -1;
+  const bool gemv = op == 'n' || op == 't' || op == 'c';
+  if (!gemv && op != 'l' && op != 'u') return -2;
+  if (n_lo < 0) return -3;
+  if (n_hi < n_lo) return -4;
+  if (gemv ? !(shape == 0 || shape == 3 || shape == 4 || shape == 5)
+           : !(shape == -1 || shape == 100 || shape == 103 || shape == 105))
+    return -5;
+  if (form < -1 || form > (op == 'n' ? 2 : gemv ? 1 : -1)) return -6;
+  if (waves < 0 || waves > 64 || (waves && op != 'n')) return -7;
+  std::lock_guard<std::mutex> lk(g_tune_mu);
+  for (TuneEntry &e : g_tune)
+    if (e.prec == prec && e.op == op && e.lo == n_lo && e.hi == n_hi) {
+      e.shape = shape;
+      e.form = form;
+      e.waves = waves;
+      return 0;
+    }
+  g_tune.push_back(TuneEntry{prec, op, n_lo, n_hi, shape, form, waves});
+  g_tune_n.store((int)g_tune.size(), std::memory_order_release);
+  return 0;
+}
+
+int kblas_tune_clear(void) {
+  std::lock_guard<std::mutex> lk(g_tune_mu);
+  g_tune.clear();
+  g_tune_n.store(0, std::memory_order_release);
+  return 0;
+}
+
+int kblas_tune_count(void) { return g_tune_n.load(std::memory_order_acquire); }
+
+int kblas_tune_get(int i, char *prec, char *op, long long *n_lo, long long *n_hi, int *shape, int *form,
+                   int *waves) {
+  std::lock_guard<std::mutex> lk(g_tune_mu);
+  if (i < 0 || i >= (int)g_tune.size()) return -1;
+  const TuneEntry &e = g_tune[i];
+  if (prec) *prec = e.prec;
+  if (op) *op = e.op;
+  if (n_lo) *n_lo = e.lo;
+  if (n_hi) *n_hi = e.hi;
+  if (shape) *shape = e.shape;
+  if (form) *form = e.form;
+  if (waves) *waves = e.waves;
+  return 0;
 }
 
 int kblas_set_tma(int mode) {
