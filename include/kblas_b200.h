@@ -454,6 +454,7 @@ int kblas_set_gemv_cluster(int mode);
 /* Single-GPU calls only; an explicit kblas_set_* value wins over the    */
 /* table, the table over the built-in rules.  The latest matching entry  */
 /* wins; an entry with the same (prec, op, n_lo, n_hi) is replaced.      */
+/* The library starts with its built-in measured table (kblas_tune_defaults). */
 /*   op 'n': shape 0 auto | 3 (4 warps x 4 cols x 2 vectors, 2 CTAs/SM)  */
 /*           | 4 (16 x 4 x 1, 1 CTA/SM) | 5 (8 x 4 x 1, 2 CTAs/SM);       */
 /*           form -1 auto | 0 stacked-rows stream-K | 1 split form with   */
@@ -466,8 +467,12 @@ int kblas_set_gemv_cluster(int mode);
 /*           waves 0.                                                    */
 /* Returns 0, or -k for an invalid argument k.                          */
 int kblas_tune_set(char prec, char op, long long n_lo, long long n_hi, int shape, int form, int waves);
-/* Remove every tuning-table entry. */
+/* Remove every tuning-table entry (built-in rules only). */
 int kblas_tune_clear(void);
+/* Replace the table by the measured B200 table built into the library  */
+/* (installed at load; paper_1410_1726_b200/tuning/b200.json).  Returns  */
+/* the number of entries.                                               */
+int kblas_tune_defaults(void);
 /* Number of tuning-table entries. */
 int kblas_tune_count(void);
 /* Read entry i (0-based) of the tuning table; -1 if out of range. */

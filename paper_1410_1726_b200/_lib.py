@@ -182,6 +182,8 @@ def load():
         lib.kblas_tune_set.restype = c_int
         lib.kblas_tune_clear.argtypes = []
         lib.kblas_tune_clear.restype = c_int
+        lib.kblas_tune_defaults.argtypes = []
+        lib.kblas_tune_defaults.restype = c_int
         lib.kblas_tune_count.argtypes = []
         lib.kblas_tune_count.restype = c_int
         lib.kblas_tune_get.argtypes = [c_int, ctypes.c_char_p, ctypes.c_char_p, POINTER(LL), POINTER(LL),

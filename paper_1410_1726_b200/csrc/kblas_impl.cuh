@@ -272,8 +272,11 @@ inline std::mutex g_tune_mu;
 inline std::vector<TuneEntry> g_tune;
 inline std::atomic<int> g_tune_n{0};
 
+void tune_builtin_once();  // kblas_runtime.cu
+
 template <class T>
 Knobs resolve_knobs(char op, long long key) {
+  tune_builtin_once();
   Knobs k;
   k.gsplit = g_gemv_split;
   k.gcluster = g_gemv_cluster;

@@ -10,6 +10,32 @@
 using namespace kb;
 using namespace kbi;
 
+namespace {
+// The measured B200 table (paper_1410_1726_b200/tuning/b200.json, made by
+// scripts/tune_all.py + scripts/merge_tuning.py), installed at load.
+const kbi::TuneEntry kBuiltinTuning[] = {
+#include "kblas_tuned_b200.inc"
+    {0, 0, 0, 0, 0, 0, 0}};
+
+int install_builtin_tuning() {
+  std::lock_guard<std::mutex> lk(g_tune_mu);
+  g_tune.clear();
+  for (const kbi::TuneEntry &e : kBuiltinTuning)
+    if (e.prec) g_tune.push_back(e);
+  g_tune_n.store((int)g_tune.size(), std::memory_order_release);
+  return (int)g_tune.size();
+}
+
+std::once_flag g_builtin_once;
+}  // namespace
+
+namespace kbi {
+// first touch of the table installs the built-in entries (lazily: the
+// table is an inline variable of the per-precision units, so a static
+// initialiser here could run before it is constructed)
+void tune_builtin_once() { std::call_once(g_builtin_once, [] { install_builtin_tuning(); }); }
+}  // namespace kbi
+
 // ====================================================================
 // extern "C" surface
 // ====================================================================
@@ -326,6 +352,7 @@ int kblas_set_gemv_split(int mode) {
 }
 
 int kblas_tune_set(char prec, char op, long long n_lo, long long n_hi, int shape, int form, int waves) {
+  tune_builtin_once();
   prec = (char)std::tolower((unsigned char)prec);
   op = (char)std::tolower((unsigned char)op);
   if (!std::strchr("sdcz", prec) || prec == 0) return -1;
@@ -351,17 +378,28 @@ int kblas_tune_set(char prec, char op, long long n_lo, long long n_hi, int shape
   return 0;
 }
 
+
+int kblas_tune_defaults(void) {
+  tune_builtin_once();
+  return install_builtin_tuning();
+}
+
 int kblas_tune_clear(void) {
+  tune_builtin_once();
   std::lock_guard<std::mutex> lk(g_tune_mu);
   g_tune.clear();
   g_tune_n.store(0, std::memory_order_release);
   return 0;
 }
 
-int kblas_tune_count(void) { return g_tune_n.load(std::memory_order_acquire); }
+int kblas_tune_count(void) {
+  tune_builtin_once();
+  return g_tune_n.load(std::memory_order_acquire);
+}
 
 int kblas_tune_get(int i, char *prec, char *op, long long *n_lo, long long *n_hi, int *shape, int *form,
                    int *waves) {
+  tune_builtin_once();
   std::lock_guard<std::mutex> lk(g_tune_mu);
   if (i < 0 || i >= (int)g_tune.size()) return -1;
   const TuneEntry &e = g_tune[i];

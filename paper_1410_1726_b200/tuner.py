@@ -44,6 +44,7 @@ import csv
 import ctypes
 import json
 import math
+import os
 from dataclasses import asdict, dataclass, field
 
 from . import _lib
@@ -118,9 +119,13 @@ def enumerate_configs(kernel: str, stage: str = "coarse", shape: int | None = No
         raise ValueError(f"stage must be 'coarse' or 'fine', got {stage!r}")
     base = AUTO_GEMV if shape is None else shape
     forms = GEMV_N_FORMS if op == "n" else GEMV_T_FORMS
-    out += [TuneConfig(base, f) for f in forms]
-    if op == "n":
-        out.append(TuneConfig(base, 1, 2))
+    # the forms of the coarse shape and, when that is not the built-in
+    # shape, of the built-in shape too (so runs whose coarse stages
+    # disagree still time the same cells)
+    for sh in dict.fromkeys((base, AUTO_GEMV)):
+        out += [TuneConfig(sh, f) for f in forms]
+        if op == "n":
+            out.append(TuneConfig(sh, 1, 2))
     if base != AUTO_GEMV:
         out.append(TuneConfig(base))
     return list(dict.fromkeys(out))
@@ -138,6 +143,7 @@ class TunePoint:
     seconds: float
     rel_diff: float
     plan: str
+    uplo: str = "l"
 
 
 @dataclass(frozen=True)
@@ -189,7 +195,16 @@ def set_entry(e: TableEntry):
 
 
 def clear():
+    """Empty the table: calls run on the built-in rules alone."""
     _lib.load().kblas_tune_clear()
+
+
+def defaults() -> int:
+    """Reinstall the measured table built into the library (BUILTIN_TABLE)."""
+    return int(_lib.load().kblas_tune_defaults())
+
+
+BUILTIN_TABLE = os.path.join(os.path.dirname(os.path.abspath(__file__)), "tuning", "b200.json")
 
 
 def restore(entries: list[TableEntry]):
@@ -262,7 +277,8 @@ class _Bench:
         g.manual_seed(seed)
         abytes = n * n * prec.element_bytes
         free = torch.cuda.mem_get_info(dev)[0]
-        copies = max(1, min(8, math.ceil(2 * self.L2_BYTES / max(1, abytes)), int(0.5 * free // max(1, abytes))))
+        # rotating copies: together > 4x L2, so every call streams from HBM
+        copies = max(1, min(64, math.ceil(4 * self.L2_BYTES / max(1, abytes)), int(0.5 * free // max(1, abytes))))
 
         def rnd(*shape):
             t = torch.empty(*shape, dtype=prec.torch_dtype, device=dev)
@@ -287,6 +303,10 @@ class _Bench:
             self.args = lambda A: (trans, n, n, self.one, A.data_ptr(), n, self.x.data_ptr(), 1, self.zero,
                                    self.y.data_ptr(), 1, self.stream)
 
+    def close(self):
+        # drop the operands now (the argument closures refer back to self)
+        self.As, self.x, self.y, self.args = [], None, None, None
+
     def call(self, i: int = 0):
         rc = self.fn(*self.args(self.As[i % len(self.As)]))
         _lib.check(rc, f"tuner {self.kernel}")
@@ -297,20 +317,18 @@ class _Bench:
         return self.y.clone()
 
     def time(self, reps: int, warmup: int) -> float:
+        """Seconds per call, back to back over the rotating copies."""
         torch = self.torch
         for i in range(warmup):
             self.call(i)
         torch.cuda.synchronize()
-        best = float("inf")
-        for _ in range(3):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            for i in range(reps):
-                self.call(i)
-            e1.record()
-            torch.cuda.synchronize()
-            best = min(best, e0.elapsed_time(e1) / 1e3 / reps)
-        return best
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for i in range(reps):
+            self.call(i)
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / 1e3 / reps
 
 
 def _alg_bytes(kernel: str, prec: Precision, n: int) -> int:
@@ -320,8 +338,9 @@ def _alg_bytes(kernel: str, prec: Precision, n: int) -> int:
 
 
 def sweep(kernel: str, prec: Precision, sizes, configs, uplo: str = "l", reps: int = 20, warmup: int = 3,
-          seed: int = 0) -> list[TunePoint]:
-    """Time every config at every size on the current CUDA device.  The
+          seed: int = 0, passes: int = 3) -> list[TunePoint]:
+    """Time every config at every size on the current CUDA device (best of
+    `passes` interleaved passes of `reps` back-to-back calls).  The
     library's tuning table is restored afterwards."""
     _check_kernel(kernel, prec)
     import torch
@@ -336,20 +355,31 @@ def sweep(kernel: str, prec: Precision, sizes, configs, uplo: str = "l", reps: i
             b = _Bench(kernel, prec, n, uplo, seed)
             nbytes = _alg_bytes(kernel, prec, n)
             ref = None
-            for cfg in configs:
+            diffs, plans = [], []
+
+            def install(cfg):
                 restore(saved)
                 if not cfg.is_auto:
                     set_entry(TableEntry(prec.tag, op, n, n, cfg.shape, cfg.form, cfg.waves))
+
+            for cfg in configs:
+                install(cfg)
                 y = b.result()
-                plan = _lib.last_plan()
+                plans.append(_lib.last_plan())
                 if ref is None:
                     ref = y
-                    diff = 0.0
-                else:
-                    scale = float(ref.abs().max()) or 1.0
-                    diff = float((y - ref).abs().max()) / scale
-                sec = b.time(reps, warmup)
-                points.append(TunePoint(kernel, prec, n, cfg, nbytes / sec / 1e9, sec, diff, plan))
+                diffs.append(float((y - ref).abs().max()) / (float(ref.abs().max()) or 1.0))
+            # timing passes interleave the candidates so clock or thermal
+            # drift does not favour the ones measured first; best pass wins
+            best = [float("inf")] * len(configs)
+            for _ in range(passes):
+                for i, cfg in enumerate(configs):
+                    install(cfg)
+                    best[i] = min(best[i], b.time(reps, warmup))
+            for i, cfg in enumerate(configs):
+                points.append(TunePoint(kernel, prec, n, cfg, nbytes / best[i] / 1e9, best[i], diffs[i], plans[i],
+                                        uplo))
+            b.close()
             del b
             torch.cuda.empty_cache()
     finally:
@@ -415,7 +445,7 @@ def tune(kernel: str, prec_tag: str, sizes, uplo: str = "l", reps: int = 20, war
     return coarse, fine
 
 
-SWEEP_CSV_HEADER = ["kernel", "precision", "shape", "form", "waves", "size", "measured_gbs", "seconds",
+SWEEP_CSV_HEADER = ["kernel", "precision", "uplo", "shape", "form", "waves", "size", "measured_gbs", "seconds",
                     "rel_diff", "plan"]
 
 
@@ -425,5 +455,5 @@ def write_sweep_csv(points, fh) -> None:
     w = csv.writer(fh)
     w.writerow(SWEEP_CSV_HEADER)
     for p in points:
-        w.writerow([p.kernel, p.precision.tag, p.config.shape, p.config.form, p.config.waves, p.size,
+        w.writerow([p.kernel, p.precision.tag, p.uplo, p.config.shape, p.config.form, p.config.waves, p.size,
                     f"{p.measured_gbs:.1f}", f"{p.seconds:.9f}", f"{p.rel_diff:.3e}", p.plan])

@@ -78,9 +78,12 @@ class TestEnumerate:
         assert [c.shape for c in tuner.enumerate_configs("gemv")[1:]] == list(tuner.GEMV_SHAPES)
         assert {c.form for c in tuner.enumerate_configs("gemv-t")[1:]} == {0}
         fine = tuner.enumerate_configs("gemv", "fine", 3)
-        assert {(c.form, c.waves) for c in fine[1:]} == {(0, 0), (1, 0), (2, 0), (1, 2), (-1, 0)}
-        assert all(c.shape == 3 for c in fine[1:])
-        assert {c.form for c in tuner.enumerate_configs("gemv-c", "fine", 5)[1:]} == {0, 1, -1}
+        assert {(c.form, c.waves) for c in fine[1:] if c.shape == 3} == {(0, 0), (1, 0), (2, 0), (1, 2), (-1, 0)}
+        assert {(c.form, c.waves) for c in fine[1:] if c.shape == 0} == {(0, 0), (1, 0), (2, 0), (1, 2)}
+        assert {c.shape for c in fine} == {0, 3}
+        assert {(c.shape, c.form) for c in tuner.enumerate_configs("gemv-c", "fine", 5)[1:]} == {
+            (5, 0), (5, 1), (5, -1), (0, 0), (0, 1)}
+        assert {c.shape for c in tuner.enumerate_configs("gemv-t", "fine")} == {0}
         assert [c.shape for c in tuner.enumerate_configs("hemv", "fine")[1:]] == list(tuner.SYMV_SHAPES)
 
     def test_errors(self):
@@ -302,3 +305,20 @@ class TestTuner:
         doc = json.loads(out.read_text())
         assert doc["format"] == "kblas-b200-tuning/1"
         assert all(e["prec"] == "z" and e["op"] == "t" for e in doc["entries"])
+
+
+class TestBuiltinTable:
+    def test_matches_shipped_json(self, clean_table):
+        assert tuner.defaults() == len(tuner.table())
+        doc = json.load(open(tuner.BUILTIN_TABLE))
+        assert doc["format"] == "kblas-b200-tuning/1"
+        assert tuner.table() == [tuner.TableEntry(**e) for e in doc["entries"]]
+
+    def test_ranges_disjoint_per_op(self):
+        doc = json.load(open(tuner.BUILTIN_TABLE))
+        by = {}
+        for e in doc["entries"]:
+            by.setdefault((e["prec"], e["op"]), []).append((e["n_lo"], e["n_hi"]))
+        for rs in by.values():
+            rs.sort()
+            assert all(a[1] < b[0] for a, b in zip(rs, rs[1:]))
