@@ -427,8 +427,12 @@ int kblas_set_symv_variant(int variant);
 /* Select the GEMV-N form: -1 (default) = automatic (the split form,   */
 /* narrow row blocks reduced inside one kernel, for small and short    */
 /* matrices; the stacked-rows stream-K form otherwise), 1 = always the */
-/* split form, 0 = never.  Returns the previous mode.                  */
+/* split form, 0 = never, 3 = the row-owning form (gemv_ro_kernel).     */
+/* Returns the previous mode.                                          */
 int kblas_set_gemv_split(int mode);
+/* Row-owning GEMV-N configuration 0..7 (tuning hook; -1 = from the     */
+/* tuning table).  Returns the previous value.                          */
+int kblas_set_gemv_rowown(int cfg);
 /* Tuning hook for the stacked GEMV-N and the GEMV-T/C kernel shapes     */
 /* (warps, columns per warp, vectors per lane, CTAs per SM); 0 = tuned   */
 /* default.  Returns the previous variant.                               */
@@ -458,7 +462,10 @@ int kblas_set_gemv_cluster(int mode);
 /*   op 'n': shape 0 auto | 3 (4 warps x 4 cols x 2 vectors, 2 CTAs/SM)  */
 /*           | 4 (16 x 4 x 1, 1 CTA/SM) | 5 (8 x 4 x 1, 2 CTAs/SM);       */
 /*           form -1 auto | 0 stacked-rows stream-K | 1 split form with   */
-/*           global partial slots | 2 split form reduced in a cluster;    */
+/*           global partial slots | 2 split form reduced in a cluster |   */
+/*           3 row-owning CTAs (shape 10..17 = its configuration: 16x4x8,  */
+/*           8x4x8, 8x2x8, 8x4x16, 8x2x16, 4x4x16, 16x2x8, 8x8x8 as warps x */
+/*           row lanes x columns in flight);                              */
 /*           waves 0 = default, else split-form grid in waves (1..64).   */
 /*   op 't'/'c': shape as for 'n' (stream-K form); form -1 auto |        */
 /*           0 stream-K | 1 column-owning; waves must be 0.              */

@@ -18,7 +18,7 @@ LIB = os.path.join(HERE, "libkblas_b200.so")
 SOURCES = [os.path.join(CSRC, f) for f in ("kblas_runtime.cu", "kblas_s.cu", "kblas_d.cu", "kblas_c.cu",
                                            "kblas_z.cu")]
 HEADERS = [os.path.join(CSRC, f) for f in ("kblas_impl.cuh", "kblas_entry_macros.cuh", "kblas_kernels.cuh",
-                                           "kblas_device.cuh", "kblas_symv_tma.cuh")]
+                                           "kblas_device.cuh", "kblas_symv_tma.cuh", "kblas_tuned_b200.inc")]
 DEPS = SOURCES + HEADERS + [os.path.join(os.path.dirname(HERE), "include", "kblas_b200.h")]
 
 NVCC_FLAGS = [

@@ -171,6 +171,8 @@ def load():
         lib.kblas_set_gemv_tc.restype = c_int
         lib.kblas_set_gemv_variant.argtypes = [c_int]
         lib.kblas_set_gemv_variant.restype = c_int
+        lib.kblas_set_gemv_rowown.argtypes = [c_int]
+        lib.kblas_set_gemv_rowown.restype = c_int
         lib.kblas_set_gemv_split.argtypes = [c_int]
         lib.kblas_set_gemv_split.restype = c_int
         lib.kblas_set_symv_mid.argtypes = [c_int]

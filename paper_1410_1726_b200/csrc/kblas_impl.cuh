@@ -249,6 +249,7 @@ inline int g_gemv_cluster = -1;
 // column-owning form (gemv_tc_kernel) choice: -1 auto, 0 never, 1 always
 inline int g_gemv_tc = -1;
 inline int g_symv_variant = -1;  // -1: per-precision default variant
+inline int g_gemv_ro_cfg = -1;   // row-owning GEMV-N configuration (kblas_set_gemv_rowown; -1: from the table)
 
 // The knobs one call runs with: the process-wide setters above (tuning
 // hooks; a non-default value wins) over the empirical tuning table
@@ -256,7 +257,7 @@ inline int g_symv_variant = -1;  // -1: per-precision default variant
 // built-in rules.  Resolved once per call at dispatch, read by the run_*
 // functions on the same thread.
 struct Knobs {
-  int gsplit = -1, gcluster = -1, gwaves = 1, gtc = -1, gvariant = 0, svariant = -1;
+  int gsplit = -1, gcluster = -1, gwaves = 1, gtc = -1, gvariant = 0, svariant = -1, rocfg = 0;
 };
 inline thread_local Knobs t_k;
 
@@ -284,6 +285,7 @@ Knobs resolve_knobs(char op, long long key) {
   k.gtc = g_gemv_tc;
   k.gvariant = g_gemv_variant;
   k.svariant = g_symv_variant;
+  k.rocfg = g_gemv_ro_cfg < 0 ? 0 : g_gemv_ro_cfg;
   if (key < 0 || g_tune_n.load(std::memory_order_acquire) == 0) return k;
   if (op == 'c' && !is_cplx<T>()) op = 't';
   std::lock_guard<std::mutex> lk(g_tune_mu);
@@ -293,6 +295,13 @@ Knobs resolve_knobs(char op, long long key) {
     if (op == 'l' || op == 'u') {
       if (k.svariant == -1 && e.shape >= 100) k.svariant = e.shape;
     } else {
+      if (e.form == 3) {  // row-owning: shape 10 + configuration
+        if (k.gsplit == -1 && k.gcluster == -1) {
+          k.gsplit = 3;
+          if (g_gemv_ro_cfg < 0) k.rocfg = e.shape - 10;
+        }
+        break;
+      }
       if (k.gvariant == 0 && e.shape > 0) k.gvariant = e.shape;
       if (op == 'n') {
         if (k.gsplit == -1 && k.gcluster == -1 && e.form >= 0) {
@@ -376,6 +385,49 @@ cudaError_t run_gemv_nc(const Path<T> &pa, long long lda, int m, int n, const T 
   return cudaGetLastError();
 }
 
+template <class T, int V, int NW, int LR, int U>
+bool run_gemv_ro(const Path<T> &pa, long long lda, int m, int n, const T *x, ColMap cm, T *y, T alpha, T beta,
+                 bool beta_zero, cudaStream_t st, cudaError_t *err) {
+  constexpr int RBo = LR * V;
+  const long long P = cdiv((long long)pa.lead + m, RBo);
+  // every CTA streams all n columns of its rows: needs enough row blocks to
+  // cover the GPU, else the caller falls back to the other forms
+  if (2 * P < dev_sms()) return false;
+  GemvParams p{pa.base, lda, m, n, pa.lead, x, nullptr, 0, 0, (int)P, 0, cm,
+               y, nullptr, widen(alpha), widen(beta), beta_zero ? 1 : 0, (long long)m};
+  {
+    TimedScope ts(st);
+    gemv_ro_kernel<T, V, NW, LR, U><<<(unsigned)P, NW * 32, 0, st>>>(p);
+  }
+  launched(1);
+  char buf[256];
+  snprintf(buf, sizeof buf, "gemv_ro %s %s lead=%d m=%d n=%d RB=%d NW=%d LR=%d U=%d P=%lld slots=1", tname<T>(),
+           V > 1 ? "v256" : "scalar", pa.lead, m, n, RBo, NW, LR, U, P);
+  g_last_plan = buf;
+  *err = cudaGetLastError();
+  return true;
+}
+
+// row-owning configurations (warps, row lanes per column, columns in
+// flight per lane); table shape 10 + index.  Measured at N = 1k-12k
+// (profiles/r1z_tune_gemv_ro*.jsonl): the best one keeps ~128-256 CTAs.
+template <class T, int V>
+bool dispatch_gemv_ro(int cfg, const Path<T> &pa, long long lda, int m, int n, const T *x, ColMap cm, T *y,
+                      T alpha, T beta, bool beta_zero, cudaStream_t st, cudaError_t *err) {
+#define KB_RO(NW, LR, U) return run_gemv_ro<T, V, NW, LR, U>(pa, lda, m, n, x, cm, y, alpha, beta, beta_zero, st, err)
+  switch (cfg) {
+    case 1: KB_RO(8, 4, 8);
+    case 2: KB_RO(8, 2, 8);
+    case 3: KB_RO(8, 4, 16);
+    case 4: KB_RO(8, 2, 16);
+    case 5: KB_RO(4, 4, 16);
+    case 6: KB_RO(16, 2, 8);
+    case 7: KB_RO(8, 8, 8);
+    default: KB_RO(16, 4, 8);
+  }
+#undef KB_RO
+}
+
 template <class T, int V, int NW, int CW, int R, int MINB = 2>
 cudaError_t run_gemv_n(const Path<T> &pa, long long lda, int m, int n, const T *x, ColMap cm, T *y,
                        T alpha, T beta, bool beta_zero, cudaStream_t st) {
@@ -390,6 +442,10 @@ cudaError_t run_gemv_n(const Path<T> &pa, long long lda, int m, int n, const T *
   // fused epilogue (the last CTA of a row block reduces it) when few CTAs
   // share a row block; otherwise a separate, parallel epilogue kernel
   const bool fused = maxslots <= kFuseMaxSlots;
+  if (t_k.gsplit == 3 && V > 1) {
+    cudaError_t err = cudaSuccess;
+    if (dispatch_gemv_ro<T, V>(t_k.rocfg, pa, lda, m, n, x, cm, y, alpha, beta, beta_zero, st, &err)) return err;
+  }
   {
     // small / short matrices: the split form keeps the row blocks narrow so
     // few CTAs share one, and reduces them in the same kernel

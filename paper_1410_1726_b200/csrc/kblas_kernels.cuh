@@ -334,6 +334,68 @@ __global__ void __launch_bounds__(NW * 32, 2) gemv_ns_kernel(const GemvParams p)
 }
 
 // ---------------------------------------------------------------------------
+// GEMV-N, row-owning form (small operands).  A CTA owns LR*V rows (LR lanes
+// of 32 bytes side by side: a 32*LR-byte segment of every column) and all
+// n columns, so no row is shared between CTAs: one kernel, no slots, no
+// counters.  Lane = (row lane rl = lane % LR, column lane cl = lane / LR);
+// a warp covers CPI = 32/LR columns per step, the NW warps take steps round
+// robin, U steps are loaded before any FMA.  At the end the CPI column
+// lanes of a row are added with shuffles and the NW warps in shared
+// memory, in fixed order.  The GEMV-T column-owning form's transpose; it
+// trades segment length (32*LR bytes) for a single pass with every CTA's
+// work identical, which wins while the call is latency-bound.
+// ---------------------------------------------------------------------------
+template <class T, int V, int NW, int LR, int U>
+__global__ void __launch_bounds__(NW * 32) gemv_ro_kernel(const GemvParams p) {
+  constexpr int CPI = 32 / LR, RBo = LR * V, STEP = NW * CPI;
+  __shared__ T red[NW][RBo];
+  const T *__restrict__ A = static_cast<const T *>(p.A);
+  const T *__restrict__ x = static_cast<const T *>(p.x);
+  T *y = static_cast<T *>(p.y);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int rl = lane % LR, cl = lane / LR;
+  const uint64_t pol = policy_evict_first();
+  const long long pw = (long long)blockIdx.x * RBo + rl * V;  // physical first row of this lane
+  const bool rok = pw < (long long)p.lead + p.m;
+  T acc[V];
+#pragma unroll
+  for (int v = 0; v < V; ++v) acc[v] = zero<T>();
+  for (int c = warp * CPI + cl; c - cl < p.n; c += U * STEP) {
+    Pack<T, V> a[U];
+    T xv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int col = c + u * STEP;
+      const bool cok = col < p.n;
+      xv[u] = cok ? __ldg(x + map_col(p.cm, col)) : zero<T>();
+      ld_pack(a[u], A + (long long)col * p.lda + pw, cok && rok, pol);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int v = 0; v < V; ++v) acc[v] = fma_(a[u].v(v), xv[u], acc[v]);
+  }
+#pragma unroll
+  for (int o = LR; o < 32; o <<= 1)
+#pragma unroll
+    for (int v = 0; v < V; ++v) acc[v] = add_(acc[v], shfl_xor_(acc[v], o));
+  if (cl == 0) {
+#pragma unroll
+    for (int v = 0; v < V; ++v) red[warp][rl * V + v] = acc[v];
+  }
+  __syncthreads();
+  if ((int)threadIdx.x < RBo) {
+    const long long i = (long long)blockIdx.x * RBo + threadIdx.x - p.lead;
+    if (i >= 0 && i < p.m) {
+      T sum = red[0][threadIdx.x];
+#pragma unroll
+      for (int w = 1; w < NW; ++w) sum = add_(sum, red[w][threadIdx.x]);
+      axpby_out(y, i, p, sum);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // GEMV-N split form over a thread-block cluster.  The S CTAs sharing a
 // 32*V-row block form one cluster (S = cluster size, up to 16): each CTA
 // reduces its warps in shared memory as gemv_ns_kernel does, then the

@@ -347,7 +347,13 @@ int kblas_set_gemv_tc(int mode, long long max_bytes) {
 
 int kblas_set_gemv_split(int mode) {
   const int prev = g_gemv_split;
-  g_gemv_split = mode < 0 ? -1 : (mode ? 1 : 0);
+  g_gemv_split = mode < 0 ? -1 : (mode == 3 ? 3 : mode ? 1 : 0);
+  return prev;
+}
+
+int kblas_set_gemv_rowown(int cfg) {
+  const int prev = g_gemv_ro_cfg;
+  g_gemv_ro_cfg = cfg < 0 ? -1 : cfg;
   return prev;
 }
 
@@ -360,10 +366,12 @@ int kblas_tune_set(char prec, char op, long long n_lo, long long n_hi, int shape
   if (!gemv && op != 'l' && op != 'u') return -2;
   if (n_lo < 0) return -3;
   if (n_hi < n_lo) return -4;
-  if (gemv ? !(shape == 0 || shape == 3 || shape == 4 || shape == 5)
-           : !(shape == -1 || shape == 100 || shape == 103 || shape == 105))
+  const bool rowown = op == 'n' && form == 3;
+  if (rowown ? !(shape >= 10 && shape <= 17)
+             : gemv ? !(shape == 0 || shape == 3 || shape == 4 || shape == 5)
+                    : !(shape == -1 || shape == 100 || shape == 103 || shape == 105))
     return -5;
-  if (form < -1 || form > (op == 'n' ? 2 : gemv ? 1 : -1)) return -6;
+  if (form < -1 || form > (op == 'n' ? 3 : gemv ? 1 : -1)) return -6;
   if (waves < 0 || waves > 64 || (waves && op != 'n')) return -7;
   std::lock_guard<std::mutex> lk(g_tune_mu);
   for (TuneEntry &e : g_tune)

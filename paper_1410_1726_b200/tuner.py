@@ -19,7 +19,8 @@ Candidates are a TuneConfig (shape, form, waves):
 * form: how the work of one row block (GEMV-N) or column block (GEMV-T/C)
   is shared between CTAs, the analogue of coop_tbs.  GEMV-N: 0 stacked-rows
   stream-K, 1 split form with global partial slots, 2 split form reduced in
-  a thread-block cluster.  GEMV-T/C: 0 stream-K, 1 column-owning CTAs.
+  a thread-block cluster, 3 row-owning CTAs (whose shape 10..17 selects
+  the configuration).  GEMV-T/C: 0 stream-K, 1 column-owning CTAs.
   -1 = built-in rule.
 * waves: split-form GEMV-N grid size in waves of the GPU (0 = default).
 
@@ -54,6 +55,7 @@ KERNELS = ("gemv", "gemv-t", "gemv-c", "symv", "hemv")
 GEMV_SHAPES = (5, 3, 4)
 SYMV_SHAPES = (100, 103, 105)
 GEMV_N_FORMS = (0, 1, 2)
+ROWOWN_SHAPES = tuple(range(10, 18))  # GEMV-N form 3: row-owning configuration 0..7
 GEMV_T_FORMS = (0, 1)
 AUTO_GEMV, AUTO_SYMV = 0, -1
 
@@ -126,6 +128,8 @@ def enumerate_configs(kernel: str, stage: str = "coarse", shape: int | None = No
         out += [TuneConfig(sh, f) for f in forms]
         if op == "n":
             out.append(TuneConfig(sh, 1, 2))
+    if op == "n":
+        out += [TuneConfig(s, 3) for s in ROWOWN_SHAPES]
     if base != AUTO_GEMV:
         out.append(TuneConfig(base))
     return list(dict.fromkeys(out))

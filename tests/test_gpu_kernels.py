@@ -498,21 +498,26 @@ class TestGemvEpilogueModes:
         check(r1.y_out, want, tag, 0.5, dense, xh, -2.0, yh)
 
 
-@pytest.fixture(params=["split", "stacked"])
+@pytest.fixture(params=["split", "stacked", "rowown0", "rowown2", "rowown5", "rowown7"])
 def gemv_form(request):
-    """Run a test on both GEMV-N forms: the split form (narrow row blocks,
-    CTAs of a row block reduced by the last to arrive) and the stacked-rows
-    stream-K form."""
-    prev = _lib.set_gemv_split(request.param == "split")
+    """Run a test on every GEMV-N form: the split form (narrow row blocks,
+    CTAs of a row block reduced by the last to arrive), the stacked-rows
+    stream-K form, and row-owning CTAs in several configurations (which
+    fall back to the other forms when the matrix has too few rows)."""
+    lib = _lib.load()
+    mode = {"split": 1, "stacked": 0}.get(request.param, 3)
+    prev = lib.kblas_set_gemv_split(mode)
+    prev_c = lib.kblas_set_gemv_rowown(int(request.param[6:]) if mode == 3 else -1)
     yield request.param
-    _lib.set_gemv_split(prev)
+    lib.kblas_set_gemv_rowown(prev_c)
+    lib.kblas_set_gemv_split(prev)
 
 
 class TestGemvNForms:
     @pytest.mark.parametrize("tag", "sdcz")
     def test_oracle_both_forms(self, gemv_form, tag):
         rng = np.random.default_rng(131)
-        for m, n in [(1, 1), (7, 5), (65, 33), (100, 3000), (1000, 37), (2049, 1537), (129, 20000)]:
+        for m, n in [(1, 1), (7, 5), (65, 33), (100, 3000), (1000, 37), (2049, 1537), (129, 20000), (4100, 301)]:
             for ld, ro in ((-(-m // 32) * 32 + 32, 0), (m + 11, 5), (m + 40, 3)):
                 host = np.full(ld * n, np.nan, dtype=naive.DTYPES[tag])
                 win = naive.window(host, ld, ro + m, n)
@@ -524,6 +529,12 @@ class TestGemvNForms:
                 rep = kb.gemv("n", 0.7, v, dvec(x), -0.3, dvec(y))
                 if gemv_form == "split":
                     assert rep.plan.startswith(("gemv_ns", "gemv_nc")), rep.plan
+                eb = v.precision.element_bytes
+                rows_per_cta = ({0: 4, 2: 2, 5: 4, 7: 8}[int(gemv_form[6:])] * (32 // eb)
+                                if gemv_form.startswith("rowown") else 0)
+                if (gemv_form.startswith("rowown") and (v.ld * eb) % 32 == 0
+                        and m >= 80 * rows_per_cta):  # enough row blocks for the GPU
+                    assert rep.plan.startswith("gemv_ro"), rep.plan
                 got = rep.y_out
                 assert torch.isfinite(got).all()
                 check(got, naive.naive_gemv("n", 0.7, a, x, -0.3, y), tag, 0.7, np.abs(a), x, -0.3, y)
@@ -540,15 +551,25 @@ class TestGemvNForms:
         check(r1, want, "d", 1.0, np.abs(a), x, 0.0, np.zeros(3000))
 
     def test_auto_picks_split_for_small(self):
+        """Built-in rules alone: the split form for a small square matrix;
+        with the built-in measured table: the row-owning form."""
         prev = _lib.set_gemv_split(-1)
+        saved = tuner.table()
         try:
             rng = np.random.default_rng(133)
             v, a = dev_matrix(rng, 1024, 1024, "d")
             x, y = naive.fill(rng, 1024, "d"), naive.fill(rng, 1024, "d")
+            want = naive.naive_gemv("n", 1.0, a, x, 1.0, y)
+            tuner.clear()
             rep = kb.gemv("n", 1.0, v, dvec(x), 1.0, dvec(y))
             assert rep.plan.startswith(("gemv_ns", "gemv_nc")), rep.plan
-            check(rep.y_out, naive.naive_gemv("n", 1.0, a, x, 1.0, y), "d", 1.0, np.abs(a), x, 1.0, y)
+            check(rep.y_out, want, "d", 1.0, np.abs(a), x, 1.0, y)
+            tuner.defaults()
+            rep = kb.gemv("n", 1.0, v, dvec(x), 1.0, dvec(y))
+            assert rep.plan.startswith("gemv_ro"), rep.plan
+            check(rep.y_out, want, "d", 1.0, np.abs(a), x, 1.0, y)
         finally:
+            tuner.restore(saved)
             _lib.set_gemv_split(prev)
 
 

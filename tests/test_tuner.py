@@ -50,8 +50,11 @@ class TestTable:
         ((b"d", b"n", -1, 2, 0, -1, 0), 3),
         ((b"d", b"n", 5, 2, 0, -1, 0), 4),
         ((b"d", b"n", 1, 2, 7, -1, 0), 5),      # not a GEMV shape
+        ((b"d", b"n", 1, 2, 5, 3, 0), 5),       # row-owning needs a configuration shape 10..17
+        ((b"d", b"n", 1, 2, 18, 3, 0), 5),
+        ((b"d", b"t", 1, 2, 12, 1, 0), 5),
         ((b"d", b"l", 1, 2, 3, -1, 0), 5),      # a GEMV shape for SYMV
-        ((b"d", b"n", 1, 2, 0, 3, 0), 6),       # GEMV-N forms are -1..2
+        ((b"d", b"n", 1, 2, 0, 4, 0), 6),       # GEMV-N forms are -1..3
         ((b"d", b"t", 1, 2, 0, 2, 0), 6),       # GEMV-T forms are -1..1
         ((b"d", b"l", 1, 2, 100, 0, 0), 6),     # SYMV has no form
         ((b"d", b"t", 1, 2, 0, -1, 2), 7),      # waves only for GEMV-N
@@ -80,7 +83,8 @@ class TestEnumerate:
         fine = tuner.enumerate_configs("gemv", "fine", 3)
         assert {(c.form, c.waves) for c in fine[1:] if c.shape == 3} == {(0, 0), (1, 0), (2, 0), (1, 2), (-1, 0)}
         assert {(c.form, c.waves) for c in fine[1:] if c.shape == 0} == {(0, 0), (1, 0), (2, 0), (1, 2)}
-        assert {c.shape for c in fine} == {0, 3}
+        assert {c.shape for c in fine if c.form == 3} == set(range(10, 18))
+        assert {c.shape for c in fine} == {0, 3} | set(range(10, 18))
         assert {(c.shape, c.form) for c in tuner.enumerate_configs("gemv-c", "fine", 5)[1:]} == {
             (5, 0), (5, 1), (5, -1), (0, 0), (0, 1)}
         assert {c.shape for c in tuner.enumerate_configs("gemv-t", "fine")} == {0}
@@ -215,9 +219,9 @@ class TestTableDrivesDispatch:
         run = _gemv_call(tag, "n", n)
         y0, plan0 = run()
         seen = {}
-        for form, prefix in ((0, "gemv_n "), (1, "gemv_ns "), (2, "gemv_nc ")):
+        for form, prefix in ((0, "gemv_n "), (1, "gemv_ns "), (2, "gemv_nc "), (3, "gemv_ro ")):
             tuner.clear()
-            tuner.set_entry(tuner.TableEntry(tag, "n", n - 10, n + 10, 5, form, 0))
+            tuner.set_entry(tuner.TableEntry(tag, "n", n - 10, n + 10, 11 if form == 3 else 5, form, 0))
             y, plan = run()
             assert plan.startswith(prefix), (form, plan)
             _close(y, y0, tag, n)
