@@ -51,9 +51,12 @@ forms = [
     ("stacked", lambda: (_lib.set_gemv_split(0), lib.kblas_set_gemv_cluster(-1))),
     ("t-streamk", lambda: (_lib.set_gemv_split(-1), lib.kblas_set_gemv_tc(0, 0))),
     ("t-colown", lambda: lib.kblas_set_gemv_tc(1, 0)),
+    ("rowown0", lambda: (lib.kblas_set_gemv_tc(-1, 0), lib.kblas_set_gemv_split(3), lib.kblas_set_gemv_rowown(0))),
+    ("rowown2", lambda: lib.kblas_set_gemv_rowown(2)),
+    ("rowown7", lambda: lib.kblas_set_gemv_rowown(7)),
 ]
 for tag in "sdcz":
-    for m, n, ld, ro in ((333, 517, 352, 3), (1025, 300, 1056, 0)):
+    for m, n, ld, ro in ((333, 517, 352, 3), (1025, 300, 1056, 0), (4100, 77, 4128, 5)):
         A = mat(tag, m, n, ld, ro)
         for fname, setf in forms:
             setf()
@@ -64,6 +67,7 @@ for tag in "sdcz":
         _lib.set_gemv_split(-1)
         lib.kblas_set_gemv_cluster(-1)
         lib.kblas_set_gemv_tc(-1, 0)
+        lib.kblas_set_gemv_rowown(-1)
     d, ld, ro = 700, 736, 5
     A = mat(tag, d + 1, d + 1, ld, ro).submatrix(0, 0, d, d)
     herm = tag in "cz"
