@@ -400,6 +400,16 @@ int kblas_mv_hostvec(char prec, char kind, char op, int hermitian, int m, int n,
                      const void *alpha, const void *dA, int lda, int offset_r,
                      int offset_c, const void *x, const void *beta,
                      const void *y_in, void *y_out, cudaStream_t stream);
+/* Same, without the final wait: returns once everything is enqueued.   */
+/* x, y_in and y_out must stay valid (and y_out unread) until the       */
+/* stream has been synchronised (kblas_stream_sync); lets the caller    */
+/* overlap its own bookkeeping with the kernels.                        */
+int kblas_mv_hostvec_async(char prec, char kind, char op, int hermitian, int m, int n,
+                           const void *alpha, const void *dA, int lda, int offset_r,
+                           int offset_c, const void *x, const void *beta,
+                           const void *y_in, void *y_out, cudaStream_t stream);
+/* cudaStreamSynchronize(stream); 0 or the CUDA error. */
+int kblas_stream_sync(cudaStream_t stream);
 /* Free every cached device buffer (per-stream workspaces, counters,   */
 /* vector staging, mgpu root buffers, SYMV tile tables) after waiting   */
 /* for the devices that own them.  The next call re-creates what it     */

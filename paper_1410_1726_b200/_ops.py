@@ -8,6 +8,10 @@ points on the current torch stream.
 
 from __future__ import annotations
 
+import ctypes
+import threading
+import weakref
+
 import numpy as np
 import torch
 
@@ -200,11 +204,50 @@ def host_vectors(x, y, inplace: bool) -> bool:
     return not inplace and not _is_torch(x) and not _is_torch(y)
 
 
+class _PinnedResults:
+    """Page-locked result buffers for the numpy-vector path, recycled when
+    the numpy array handed to the caller (and every view of it) is
+    released.  torch's caching host allocator records and polls a CUDA
+    event per block (~14 us per allocation once earlier results are still
+    alive); no event is needed here, because kblas_mv_hostvec has
+    synchronised its stream before the array is returned, so the GPU no
+    longer touches a buffer the caller can see or release."""
+
+    KEEP = 4  # free buffers kept per (dtype, length)
+
+    def __init__(self):
+        self._free: dict = {}
+        self._lock = threading.Lock()
+
+    def get(self, n: int, dtype: torch.dtype):
+        key = (dtype, n)
+        with self._lock:
+            lst = self._free.get(key)
+            t = lst.pop() if lst else None
+        if t is None:
+            t = torch.empty(n, dtype=dtype, pin_memory=True)
+        arr = t.numpy()
+        weakref.finalize(arr, self._release, key, t)
+        return t, arr
+
+    def _release(self, key, t):
+        with self._lock:
+            lst = self._free.setdefault(key, [])
+            if len(lst) < self.KEEP:
+                lst.append(t)
+
+
+_PINNED = _PinnedResults()
+
+
 def call_hostvec(prec: Precision, kind: str, op: str, hermitian: bool, m: int, n: int, alpha, a_ptr: int,
-                 lda: int, x, x_len: int, beta, y, y_len: int, device, off_r: int = 0, off_c: int = 0):
+                 lda: int, x, x_len: int, beta, y, y_len: int, device, off_r: int = 0, off_c: int = 0,
+                 while_running=None):
     """One FFI crossing for a numpy-vector call: H2D of x (and y when beta
-    != 0), the kernels, D2H of the result into a fresh page-locked buffer
-    (torch's caching host allocator), wait.  Returns the numpy result."""
+    != 0), the kernels, D2H of the result into a page-locked buffer
+    (_PinnedResults), then the wait.  `while_running()` (the caller's
+    report bookkeeping) runs between the enqueue and the wait, overlapped
+    with the kernels.  Returns (numpy result, while_running's result)."""
     xa = np.ascontiguousarray(np.asarray(x, dtype=prec.dtype))
     if xa.ndim != 1 or xa.size != x_len:
         raise ValueError(f"x must be a vector of length {x_len}")
@@ -217,15 +260,23 @@ def call_hostvec(prec: Precision, kind: str, op: str, hermitian: bool, m: int, n
         ya = np.ascontiguousarray(np.asarray(y, dtype=prec.dtype))
         if ya.ndim != 1 or ya.size != y_len:
             raise ValueError(f"y must be a vector of length {y_len}")
-    out = torch.empty(y_len, dtype=prec.torch_dtype, pin_memory=True)
+    out, out_np = _PINNED.get(y_len, prec.torch_dtype)
     a_c, b_c = _lib.scalar(prec.tag, alpha), _lib.scalar(prec.tag, beta)
-    import ctypes
-
+    extra = None
     with _on_device(device):
-        rc = _fn("kblas_mv_hostvec")(prec.tag.encode(), kind.encode(), op.encode(), 1 if hermitian else 0, m, n,
-                                     ctypes.addressof(a_c), a_ptr, lda, off_r, off_c, xa.ctypes.data,
-                                     ctypes.addressof(b_c), None if ya is None else ya.ctypes.data,
-                                     out.data_ptr(), stream_handle(device))
-    _lib.check(rc, "kblas_mv_hostvec")
-    return out.numpy()
+        sh = stream_handle(device)
+        rc = _fn("kblas_mv_hostvec_async")(prec.tag.encode(), kind.encode(), op.encode(), 1 if hermitian else 0,
+                                           m, n, ctypes.addressof(a_c), a_ptr, lda, off_r, off_c, xa.ctypes.data,
+                                           ctypes.addressof(b_c), None if ya is None else ya.ctypes.data,
+                                           out.data_ptr(), sh)
+        try:
+            if rc == 0 and while_running is not None:
+                extra = while_running()
+        finally:
+            # x, y_in and the result buffer stay referenced until the wait
+            rc_sync = _fn("kblas_stream_sync")(sh)
+    _lib.check(rc, "kblas_mv_hostvec_async")
+    _lib.check(rc_sync, "kblas_stream_sync")
+    del xa, ya
+    return out_np, extra
 

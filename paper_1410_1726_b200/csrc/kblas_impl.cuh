@@ -1162,7 +1162,8 @@ inline cudaError_t vec_staging(size_t bytes, cudaStream_t st, void **out) {
 
 template <class T>
 int hostvec_entry(bool is_gemv, char op, bool herm, int m, int n, T alpha, const T *dA, int lda,
-                         int off_r, int off_c, const T *hx, T beta, const T *hy_in, T *hy_out, cudaStream_t st) {
+                         int off_r, int off_c, const T *hx, T beta, const T *hy_in, T *hy_out, cudaStream_t st,
+                         bool sync) {
   const char o = (char)(op | 0x20);
   const bool tr = is_gemv && o != 'n';
   const long long xlen = is_gemv ? (tr ? m : n) : n;
@@ -1200,7 +1201,7 @@ int hostvec_entry(bool is_gemv, char op, bool herm, int m, int n, T alpha, const
   if (dyk == dy && ylen > 0 &&
       (e = cudaMemcpyAsync(hy_out, dy, ylen * sizeof(T), cudaMemcpyDeviceToHost, st)) != cudaSuccess)
     return (int)e;
-  return code(cudaStreamSynchronize(st));
+  return code(sync ? cudaStreamSynchronize(st) : cudaGetLastError());
 }
 
 template <class T>
@@ -1255,7 +1256,7 @@ int partial_p2p(bool is_gemv, char op, bool herm, int m, int n, T alpha, const T
   EXT template int partial_entry<T>(bool, char, bool, int, int, T, const T *, int, const T *, T *, int, int, int, \
                                     cudaStream_t);                                                            \
   EXT template int hostvec_entry<T>(bool, char, bool, int, int, T, const T *, int, int, int, const T *, T,       \
-                                    const T *, T *, cudaStream_t);                                            \
+                                    const T *, T *, cudaStream_t, bool);                                      \
   EXT template int partial_p2p<T>(bool, char, bool, int, int, T, const T *, int, const T *, int, int, int, T *,   \
                                   long long, unsigned long long *, unsigned long long *, unsigned *,           \
                                   unsigned long long, T, const T *, T *, cudaStream_t);

@@ -139,20 +139,38 @@ int kblas_getmatrix_async(int rows, int cols, size_t esize, const void *dA, int 
                                 (size_t)cols, cudaMemcpyDeviceToHost, stream));
 }
 
-int kblas_mv_hostvec(char prec, char kind, char op, int hermitian, int m, int n, const void *alpha,
-                     const void *dA, int lda, int offset_r, int offset_c, const void *hx, const void *beta,
-                     const void *hy_in, void *hy_out, cudaStream_t stream) {
+namespace {
+int mv_hostvec(char prec, char kind, char op, int hermitian, int m, int n, const void *alpha, const void *dA,
+               int lda, int offset_r, int offset_c, const void *hx, const void *beta, const void *hy_in,
+               void *hy_out, cudaStream_t stream, bool sync) {
   const bool g = (kind | 0x20) == 'g';
   if (!g && (kind | 0x20) != 's') return -2;
   if (!g && offset_r != offset_c) return -11;
   switch (prec | 0x20) {
-    case 's': return hostvec_entry<float>(g, op, false, m, n, *(const float *)alpha, (const float *)dA, lda, offset_r, offset_c, (const float *)hx, *(const float *)beta, (const float *)hy_in, (float *)hy_out, stream);
-    case 'd': return hostvec_entry<double>(g, op, false, m, n, *(const double *)alpha, (const double *)dA, lda, offset_r, offset_c, (const double *)hx, *(const double *)beta, (const double *)hy_in, (double *)hy_out, stream);
-    case 'c': return hostvec_entry<float2>(g, op, hermitian != 0, m, n, *(const float2 *)alpha, (const float2 *)dA, lda, offset_r, offset_c, (const float2 *)hx, *(const float2 *)beta, (const float2 *)hy_in, (float2 *)hy_out, stream);
-    case 'z': return hostvec_entry<double2>(g, op, hermitian != 0, m, n, *(const double2 *)alpha, (const double2 *)dA, lda, offset_r, offset_c, (const double2 *)hx, *(const double2 *)beta, (const double2 *)hy_in, (double2 *)hy_out, stream);
+    case 's': return hostvec_entry<float>(g, op, false, m, n, *(const float *)alpha, (const float *)dA, lda, offset_r, offset_c, (const float *)hx, *(const float *)beta, (const float *)hy_in, (float *)hy_out, stream, sync);
+    case 'd': return hostvec_entry<double>(g, op, false, m, n, *(const double *)alpha, (const double *)dA, lda, offset_r, offset_c, (const double *)hx, *(const double *)beta, (const double *)hy_in, (double *)hy_out, stream, sync);
+    case 'c': return hostvec_entry<float2>(g, op, hermitian != 0, m, n, *(const float2 *)alpha, (const float2 *)dA, lda, offset_r, offset_c, (const float2 *)hx, *(const float2 *)beta, (const float2 *)hy_in, (float2 *)hy_out, stream, sync);
+    case 'z': return hostvec_entry<double2>(g, op, hermitian != 0, m, n, *(const double2 *)alpha, (const double2 *)dA, lda, offset_r, offset_c, (const double2 *)hx, *(const double2 *)beta, (const double2 *)hy_in, (double2 *)hy_out, stream, sync);
   }
   return -1;
 }
+}  // namespace
+
+int kblas_mv_hostvec(char prec, char kind, char op, int hermitian, int m, int n, const void *alpha,
+                     const void *dA, int lda, int offset_r, int offset_c, const void *hx, const void *beta,
+                     const void *hy_in, void *hy_out, cudaStream_t stream) {
+  return mv_hostvec(prec, kind, op, hermitian, m, n, alpha, dA, lda, offset_r, offset_c, hx, beta, hy_in, hy_out,
+                    stream, true);
+}
+
+int kblas_mv_hostvec_async(char prec, char kind, char op, int hermitian, int m, int n, const void *alpha,
+                           const void *dA, int lda, int offset_r, int offset_c, const void *hx, const void *beta,
+                           const void *hy_in, void *hy_out, cudaStream_t stream) {
+  return mv_hostvec(prec, kind, op, hermitian, m, n, alpha, dA, lda, offset_r, offset_c, hx, beta, hy_in, hy_out,
+                    stream, false);
+}
+
+int kblas_stream_sync(cudaStream_t stream) { return code(cudaStreamSynchronize(stream)); }
 
 // ------------------------------------------------ peer-memory exchange
 int kblas_ipc_get_handle(const void *dptr, void *handle_out) {

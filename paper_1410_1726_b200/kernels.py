@@ -168,12 +168,16 @@ def gemv(trans: str, alpha, a: MatrixView, x, beta, y, config: KernelConfig = DE
 def _gemv_hostvec(trans, alpha, a: MatrixView, x, beta, y, prec, x_len, y_len, dev) -> ExecutionReport:
     """numpy x and y: one kblas_mv_hostvec call (copies, kernels, result)."""
     ptr, lda, keep = _ops.matrix_in(a, dev)
-    y_out = _ops.call_hostvec(prec, "g", trans, False, a.rows, a.cols, alpha, ptr, lda, x, x_len, beta, y, y_len,
-                              dev)
-    rep = ExecutionReport()
-    fill_report(rep, prec, a.rows * a.cols, x_len, y_len, _is_zero(beta),
-                roofline.gemv_flops(prec, a.rows, a.cols, trans), _lib.last_plan())
-    rep.scal_invocations = 1
+
+    def report():  # built while the kernels run
+        rep = ExecutionReport()
+        fill_report(rep, prec, a.rows * a.cols, x_len, y_len, _is_zero(beta),
+                    roofline.gemv_flops(prec, a.rows, a.cols, trans), _lib.last_plan())
+        rep.scal_invocations = 1
+        return rep
+
+    y_out, rep = _ops.call_hostvec(prec, "g", trans, False, a.rows, a.cols, alpha, ptr, lda, x, x_len, beta, y,
+                                   y_len, dev, while_running=report)
     rep.y_out = y_out
     del keep
     return rep
@@ -199,10 +203,15 @@ def symv_hemv(uplo: str, alpha, a: HermitianView, x, beta, y, config: KernelConf
     if _ops.host_vectors(x, y, inplace) and not _is_zero(alpha):
         # numpy x and y: one kblas_mv_hostvec call (copies, kernels, result)
         ptr, lda, keep = _ops.matrix_in(a.base, dev, lower_tri=uplo)
-        y_out = _ops.call_hostvec(prec, "s", uplo, hermitian, d, d, alpha, ptr, lda, x, d, beta, y, d, dev)
-        rep = ExecutionReport()
-        fill_report(rep, prec, d * (d + 1) // 2, d, d, _is_zero(beta), roofline.symv_flops(prec, d),
-                    _lib.last_plan())
+
+        def report():  # built while the kernels run
+            rep = ExecutionReport()
+            fill_report(rep, prec, d * (d + 1) // 2, d, d, _is_zero(beta), roofline.symv_flops(prec, d),
+                        _lib.last_plan())
+            return rep
+
+        y_out, rep = _ops.call_hostvec(prec, "s", uplo, hermitian, d, d, alpha, ptr, lda, x, d, beta, y, d, dev,
+                                       while_running=report)
         rep.y_out = y_out
         del keep
         return rep

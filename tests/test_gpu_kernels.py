@@ -654,6 +654,32 @@ class TestHostVectorPath:
         check(rep.y_out, want, tag, 0.5, np.abs(naive.dense_from_triangle(tri, uplo, herm)), x, 2.0, y)
         assert rep.flops > 0 and rep.plan.startswith("symv")
 
+    def test_result_buffers_fresh_and_recycled(self):
+        """Results own their memory while alive (no aliasing between calls)
+        and the page-locked buffer is reused once a result is released."""
+        import gc
+
+        rng = np.random.default_rng(154)
+        v, a = dev_matrix(rng, 500, 400, "d")
+        x1, x2 = naive.fill(rng, 400, "d"), naive.fill(rng, 400, "d")
+        y = np.zeros(500)
+        r1 = kb.gemv("n", 1.0, v, x1, 0.0, y).y_out
+        keep = r1.copy()
+        r2 = kb.gemv("n", 1.0, v, x2, 0.0, y).y_out
+        assert r1.ctypes.data != r2.ctypes.data
+        assert np.array_equal(r1, keep)  # the second call did not write into the first result
+        view = r2[10:]
+        ptr2 = r2.ctypes.data
+        del r2
+        gc.collect()
+        r3 = kb.gemv("n", 1.0, v, x1, 0.0, y).y_out
+        assert r3.ctypes.data != ptr2  # a view keeps the buffer alive
+        assert np.array_equal(r3, keep)
+        del view, r3
+        gc.collect()
+        r4 = kb.gemv("n", 1.0, v, x2, 0.0, y).y_out
+        assert np.isfinite(r4).all()
+
     def test_inputs_not_mutated_and_errors(self):
         rng = np.random.default_rng(153)
         v, a = dev_matrix(rng, 300, 200, "d")
