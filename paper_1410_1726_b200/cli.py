@@ -299,6 +299,93 @@ def cmd_tune(args) -> int:
     return 0
 
 
+def cmd_roofline(args) -> int:
+    """Intensity / bandwidth-bound table (reference cli.py:236-248), with
+    the B200's measured copy bandwidth as the bound."""
+    from . import roofline
+
+    peak, source = copy_peak()
+    fh = open(args.csv, "w", newline="") if args.csv else sys.stdout
+    try:
+        roofline.write_intensity_csv(fh, peak, source, args.sample_n)
+    finally:
+        if fh is not sys.stdout:
+            fh.close()
+    return 0
+
+
+OFFSET_SCAN_HEADER = ["offset", "matrix_bytes", "measured_seconds", "achieved_gbs", "inflation"]
+
+
+def cmd_offset_scan(args) -> int:
+    """Measured counterpart of the reference's transaction-inflation scan
+    (cli.py:251-292): the standard kernel on an n x n window at every row
+    offset 0..max_off of one parent matrix, timed on the GPU; inflation is
+    the time relative to offset 0 (the reference's modelled segment count
+    has no meaning for the realigned 256-bit loads)."""
+    from .core import precision
+
+    try:
+        prec = precision(args.prec)
+        if args.n < 1 or args.max_off < 0:
+            raise ValueError("--n must be >= 1 and --max-off >= 0")
+    except ValueError as e:
+        print(f"error: {e}", file=sys.stderr)
+        return 2
+    import torch
+
+    if not torch.cuda.is_available():
+        print("error: offset-scan needs a CUDA device (it times the sm_100a kernels)", file=sys.stderr)
+        return 2
+    from . import _lib, roofline
+    from .core import MatrixView
+
+    dev = torch.device("cuda", torch.cuda.current_device())
+    n, mo = args.n, args.max_off
+    ld = -(-(n + mo) // 32) * 32
+    base = torch.empty(ld * n, dtype=prec.torch_dtype, device=dev)
+    (torch.view_as_real(base) if prec.is_complex else base).uniform_(-1, 1)
+    parent = MatrixView(base, n + mo, n, ld, prec)
+    x = torch.ones(n, dtype=prec.torch_dtype, device=dev)
+    y = torch.empty(n, dtype=prec.torch_dtype, device=dev)
+    trans = "n" if args.kernel == "gemv" else "t"
+    f = getattr(_lib.load(), f"kblas_{prec.tag}gemv_async")
+    one, zero = _lib.scalar(prec.tag, 1.0), _lib.scalar(prec.tag, 0.0)
+    st = torch.cuda.current_stream(dev).cuda_stream
+    nbytes = roofline.gemv_bytes(prec, n, n, trans)
+    rows, t0 = [], None
+    for off in range(mo + 1):
+        sub = parent.submatrix(off, 0, n, n)
+        ptr = base.data_ptr() + sub.linear_index(0, 0) * prec.element_bytes
+
+        def call():
+            _lib.check(f(trans.encode(), n, n, one, ptr, ld, x.data_ptr(), 1, zero, y.data_ptr(), 1, st),
+                       "offset-scan")
+
+        for _ in range(args.warmup):
+            call()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.reps):
+            call()
+        e1.record()
+        torch.cuda.synchronize(dev)
+        sec = e0.elapsed_time(e1) / 1e3 / args.reps
+        t0 = sec if t0 is None else t0
+        rows.append((off, nbytes, sec, nbytes / sec / 1e9, sec / t0))
+    fh = open(args.csv, "w", newline="") if args.csv else sys.stdout
+    try:
+        w = csv.writer(fh)
+        w.writerow(OFFSET_SCAN_HEADER)
+        for off, b, sec, gbs, infl in rows:
+            w.writerow([off, b, f"{sec:.9f}", f"{gbs:.1f}", f"{infl:.6f}"])
+    finally:
+        if fh is not sys.stdout:
+            fh.close()
+    return 0
+
+
 def build_parser() -> argparse.ArgumentParser:
     parser = argparse.ArgumentParser(
         prog="python -m paper_1410_1726_b200",
@@ -327,6 +414,21 @@ def build_parser() -> argparse.ArgumentParser:
     p.add_argument("--verify-max", type=int, default=16384)
     p.add_argument("--csv", help="write the report here instead of stdout")
     p.set_defaults(func=cmd_run)
+
+    p = sub.add_parser("roofline", help="emit the intensity / bandwidth-bound table for the B200")
+    p.add_argument("--sample-n", type=int, default=1_000_000)
+    p.add_argument("--csv", help="write the table here instead of stdout")
+    p.set_defaults(func=cmd_roofline)
+
+    p = sub.add_parser("offset-scan", help="measured time versus row offset (realignment check)")
+    p.add_argument("--kernel", choices=("gemv", "gemv-t"), default="gemv")
+    p.add_argument("--prec", choices="sdcz", default="s")
+    p.add_argument("--n", type=int, default=4096)
+    p.add_argument("--max-off", type=int, default=64)
+    p.add_argument("--reps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--csv", help="write the scan here instead of stdout")
+    p.set_defaults(func=cmd_offset_scan)
 
     p = sub.add_parser("tune", help="measured coarse/fine configuration search on the GPU")
     p.add_argument("--kernel", choices=KERNEL_CHOICES, required=True)

@@ -49,3 +49,25 @@ def gemv_flops(prec: Precision, m: int, n: int, trans: str = "n") -> int:
 
 def symv_flops(prec: Precision, d: int) -> int:
     return prec.flops_per_mul * (d * d + 2 * d) + prec.flops_per_add * d * d
+
+
+ROOFLINE_CSV_HEADER = ["precision", "family", "n", "flops", "bytes", "intensity", "peak_gflops", "note"]
+
+
+def write_intensity_csv(fh, copy_peak_gbs: float, source: str, sample_n: int = 1_000_000) -> None:
+    """The intensity / bandwidth-bound table of blockmv/roofline.py:92-136
+    for the B200: all 4 precisions x 2 families, intensity exact at
+    sample_n, peak = intensity x the measured copy bandwidth (the roofline
+    every kernel here is bound by)."""
+    import csv
+
+    from .core import precision
+
+    w = csv.writer(fh)
+    w.writerow(ROOFLINE_CSV_HEADER)
+    for tag in "sdcz":
+        prec = precision(tag)
+        for family in FAMILIES:
+            f, b = flop_count(prec, family, sample_n), byte_count(prec, family, sample_n)
+            w.writerow([tag, family, sample_n, f, b, f"{f / b:.6f}", f"{f / b * copy_peak_gbs:.2f}",
+                        f"copy peak {copy_peak_gbs:.1f} GB/s ({source})"])

@@ -73,3 +73,43 @@ class TestRunGpu:
         assert float(merged["achieved_gbs"]) > 0 and float(merged["measured_seconds"]) > 0
         devices = int(merged["devices"])
         assert len(rows) == 1 + (devices if devices > 1 else 0)
+
+
+class TestRooflineTable:
+    """`roofline` mirrors the reference's intensity table (test_cli.py:90-110):
+    8 rows, intensity exact at the sample size, peak = intensity x the copy
+    bandwidth."""
+
+    def test_eight_rows(self, tmp_path, monkeypatch):
+        monkeypatch.setenv("KBLAS_COPY_PEAK_GBS", "100")
+        out = tmp_path / "roofline.csv"
+        assert cli.main(["roofline", "--csv", str(out)]) == 0
+        rows = list(csv.reader(open(out)))
+        assert rows[0] == ["precision", "family", "n", "flops", "bytes", "intensity", "peak_gflops", "note"]
+        assert len(rows) == 9
+        s_gemv = next(r for r in rows[1:] if r[0] == "s" and r[1] == "gemv")
+        assert float(s_gemv[5]) == pytest.approx(0.50, abs=5e-6)
+        assert float(s_gemv[6]) == pytest.approx(50.0, abs=0.01)
+        z_symv = next(r for r in rows[1:] if r[0] == "z" and r[1] == "symv")
+        assert float(z_symv[5]) == pytest.approx(1.0, abs=1e-5)
+
+
+class TestOffsetScanArgs:
+    def test_errors(self):
+        assert cli.main(["offset-scan", "--n", "0"]) == 2
+        assert cli.main(["offset-scan", "--max-off", "-1"]) == 2
+
+
+@pytest.mark.gpu
+class TestOffsetScanGpu:
+    @pytest.mark.parametrize("kernel", ["gemv", "gemv-t"])
+    @pytest.mark.parametrize("tag", "dz")
+    def test_scan(self, tmp_path, kernel, tag):
+        out = tmp_path / "scan.csv"
+        assert cli.main(["offset-scan", "--kernel", kernel, "--prec", tag, "--n", "1024", "--max-off", "33",
+                         "--reps", "3", "--csv", str(out)]) == 0
+        rows = list(csv.reader(open(out)))
+        assert rows[0] == ["offset", "matrix_bytes", "measured_seconds", "achieved_gbs", "inflation"]
+        assert [int(r[0]) for r in rows[1:]] == list(range(34))
+        assert float(rows[1][4]) == 1.0
+        assert all(float(r[3]) > 0 for r in rows[1:])
