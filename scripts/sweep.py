@@ -126,6 +126,7 @@ def main():
     ap.add_argument("--no-cublas", action="store_true")
     ap.add_argument("--out", default=None)
     ap.add_argument("--passes", type=int, default=3, help="interleaved timing passes (best kept)")
+    ap.add_argument("--ld-pad", type=int, default=0, help="leading dimension = round_up(m, 32) + this")
     ap.add_argument("--ab-table", action="store_true",
                     help="also time each point with the tuning table cleared (built-in rules only)")
     args = ap.parse_args()
@@ -140,7 +141,7 @@ def main():
         p = precision(tag)
         for n in [int(s) for s in args.sizes.split(",")]:
             m = n
-            ld = -(-m // 32) * 32
+            ld = -(-m // 32) * 32 + args.ld_pad
             if n * ld * p.element_bytes > args.max_gb * 1e9:
                 continue
             mat_alloc = n * ld * p.element_bytes
@@ -203,7 +204,7 @@ def main():
             ms = best[0]
             sms = measure_single(ours, args.reps, flush)
             plan = _lib.last_plan()
-            row = {"op": opname, "n": n, "ms": round(ms, 5), "gbs": round(nbytes / ms / 1e6, 1),
+            row = {"op": opname, "n": n, "ld": ld, "ms": round(ms, 5), "gbs": round(nbytes / ms / 1e6, 1),
                    "pct_peak": round(100 * nbytes / ms / 1e6 / PEAK, 1), "single_ms": round(sms, 5),
                    "single_gbs": round(nbytes / sms / 1e6, 1), "copies": ncop, "plan": plan}
             if saved_table is not None:
