@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <initializer_list>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <tuple>
@@ -269,9 +270,16 @@ struct TuneEntry {
   long long lo, hi;
   int shape, form, waves;
 };
-inline std::mutex g_tune_mu;
-inline std::vector<TuneEntry> g_tune;
+inline std::mutex g_tune_mu;            // writers (kblas_tune_*)
+inline std::vector<TuneEntry> g_tune;     // guarded by g_tune_mu
 inline std::atomic<int> g_tune_n{0};
+// immutable copy the dispatcher reads without taking g_tune_mu
+inline std::shared_ptr<const std::vector<TuneEntry>> g_tune_snap;
+// call with g_tune_mu held after changing g_tune
+inline void publish_tune() {
+  std::atomic_store(&g_tune_snap, std::make_shared<const std::vector<TuneEntry>>(g_tune));
+  g_tune_n.store((int)g_tune.size(), std::memory_order_release);
+}
 
 void tune_builtin_once();  // kblas_runtime.cu
 
@@ -288,8 +296,9 @@ Knobs resolve_knobs(char op, long long key) {
   k.rocfg = g_gemv_ro_cfg < 0 ? 0 : g_gemv_ro_cfg;
   if (key < 0 || g_tune_n.load(std::memory_order_acquire) == 0) return k;
   if (op == 'c' && !is_cplx<T>()) op = 't';
-  std::lock_guard<std::mutex> lk(g_tune_mu);
-  for (auto it = g_tune.rbegin(); it != g_tune.rend(); ++it) {  // latest entry wins
+  const auto snap = std::atomic_load(&g_tune_snap);
+  if (!snap) return k;
+  for (auto it = snap->rbegin(); it != snap->rend(); ++it) {  // latest entry wins
     const TuneEntry &e = *it;
     if (e.prec != tname<T>()[0] || e.op != op || key < e.lo || key > e.hi) continue;
     if (op == 'l' || op == 'u') {

@@ -22,7 +22,7 @@ int install_builtin_tuning() {
   g_tune.clear();
   for (const kbi::TuneEntry &e : kBuiltinTuning)
     if (e.prec) g_tune.push_back(e);
-  g_tune_n.store((int)g_tune.size(), std::memory_order_release);
+  publish_tune();
   return (int)g_tune.size();
 }
 
@@ -397,10 +397,11 @@ int kblas_tune_set(char prec, char op, long long n_lo, long long n_hi, int shape
       e.shape = shape;
       e.form = form;
       e.waves = waves;
+      publish_tune();
       return 0;
     }
   g_tune.push_back(TuneEntry{prec, op, n_lo, n_hi, shape, form, waves});
-  g_tune_n.store((int)g_tune.size(), std::memory_order_release);
+  publish_tune();
   return 0;
 }
 
@@ -414,7 +415,7 @@ int kblas_tune_clear(void) {
   tune_builtin_once();
   std::lock_guard<std::mutex> lk(g_tune_mu);
   g_tune.clear();
-  g_tune_n.store(0, std::memory_order_release);
+  publish_tune();
   return 0;
 }
 
