@@ -150,81 +150,125 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------ CPU legs
-def cpu_baseline(seconds: float, n: int = CPU_SAMPLE_N, max_calls: int | None = None):
-    """The oracle (C restatement of the reference's naive_symv_hemv, all
-    host threads) on DSYMV lower N=n; GB/s on the same algorithmic bytes."""
+def _cpu_problem(opname: str, n: int):
+    """Host operands of the reference CPU path for --op at order n (seeded)."""
     import numpy as np
 
-    from oracle import streamed  # CPU baseline leg only
     from paper_1410_1726_b200 import roofline
     from paper_1410_1726_b200.core import precision
 
+    tag, family, op, herm = OPS[opname]
+    p = precision(tag)
     rng = np.random.default_rng(0)
-    a = np.asfortranarray(rng.uniform(-1, 1, size=(n, n)))
-    x = rng.uniform(-1, 1, size=n)
-    y = rng.uniform(-1, 1, size=n)
+
+    def rnd(*shape):
+        v = rng.uniform(-1, 1, size=shape)
+        if p.is_complex:
+            v = v + 1j * rng.uniform(-1, 1, size=shape)
+        return v.astype(p.dtype)
+
+    a = np.asfortranarray(rnd(n, n))
+    x, y = rnd(n), rnd(n)
+    nbytes = roofline.symv_bytes(p, n) if family == "symv" else roofline.gemv_bytes(p, n, n, op)
+    return tag, family, op, herm, a, x, y, nbytes
+
+
+def _cpu_call(streamed, family, op, herm, a, x, y):
+    if family == "symv":
+        streamed.symv(op, 1.0, a, x, 0.0, y, hermitian=herm)
+    else:
+        streamed.gemv(op, 1.0, a, x, 0.0, y)
+
+
+def cpu_sample_n(opname: str, n: int) -> int:
+    """Order of the CPU sample: the workload itself when it is small enough
+    (configs[0], DGEMV 4096), else CPU_SAMPLE_N (a bounded sample)."""
+    return min(n, CPU_SAMPLE_N)
+
+
+def cpu_baseline(seconds: float, opname: str = "dsymv", n: int = CPU_SAMPLE_N, max_calls: int | None = None):
+    """The oracle (C restatement of the reference's naive_gemv /
+    naive_symv_hemv, all host threads) on the --op workload at order n; GB/s
+    on the same algorithmic bytes."""
+    from oracle import streamed  # CPU baseline leg only
+
+    tag, family, op, herm, a, x, y, nbytes = _cpu_problem(opname, n)
     threads = streamed.max_threads()
-    streamed.symv("l", 1.0, a, x, 0.0, y)  # warm
+    _cpu_call(streamed, family, op, herm, a, x, y)  # warm
     calls, t0 = 0, time.perf_counter()
     while True:
-        streamed.symv("l", 1.0, a, x, 0.0, y)
+        _cpu_call(streamed, family, op, herm, a, x, y)
         calls += 1
         el = time.perf_counter() - t0
         if el >= seconds or (max_calls and calls >= max_calls):
             break
-    gbs = roofline.symv_bytes(precision("d"), n) * calls / el / 1e9
+    gbs = nbytes * calls / el / 1e9
     return {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "port",
-            "sample": f"oracle/streamed.c DSYMV lower N={n} (host matrix, f64 accumulation), "
+            "sample": f"oracle/streamed.c {opname} ({op}) N={n} (host matrix, wide accumulation), "
                       f"{calls} calls in {el:.1f} s, {threads} threads"}
 
 
+def metric_name(opname: str) -> str:
+    tag, family, op, herm = OPS[opname]
+    label = {"symv": "SYMV" if not herm else "HEMV", "gemv": "GEMV"}[family]
+    if opname == "dsymv":
+        return "achieved HBM GB/s (DSYMV lower, algorithmic bytes)"
+    return f"achieved HBM GB/s ({tag.upper()}{label}{'' if family == 'symv' else '-' + op.upper()}, algorithmic bytes)"
+
+
 def run_reference(args):
-    """--impl reference: the reference's CPU path (oracle port), rank 0 only."""
+    """--impl reference: the reference's CPU path (oracle port), rank 0 only,
+    on the same --op workload (a bounded sample when the order is large)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import numpy as np
-
     from oracle import streamed
-    from paper_1410_1726_b200 import roofline
-    from paper_1410_1726_b200.core import precision
 
-    n = CPU_SAMPLE_N
-    rng = np.random.default_rng(0)
-    a = np.asfortranarray(rng.uniform(-1, 1, size=(n, n)))
-    x = rng.uniform(-1, 1, size=n)
-    y = rng.uniform(-1, 1, size=n)
+    n_work = args.n or (32768 if OPS[args.op][1] == "symv" else 16384)  # bench_single's defaults
+    n = cpu_sample_n(args.op, n_work)
+    tag, family, op, herm, a, x, y, nbytes = _cpu_problem(args.op, n)
     threads = streamed.max_threads()
     for _ in range(args.warmup):
-        streamed.symv("l", 1.0, a, x, 0.0, y)
+        _cpu_call(streamed, family, op, herm, a, x, y)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        streamed.symv("l", 1.0, a, x, 0.0, y)
+        _cpu_call(streamed, family, op, herm, a, x, y)
     el = time.perf_counter() - t0
-    nbytes = roofline.symv_bytes(precision("d"), n)
     gbs = nbytes * args.steps / el / 1e9
-    sample = (f"oracle/streamed.c (C restatement of blockmv naive_symv_hemv) DSYMV lower N={n}, "
-              f"{threads} threads; bounded sample of configs[1] (DSYMV lower N=32768)")
+    whole = n == n_work
+    sample = (f"oracle/streamed.c (C restatement of blockmv naive_gemv / naive_symv_hemv) {args.op} N={n}, "
+              f"{threads} threads; " + ("the whole workload" if whole else f"bounded sample of N={n_work}"))
     blockmv_gbs = None
-    try:  # the reference package itself, if installed into baseline/_ref (pure-Python simulator)
-        sys.path.insert(0, os.path.join(ROOT, "baseline", "_ref"))
-        import blockmv
+    if args.op == "dsymv":
+        try:  # the reference package itself, if installed into baseline/_ref (pure-Python simulator)
+            import numpy as np
 
-        ns = 2048
-        v = blockmv.make_padded_view(ns, ns, blockmv.precision("d"), pad_to=32)
-        v.array()[:, :] = rng.uniform(-1, 1, size=(ns, ns))
-        hv = blockmv.HermitianView(base=v, uplo="l")
-        t1 = time.perf_counter()
-        blockmv.symv_hemv("l", 1.0, hv, x[:ns], 0.0, y[:ns], blockmv.KernelConfig(64, 4))
-        blockmv_gbs = round(roofline.symv_bytes(precision("d"), ns) / (time.perf_counter() - t1) / 1e9, 4)
-    except Exception:
-        pass
+            from paper_1410_1726_b200 import roofline
+            from paper_1410_1726_b200.core import precision
+
+            sys.path.insert(0, os.path.join(ROOT, "baseline", "_ref"))
+            import blockmv
+
+            ns = 2048
+            rng = np.random.default_rng(0)
+            v = blockmv.make_padded_view(ns, ns, blockmv.precision("d"), pad_to=32)
+            v.array()[:, :] = rng.uniform(-1, 1, size=(ns, ns))
+            hv = blockmv.HermitianView(base=v, uplo="l")
+            t1 = time.perf_counter()
+            blockmv.symv_hemv("l", 1.0, hv, x[:ns], 0.0, y[:ns], blockmv.KernelConfig(64, 4))
+            blockmv_gbs = round(roofline.symv_bytes(precision("d"), ns) / (time.perf_counter() - t1) / 1e9, 4)
+        except Exception:
+            pass
+    workload = ("DSYMV lower N=32768 (BASELINE configs[1])" if args.op == "dsymv" and n_work == 32768
+                else "DGEMV non-transposed N=4096 (BASELINE configs[0])" if args.op == "dgemv" and n_work == 4096
+                else f"{args.op} m={n_work} n={n_work}")
     print(json.dumps({
-        "impl": "reference", "metric": "achieved HBM GB/s (DSYMV lower, algorithmic bytes)", "value": round(gbs, 3),
+        "impl": "reference", "metric": metric_name(args.op), "value": round(gbs, 3),
         "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(el / args.steps * 1e3, 4), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic U(-1,1)",
-        "config": {"workload": f"DSYMV lower N={n} (CPU sample of configs[1])", "n": n, "uplo": "l"},
+        "scaling": "weak", "vs_baseline": None, "dtype": {"s": "f32", "d": "f64", "c": "c64", "z": "c128"}[tag],
+        "data": "synthetic U(-1,1)",
+        "config": {"workload": workload, "cpu_sample_n": n, "op": args.op},
         "cpu_baseline": {"value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "port",
                          "sample": sample},
         "e2e": {"value": round(gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -249,6 +293,10 @@ def bench_single(args, dev, rank):
     # column-major A: a (n, ld) row-major tensor whose row j is column j
     A = torch.empty(n, ld, dtype=p.torch_dtype, device=dev)
     (torch.view_as_real(A) if p.is_complex else A).uniform_(-1, 1)
+    # operands smaller than 4x the 126 MB L2 rotate over copies of A (>= 512
+    # MB together), so every step streams its matrix from HBM
+    ncopies = max(1, min(16, -(-(512 << 20) // A.numel() // p.element_bytes)))
+    As = [A] + [A.clone() for _ in range(ncopies - 1)]
     x_len, y_len = (n, m) if (family == "symv" or op == "n") else (m, n)
     x = torch.empty(x_len, dtype=p.torch_dtype, device=dev)
     y = torch.empty(y_len, dtype=p.torch_dtype, device=dev)
@@ -261,35 +309,36 @@ def bench_single(args, dev, rank):
         name = {("s", False): "ssymv", ("d", False): "dsymv", ("c", True): "chemv", ("z", True): "zhemv"}[(tag, herm)]
         fn = getattr(lib, f"kblas_{name}_async")
 
-        def step():
-            rc = fn(op.encode(), n, one, A.data_ptr(), ld, x.data_ptr(), 1, zero, y.data_ptr(), 1, sh)
+        def step(i=0):
+            rc = fn(op.encode(), n, one, As[i % ncopies].data_ptr(), ld, x.data_ptr(), 1, zero, y.data_ptr(), 1, sh)
             assert rc == 0, rc
     else:
         fn = getattr(lib, f"kblas_{tag}gemv_async")
 
-        def step():
-            rc = fn(op.encode(), m, n, one, A.data_ptr(), ld, x.data_ptr(), 1, zero, y.data_ptr(), 1, sh)
+        def step(i=0):
+            rc = fn(op.encode(), m, n, one, As[i % ncopies].data_ptr(), ld, x.data_ptr(), 1, zero, y.data_ptr(), 1,
+                    sh)
             assert rc == 0, rc
 
     nbytes = alg_bytes(tag, family, m, n, op)
     nflops = alg_flops(tag, family, m, n, op)
-    for _ in range(args.warmup):
-        step()
+    for i in range(args.warmup):
+        step(i)
     torch.cuda.synchronize(dev)
     plan = _lib.last_plan()
     clock = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
     clock.start()
     time.sleep(0.3)
     # warm the clocks up to the sampler's first reading, then time exactly K steps
-    for _ in range(args.warmup):
-        step()
+    for i in range(args.warmup):
+        step(i)
     torch.cuda.synchronize(dev)
     l0 = _lib.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize(dev)
     e0.record(stream)
-    for _ in range(args.steps):
-        step()
+    for i in range(args.steps):
+        step(i)
     e1.record(stream)
     torch.cuda.synchronize(dev)
     launches = _lib.launch_count() - l0
@@ -299,8 +348,8 @@ def bench_single(args, dev, rank):
     # brackets around each streaming-kernel launch (kept out of the timed
     # region above because the extra event records break the PDL overlap)
     _lib.timing_enable(True)
-    for _ in range(min(args.steps, 50)):
-        step()
+    for i in range(min(args.steps, 50)):
+        step(i)
     torch.cuda.synchronize(dev)
     _lib.timing_enable(False)
     kern_ms, kern_n = _lib.timing_read()
@@ -309,14 +358,14 @@ def bench_single(args, dev, rank):
     kern_avg = kern_ms / max(kern_n, 1)
     res = dict(tag=tag, family=family, op=op, m=m, n=n, ld=ld, nbytes=nbytes, nflops=nflops, ms_step=ms_step,
                gbs=gbs, kern_avg_ms=kern_avg, kern_launches=kern_n, launches=launches, plan=plan,
-               clocks=clocks, total_ms=total_ms)
+               clocks=clocks, total_ms=total_ms, ncopies=ncopies)
     # end to end through the public API with host (pinned) buffers
     if not args.no_e2e and args.e2e_steps > 0:
-        res["e2e"] = e2e_single(args, A, x, y, tag, family, op, herm, m, n, ld, dev, nbytes)
+        res["e2e"] = e2e_single(args, As, x, y, tag, family, op, herm, m, n, ld, dev, nbytes)
     return res
 
 
-def e2e_single(args, A, x, y, tag, family, op, herm, m, n, ld, dev, nbytes):
+def e2e_single(args, As, x, y, tag, family, op, herm, m, n, ld, dev, nbytes):
     """End to end through the public API (paper_1410_1726_b200.symv_hemv /
     gemv), as an iterative solver calls it: the matrix stays resident in HBM
     (uploaded once, like model weights), and every step copies that step's
@@ -336,22 +385,25 @@ def e2e_single(args, A, x, y, tag, family, op, herm, m, n, ld, dev, nbytes):
     eb = p.element_bytes
     x_len = n if (family == "symv" or op == "n") else m
 
-    def run(view, steps):
-        def step():
+    def run(views, steps):
+        def step(i):
+            view = views[i % len(views)]
             if family == "symv":
                 return kb.symv_hemv(op, 1.0, kb.HermitianView(view, op), npx, 0.0, npy, hermitian=herm).y_out
             return kb.gemv(op, 1.0, view, npx, 0.0, npy).y_out
 
-        step()
+        step(0)
         torch.cuda.synchronize(dev)
         t0 = time.perf_counter()
-        for _ in range(steps):
-            out = step()
+        for i in range(steps):
+            out = step(i)
         torch.cuda.synchronize(dev)
         return (time.perf_counter() - t0) / steps, out
 
-    # resident matrix: the headline end-to-end figure
-    el, out = run(kb.MatrixView(A.reshape(-1), m, n, ld, p), max(args.e2e_steps, 20))
+    # resident matrix (rotating over the same copies as the device-timed
+    # steps): the headline end-to-end figure
+    A = As[0]
+    el, out = run([kb.MatrixView(a.reshape(-1), m, n, ld, p) for a in As], max(args.e2e_steps, 20))
     y_len = len(out)
     res = {"value": round(nbytes / el / 1e9, 3), "unit": "GB/s",
            "h2d_bytes_per_step": int(x_len * eb + y_len * eb), "d2h_bytes_per_step": int(y_len * eb),
@@ -361,7 +413,7 @@ def e2e_single(args, A, x, y, tag, family, op, herm, m, n, ld, dev, nbytes):
     # host-resident matrix: the referenced part of A is uploaded every step too
     hA = torch.empty(A.numel(), dtype=A.dtype, pin_memory=True)
     hA.copy_(A.reshape(-1))
-    el2, _ = run(kb.MatrixView(hA.numpy(), m, n, ld, p), args.e2e_steps)
+    el2, _ = run([kb.MatrixView(hA.numpy(), m, n, ld, p)], args.e2e_steps)
     if family == "symv":
         blocks = [(b0, min(n, b0 + 256)) for b0 in range(0, n, 256)]
         h2d_a = sum((b1 - b0) * ((m - b0) if op == "l" else b1) for b0, b1 in blocks) * eb
@@ -442,8 +494,8 @@ def bench_mgpu(args, dev, rank, world):
     launches = _lib.launch_count() - l0
     clocks = clock.stop()
     _lib.timing_enable(True)
-    for _ in range(min(args.steps, 50)):
-        step()
+    for i in range(min(args.steps, 50)):
+        step(i)
     torch.cuda.synchronize(dev)
     _lib.timing_enable(False)
     kern_ms, kern_n = _lib.timing_read()
@@ -548,6 +600,8 @@ def main():
                         f"{xch} (weak scaling: n = 32768*sqrt(G))")
         elif args.op == "dsymv" and res["n"] == 32768:
             workload = "DSYMV lower N=32768 (BASELINE configs[1])"
+        elif args.op == "dgemv" and res["n"] == 4096 and res["m"] == 4096:
+            workload = "DGEMV non-transposed N=4096 (BASELINE configs[0])"
         else:
             workload = f"{opname} m={res['m']} n={res['n']}"
         prof_traffic = None
@@ -557,8 +611,7 @@ def main():
         except Exception:
             pass
         line = {
-            "metric": "achieved HBM GB/s (DSYMV lower, algorithmic bytes)" if opname == "dsymv"
-            else f"achieved HBM GB/s ({opname.upper()}, algorithmic bytes)",
+            "metric": metric_name(opname),
             "value": round(res["gbs"], 2),
             "unit": "GB/s",
             "n_gpus": world,
@@ -572,7 +625,10 @@ def main():
             "data": "synthetic U(-1,1), generated on device",
             "config": {"workload": workload, "op": opname, "m": res["m"], "n": res["n"], "ld": res["ld"],
                        "uplo_or_trans": op, "alpha": 1.0, "beta": 0.0,
-                       "l2": "inputs > 126 MB L2 (A streamed from HBM every step), no flush",
+                       "l2": ("inputs > 126 MB L2 (A streamed from HBM every step), no flush"
+                              if res.get("ncopies", 1) == 1 else
+                              f"{res['ncopies']} rotating copies of A (>= 512 MB together, > 4x the L2): "
+                              "every step streams its matrix from HBM"),
                        "parallelism": f"{world} GPU" + ("s, one process each" if world > 1 else "")},
             "pct_of_copy_peak": round(100 * res["gbs"] / hbm_peak, 2),
             "gflops": round(res.get("nflops", 0) / (res["ms_step"] * 1e-3) / 1e9, 2) if res.get("nflops") else None,
@@ -589,7 +645,7 @@ def main():
         }
         line["e2e"] = res.get("e2e")
         if not args.no_cpu and world == 1:
-            line["cpu_baseline"] = cpu_baseline(args.cpu_seconds)
+            line["cpu_baseline"] = cpu_baseline(args.cpu_seconds, args.op, cpu_sample_n(args.op, res["n"]))
         print(json.dumps(line), flush=True)
     if mgpu:
         import torch.distributed as dist
