@@ -290,12 +290,13 @@ def cmd_tune(args) -> int:
     for size in sorted(fine.per_size):
         print(f"  size {size}: {fine.per_size[size].label()}", file=sys.stderr)
     if args.save:
-        rows = tuner.entries_for(fine)
-        if args.merge and os.path.exists(args.save):
-            tuner.load(args.save)
+        # the file holds this run's ranges (and, with --merge, the file's
+        # earlier ranges for other kernels), never the library's built-in table
+        old = tuner.read(args.save) if args.merge and os.path.exists(args.save) else []
+        entries = tuner.merge_entries(old, fine)
         tuner.apply(fine)
-        tuner.save(args.save, device=torch.cuda.get_device_name())
-        print(f"saved {len(rows)} tuned range(s) to {args.save}", file=sys.stderr)
+        tuner.save(args.save, entries, device=torch.cuda.get_device_name())
+        print(f"saved {len(entries)} tuned range(s) to {args.save}", file=sys.stderr)
     return 0
 
 

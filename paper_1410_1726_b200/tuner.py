@@ -225,18 +225,31 @@ def save(path: str, entries: list[TableEntry] | None = None, device: str | None 
         fh.write("\n")
 
 
-def load(path: str, replace: bool = False) -> int:
-    """Install a saved table; returns the number of entries added."""
+def read(path: str) -> list[TableEntry]:
+    """The entries of a saved table (nothing is installed)."""
     with open(path) as fh:
         doc = json.load(fh)
     if doc.get("format") != "kblas-b200-tuning/1":
         raise ValueError(f"{path}: not a kblas-b200 tuning table")
+    return [TableEntry(**e) for e in doc["entries"]]
+
+
+def load(path: str, replace: bool = False) -> int:
+    """Install a saved table; returns the number of entries added."""
+    entries = read(path)
     if replace:
         clear()
-    entries = [TableEntry(**e) for e in doc["entries"]]
     for e in entries:
         set_entry(e)
     return len(entries)
+
+
+def merge_entries(old: list[TableEntry], result: FineResult) -> list[TableEntry]:
+    """`old` with every entry of the result's (precision, op) replaced by
+    the result's rows (a re-tune supersedes the earlier ranges)."""
+    op = op_of("symv" if result.kernel in ("symv", "hemv") else result.kernel, result.uplo)
+    kept = [e for e in old if (e.prec, e.op) != (result.precision.tag, op)]
+    return kept + entries_for(result)
 
 
 def entries_for(result: FineResult) -> list[TableEntry]:

@@ -142,6 +142,21 @@ class TestSaveLoad:
         doc = json.load(open(path))
         assert doc["device"] == "test" and doc["format"] == "kblas-b200-tuning/1"
 
+    def test_merge_replaces_only_the_retuned_kernel(self):
+        old = [tuner.TableEntry("d", "n", 1, 10, 3, 0), tuner.TableEntry("z", "l", 1, 10, 105),
+               tuner.TableEntry("d", "t", 1, 10, 0, 1)]
+        fine = tuner.FineResult("gemv", precision("d"), "l", {2048: tuner.TuneConfig(11, 3)},
+                                tuner.TuneConfig(11, 3))
+        merged = tuner.merge_entries(old, fine)
+        assert merged[:2] == [old[1], old[2]]
+        assert [(e.prec, e.op, e.shape, e.form) for e in merged[2:]] == [("d", "n", 11, 3)]
+
+    def test_read_does_not_install(self, clean_table, tmp_path):
+        path = str(tmp_path / "t.json")
+        tuner.save(path, [tuner.TableEntry("s", "n", 10, 20, 4, 2, 0)])
+        assert tuner.read(path) == [tuner.TableEntry("s", "n", 10, 20, 4, 2, 0)]
+        assert tuner.table() == []
+
     def test_bad_file(self, clean_table, tmp_path):
         p = tmp_path / "bad.json"
         p.write_text(json.dumps({"format": "other", "entries": []}))
@@ -308,7 +323,13 @@ class TestTuner:
                          "--csv", str(tmp_path / "t.csv"), "--save", str(out)]) == 0
         doc = json.loads(out.read_text())
         assert doc["format"] == "kblas-b200-tuning/1"
-        assert all(e["prec"] == "z" and e["op"] == "t" for e in doc["entries"])
+        assert all(e["prec"] == "z" and e["op"] == "t" for e in doc["entries"])  # no built-in rows
+        # --merge keeps the file's other kernels
+        assert cli.main(["tune", "--kernel", "hemv", "--prec", "z", "--sizes", "1024", "--reps", "3",
+                         "--csv", str(tmp_path / "h.csv"), "--save", str(out), "--merge"]) == 0
+        doc2 = json.loads(out.read_text())
+        assert {(e["prec"], e["op"]) for e in doc2["entries"]} <= {("z", "t"), ("z", "l")}
+        assert [e for e in doc2["entries"] if e["op"] == "t"] == doc["entries"]
 
 
 class TestBuiltinTable:
