@@ -451,9 +451,11 @@ cudaError_t run_gemv_n(const Path<T> &pa, long long lda, int m, int n, const T *
   // fused epilogue (the last CTA of a row block reduces it) when few CTAs
   // share a row block; otherwise a separate, parallel epilogue kernel
   const bool fused = maxslots <= kFuseMaxSlots;
-  if (t_k.gsplit == 3 && V > 1) {
+  if (t_k.gsplit == 3) {
     cudaError_t err = cudaSuccess;
-    if (dispatch_gemv_ro<T, V>(t_k.rocfg, pa, lda, m, n, x, cm, y, alpha, beta, beta_zero, st, &err)) return err;
+    if (V > 1 && dispatch_gemv_ro<T, V>(t_k.rocfg, pa, lda, m, n, x, cm, y, alpha, beta, beta_zero, st, &err))
+      return err;
+    t_k.gsplit = -1;  // too few rows (or unaligned ld): the built-in rule picks among the other forms
   }
   {
     // small / short matrices: the split form keeps the row blocks narrow so

@@ -261,6 +261,24 @@ class TestTableDrivesDispatch:
             assert plan.startswith(prefix), (form, plan)
             _close(y, y0, tag, n)
 
+    def test_rowown_declined_falls_back_to_rules(self, clean_table):
+        """A short, wide matrix keyed into a row-owning range has too few
+        row blocks for it: the call runs what the built-in rules pick."""
+        import torch
+
+        import paper_1410_1726_b200 as kb
+
+        m, n = 64, 65536
+        A = torch.empty(n, m, dtype=torch.float64, device="cuda").uniform_(-1, 1)
+        v = kb.view_of(A.T)
+        x = torch.empty(n, dtype=torch.float64, device="cuda").uniform_(-1, 1)
+        y = torch.zeros(m, dtype=torch.float64, device="cuda")
+        r0 = kb.gemv("n", 1.0, v, x, 0.0, y)
+        tuner.set_entry(tuner.TableEntry("d", "n", 1000, 5000, 11, 3, 0))  # key sqrt(64*65536) = 2048
+        r1 = kb.gemv("n", 1.0, v, x, 0.0, y)
+        assert r1.plan == r0.plan and not r1.plan.startswith("gemv_ro")
+        assert torch.equal(r0.y_out, r1.y_out)
+
     def test_setter_wins_over_table(self, clean_table):
         n = 3000
         run = _gemv_call("d", "n", n)
