@@ -466,7 +466,10 @@ int kblas_set_gemv_cluster(int mode);
 /* operation op whose order key lies in [n_lo, n_hi] run with the given  */
 /* choices; the key is round(sqrt(m*n)) for GEMV and d for SYMV/HEMV.   */
 /* Single-GPU calls only; an explicit kblas_set_* value wins over the    */
-/* table, the table over the built-in rules.  The latest matching entry  */
+/* table, the table over the built-in rules.  A table form is a          */
+/* preference: it is skipped (built-in rule) when the call's shape       */
+/* gives too few CTAs for it, e.g. a short, wide matrix whose order key  */
+/* falls into a row-owning range.  The latest matching entry             */
 /* wins; an entry with the same (prec, op, n_lo, n_hi) is replaced.      */
 /* The library starts with its built-in measured table (kblas_tune_defaults). */
 /*   op 'n': shape 0 auto | 3 (4 warps x 4 cols x 2 vectors, 2 CTAs/SM)  */

@@ -314,12 +314,14 @@ Knobs resolve_knobs(char op, long long key) {
       if (k.gvariant == 0 && e.shape > 0) k.gvariant = e.shape;
       if (op == 'n') {
         if (k.gsplit == -1 && k.gcluster == -1 && e.form >= 0) {
-          k.gsplit = e.form >= 1 ? 1 : 0;
-          k.gcluster = e.form == 2 ? 1 : (e.form == 1 ? 0 : -1);
+          // 2 = preferred by the table: taken when the grid still covers
+          // the GPU (the shape guards below), unlike an explicit setter
+          k.gsplit = e.form >= 1 ? 2 : 0;
+          k.gcluster = e.form == 2 ? 2 : (e.form == 1 ? 0 : -1);
         }
         if (k.gwaves == 1 && e.waves > 0) k.gwaves = e.waves;
       } else if (k.gtc == -1 && e.form >= 0) {
-        k.gtc = e.form ? 1 : 0;
+        k.gtc = e.form ? 2 : 0;
       }
     }
     break;
@@ -476,13 +478,14 @@ cudaError_t run_gemv_n(const Path<T> &pa, long long lda, int m, int n, const T *
     const double eff = (double)Pg / (double)(cdiv(Pg, Ps) * Ps);
     const bool large_ok = S <= 2 && eff >= 0.85 && fills;
     const bool half_fills = 2 * nrb_s * S >= dev_sms();  // small calls are latency-bound anyway
-    if (t_k.gsplit == 1 || (t_k.gsplit == -1 && ((!fused && half_fills && small) || large_ok))) {
+    if (t_k.gsplit == 1 || (t_k.gsplit == 2 && half_fills) ||
+        (t_k.gsplit == -1 && ((!fused && half_fills && small) || large_ok))) {
       // the CTAs of a row block as one cluster, reduced through DSMEM
       // (cluster sizes 2..16; 16 is the opt-in non-portable maximum)
       int Sc = 1;
       while (Sc < 16 && Sc < S) Sc *= 2;
       const bool cl_ok = S > 1 && n / Sc >= NWs * CWs && 4 * nrb_s * Sc >= dev_sms();
-      if (t_k.gcluster == 1 || (t_k.gcluster == -1 && cl_ok && small))
+      if (t_k.gcluster == 1 || (t_k.gcluster == 2 && cl_ok) || (t_k.gcluster == -1 && cl_ok && small))
         return run_gemv_nc<T, V, NWs, CWs>(pa, lda, m, n, x, cm, y, alpha, beta, beta_zero, st, Sc, nrb_s);
       return run_gemv_ns<T, V, NWs, CWs>(pa, lda, m, n, x, cm, y, alpha, beta, beta_zero, st, S, nrb_s);
     }
@@ -553,7 +556,7 @@ cudaError_t run_gemv_t(const Path<T> &pa, long long lda, int m, int n, long long
     const bool enough = Pc >= dev_sms() / 2;
     const bool small = (long long)m * n * (long long)sizeof(T) <= g_gemv_tc_max_bytes;
     const bool any_size = (sizeof(T) == 16 || (sizeof(T) == 8 && !is_cplx<T>())) && eff >= 0.8;
-    if (t_k.gtc == 1 || (t_k.gtc == -1 && enough && (small || any_size)))
+    if (t_k.gtc == 1 || (enough && (t_k.gtc == 2 || (t_k.gtc == -1 && (small || any_size)))))
       return run_gemv_tc<T, V, 8, CBc, CONJ>(pa, lda, m, n, nglob, x, cm, y, alpha, beta, beta_zero, st);
   }
   constexpr int H = 32 * V * R, CBW = NW * CW;
