@@ -9,8 +9,8 @@ points on the current torch stream.
 from __future__ import annotations
 
 import ctypes
+import sys
 import threading
-import weakref
 
 import numpy as np
 import torch
@@ -205,36 +205,43 @@ def host_vectors(x, y, inplace: bool) -> bool:
 
 
 class _PinnedResults:
-    """Page-locked result buffers for the numpy-vector path, recycled when
-    the numpy array handed to the caller (and every view of it) is
-    released.  torch's caching host allocator records and polls a CUDA
-    event per block (~14 us per allocation once earlier results are still
-    alive); no event is needed here, because kblas_mv_hostvec has
-    synchronised its stream before the array is returned, so the GPU no
-    longer touches a buffer the caller can see or release."""
+    """Page-locked result buffers for the numpy-vector path, reused once
+    the numpy array handed to the caller (and every view of it) has been
+    released, which the array's reference count shows.  torch's caching
+    host allocator records and polls a CUDA event per block (~14 us per
+    allocation once earlier results are still alive); no event is needed
+    here, because kblas_mv_hostvec has synchronised its stream before the
+    array is returned, so the GPU no longer touches a buffer the caller can
+    see or release."""
 
-    KEEP = 4  # free buffers kept per (dtype, length)
+    KEEP = 8  # tracked buffers per (dtype, length); beyond that, untracked allocations
 
     def __init__(self):
-        self._free: dict = {}
+        self._bufs: dict = {}
         self._lock = threading.Lock()
+        # reference count of an array held only by its pool entry, measured
+        # the way get() measures it (interpreter-version independent)
+        probe = [(None, np.zeros(1))]
+        self._free_refs = min(self._refs(e) for e in probe)
+
+    @staticmethod
+    def _refs(entry) -> int:
+        return sys.getrefcount(entry[1])
 
     def get(self, n: int, dtype: torch.dtype):
         key = (dtype, n)
         with self._lock:
-            lst = self._free.get(key)
-            t = lst.pop() if lst else None
-        if t is None:
+            lst = self._bufs.setdefault(key, [])
+            for entry in lst:
+                if self._refs(entry) <= self._free_refs:
+                    # a new tuple: it holds the array (count above free)
+                    # before the lock is released
+                    return entry[0], entry[1]
             t = torch.empty(n, dtype=dtype, pin_memory=True)
-        arr = t.numpy()
-        weakref.finalize(arr, self._release, key, t)
-        return t, arr
-
-    def _release(self, key, t):
-        with self._lock:
-            lst = self._free.setdefault(key, [])
+            entry = (t, t.numpy())
             if len(lst) < self.KEEP:
-                lst.append(t)
+                lst.append(entry)
+            return entry[0], entry[1]
 
 
 _PINNED = _PinnedResults()
