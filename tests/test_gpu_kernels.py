@@ -654,6 +654,20 @@ class TestHostVectorPath:
         check(rep.y_out, want, tag, 0.5, np.abs(naive.dense_from_triangle(tri, uplo, herm)), x, 2.0, y)
         assert rep.flops > 0 and rep.plan.startswith("symv")
 
+    @pytest.mark.parametrize("tag", "dz")
+    def test_gemv_numpy_vectors_tuned_forms(self, tag):
+        """numpy x/y at orders where the built-in table selects the
+        row-owning GEMV-N kernel (y written straight into the page-locked
+        result) and the cluster split form."""
+        rng = np.random.default_rng(155)
+        for n in (2048, 4096):
+            v, a = dev_matrix(rng, n, n, tag)
+            for beta in (0.0, 0.75):
+                x, y = naive.fill(rng, n, tag), naive.fill(rng, n, tag)
+                rep = kb.gemv("n", 1.25, v, x, beta, y)
+                assert rep.plan.startswith(("gemv_ro", "gemv_nc", "gemv_ns", "gemv_n ")), rep.plan
+                check(rep.y_out, naive.naive_gemv("n", 1.25, a, x, beta, y), tag, 1.25, np.abs(a), x, beta, y)
+
     def test_result_buffers_fresh_and_recycled(self):
         """Results own their memory while alive (no aliasing between calls)
         and the page-locked buffer is reused once a result is released."""
