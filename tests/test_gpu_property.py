@@ -9,7 +9,7 @@ simulator)."""
 import numpy as np
 import pytest
 import torch
-from hypothesis import HealthCheck, given, settings
+from hypothesis import HealthCheck, example, given, settings
 from hypothesis import strategies as st
 
 import paper_1410_1726_b200 as kb
@@ -18,7 +18,7 @@ from paper_1410_1726_b200 import _lib
 
 pytestmark = pytest.mark.gpu
 
-SETTINGS = settings(max_examples=40, deadline=None, derandomize=True,
+SETTINGS = settings(max_examples=150, deadline=None, derandomize=True,
                     suppress_health_check=[HealthCheck.too_slow, HealthCheck.function_scoped_fixture])
 
 
@@ -42,6 +42,10 @@ def _bound(tag, alpha, dense_abs, x, beta, y):
        form=st.sampled_from(["rules", "rowown", "split", "stacked"]),
        alpha=st.sampled_from([1.0, -0.5, 2.25]), beta=st.sampled_from([0.0, 1.0, -0.75]),
        seed=st.integers(0, 2 ** 16))
+@example(tag="z", m=4100, n=2049, pad=7, ro=3, co=1, trans="n", form="rowown", alpha=-0.5, beta=1.0, seed=1)
+@example(tag="s", m=5000, n=3000, pad=0, ro=0, co=0, trans="n", form="rules", alpha=1.0, beta=0.0, seed=2)
+@example(tag="d", m=3000, n=4999, pad=33, ro=5, co=2, trans="c", form="rules", alpha=2.25, beta=-0.75, seed=3)
+@example(tag="c", m=2048, n=2048, pad=0, ro=0, co=0, trans="n", form="split", alpha=1.0, beta=1.0, seed=4)
 def test_gemv_any_form_matches_oracle(tag, m, n, pad, ro, co, trans, form, alpha, beta, seed):
     lib = _lib.load()
     rng = np.random.default_rng(seed)
@@ -65,6 +69,8 @@ def test_gemv_any_form_matches_oracle(tag, m, n, pad, ro, co, trans, form, alpha
 @given(tag=st.sampled_from("sdcz"), d=st.integers(1, 3000), pad=st.integers(0, 40), off=st.integers(0, 9),
        uplo=st.sampled_from("lu"), herm=st.booleans(), alpha=st.sampled_from([1.0, -0.5]),
        beta=st.sampled_from([0.0, 0.5]), seed=st.integers(0, 2 ** 16))
+@example(tag="z", d=3000, pad=5, off=3, uplo="l", herm=True, alpha=-0.5, beta=0.5, seed=1)
+@example(tag="s", d=2999, pad=0, off=0, uplo="u", herm=False, alpha=1.0, beta=0.0, seed=2)
 def test_symv_hemv_matches_oracle(tag, d, pad, off, uplo, herm, alpha, beta, seed):
     herm = herm and tag in "cz"
     rng = np.random.default_rng(seed)
