@@ -76,14 +76,21 @@ class Cublas:
         return rc == 0
 
 
-def measure(fn, reps, ncopies):
+def measure(fn, reps, ncopies, min_ms: float = 2.0):
     """Back-to-back calls (throughput); fn(k) uses operand copy k % ncopies so
-    the operands streamed per window exceed the L2 several times over."""
+    the operands streamed per window exceed the L2 several times over.  The
+    window is at least `min_ms` long (more calls for small operands, whose
+    single-call times are a few microseconds)."""
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     for k in range(3):
         fn(k % ncopies)
     torch.cuda.synchronize()
-    calls = max(reps, ncopies)
+    e0.record()
+    fn(0)
+    e1.record()
+    torch.cuda.synchronize()
+    one = max(e0.elapsed_time(e1), 1e-3)
+    calls = max(reps, ncopies, min(2000, int(min_ms / one) + 1))
     e0.record()
     for k in range(calls):
         fn(k % ncopies)
