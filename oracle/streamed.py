@@ -37,10 +37,21 @@ def load():
                                              ctypes.c_longlong]
         lib.oracle_symv_norm_inf.restype = ctypes.c_double
         lib.oracle_max_threads.restype = ctypes.c_int
+        u64, ll = ctypes.c_ulonglong, ctypes.c_longlong
+        lib.oracle_gemv_gen.argtypes = [ctypes.c_char, ctypes.c_char, ctypes.c_int, ctypes.c_int, u64, ll, ll, ll,
+                                        dp, vp, dp, vp, dp, dp, ctypes.c_int]
+        lib.oracle_gemv_gen.restype = ctypes.c_int
+        lib.oracle_symv_gen.argtypes = [ctypes.c_char, ctypes.c_char, ctypes.c_int, ctypes.c_int, u64, ll, ll,
+                                        dp, vp, dp, vp, dp, dp, ctypes.c_int]
+        lib.oracle_symv_gen.restype = ctypes.c_int
+        lib.oracle_gen_fill.argtypes = [ctypes.c_char, ctypes.c_int, ctypes.c_int, u64, ll, ll, ll, vp, ll,
+                                        ctypes.c_int]
+        lib.oracle_gen_fill.restype = ctypes.c_int
         _lib = lib
     return _lib
 
 
+DTYPES = {"s": np.float32, "d": np.float64, "c": np.complex64, "z": np.complex128}
 TAG = {np.dtype(np.float32): "s", np.dtype(np.float64): "d", np.dtype(np.complex64): "c",
        np.dtype(np.complex128): "z"}
 
@@ -118,3 +129,65 @@ def symv_norm_inf(uplo, a2d, hermitian=None) -> float:
 
 def max_threads() -> int:
     return int(load().oracle_max_threads())
+
+
+# ------------------------------------------------ generated operands
+# The operand is regenerated inside the C loops from a counter-based
+# generator (streamed.c header; oracle/gen.py restates it for the device),
+# so no host copy of a 28-160 GB matrix is needed.
+KEY_LIMIT = 1 << 36
+
+
+def _check_keys(tag, gen_ld, rows, cols):
+    kmax = (cols * gen_ld + rows) * (2 if tag in "cz" else 1)
+    if kmax >= KEY_LIMIT:
+        raise ValueError("generated operand too large for the 36-bit key space")
+
+
+def gemv_gen(tag, trans, m, n, seed, gen_ld, ro, co, alpha, x, beta, y, nthreads: int = 0,
+             wide_out: bool = False):
+    """naive_gemv (reference.py:39-50) on the m x n operand generated with
+    (seed, gen_ld) at offset (ro, co).  Returns (y_out, ||op(A)||_inf)."""
+    dt = DTYPES[tag]
+    trans = trans.lower()
+    if trans == "c" and tag in "sd":
+        trans = "t"
+    _check_keys(tag, gen_ld, ro + m, co + n)
+    x = np.ascontiguousarray(x, dtype=dt)
+    y = np.ascontiguousarray(y, dtype=dt)
+    ylen = m if trans == "n" else n
+    out = np.zeros(2 * ylen, dtype=np.float64)
+    norm = ctypes.c_double(0.0)
+    rc = load().oracle_gemv_gen(tag.encode(), trans.encode(), m, n, seed, gen_ld, ro, co, _wide2(alpha), _ptr(x),
+                                _wide2(beta), _ptr(y), out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                ctypes.byref(norm), nthreads)
+    assert rc == 0
+    return (out.view(np.complex128) if wide_out else _out(tag, out, dt)), norm.value
+
+
+def symv_gen(tag, uplo, n, seed, gen_ld, off, alpha, x, beta, y, hermitian=None, nthreads: int = 0,
+             wide_out: bool = False):
+    """naive_symv_hemv (reference.py:53-59) on the diagonal n x n block at
+    (off, off) of the generated operand.  Returns (y_out, ||A_dense||_inf)."""
+    dt = DTYPES[tag]
+    if hermitian is None:
+        hermitian = tag in "cz"
+    _check_keys(tag, gen_ld, off + n, off + n)
+    x = np.ascontiguousarray(x, dtype=dt)
+    y = np.ascontiguousarray(y, dtype=dt)
+    out = np.zeros(2 * n, dtype=np.float64)
+    norm = ctypes.c_double(0.0)
+    rc = load().oracle_symv_gen(tag.encode(), uplo.lower().encode(), int(bool(hermitian)), n, seed, gen_ld, off,
+                                _wide2(alpha), _ptr(x), _wide2(beta), _ptr(y),
+                                out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ctypes.byref(norm), nthreads)
+    assert rc == 0
+    return (out.view(np.complex128) if wide_out else _out(tag, out, dt)), norm.value
+
+
+def gen_fill(tag, m, n, seed, gen_ld, ro=0, co=0, nthreads: int = 0):
+    """The generated m x n operand at (ro, co), materialised (Fortran order)."""
+    _check_keys(tag, gen_ld, ro + m, co + n)
+    out = np.zeros((n, m), dtype=DTYPES[tag])  # row j = column j
+    rc = load().oracle_gen_fill(tag.encode(), m, n, seed, gen_ld, ro, co, _ptr(out), m, nthreads)
+    assert rc == 0
+    return out.T

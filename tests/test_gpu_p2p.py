@@ -1,7 +1,9 @@
 """The peer-memory exchange of the one-process-per-GPU mgpu path
-(dist.P2PExchange / p2p_mv): world size 2 on one B200 (two processes,
-gloo for the one-time IPC handle exchange; the data path is CUDA IPC
-peer stores plus device flags, no NCCL).  Several calls in a row check the
+(dist.P2PExchange / p2p_mv): world size 2, rank r on cuda:(r % #GPUs) —
+two processes on one B200 here, two GPUs (cross-device IPC mapping,
+NVLink stores, system-scope flags) on a multi-GPU box.  gloo carries the
+one-time IPC handle exchange; the data path is CUDA IPC peer stores plus
+device flags, no NCCL.  Several calls in a row check the
 slot reuse handshake; rank 0's result must match the single-GPU API."""
 
 import os
@@ -27,27 +29,27 @@ def _free_port():
 def _worker(rank, world, port, kind, op, tag, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    torch.cuda.set_device(0)
+    dev = torch.device("cuda", rank % torch.cuda.device_count())
+    torch.cuda.set_device(dev)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     import paper_1410_1726_b200 as kb
+    from oracle import gen
     from paper_1410_1726_b200.dist import P2PExchange, p2p_mv
 
     prec = kb.precision(tag)
     n, nb = 1000, 64
-    g = torch.Generator(device="cuda").manual_seed(3)
-    A = torch.empty(n, n, dtype=prec.torch_dtype, device="cuda")
-    (torch.view_as_real(A) if A.is_complex() else A).uniform_(-1, 1, generator=g)
+    # identical operands on every rank's device (counter-based generator)
+    A = torch.empty(n, n, dtype=prec.torch_dtype, device=dev)
+    gen.fill_columns(A, tag, 3, n, n)
     full = kb.view_of(A.T)  # column-major n x n
-    dist_mat = kb.distribute(full, nb, world, devices=["cuda:0"] * world)
+    dist_mat = kb.distribute(full, nb, world, devices=[dev] * world)
     panel = dist_mat.local_views[rank]
     herm = kind == "s" and prec.is_complex
     ex = P2PExchange(n, prec.torch_dtype)
     errs = []
     for it in range(4):
-        x = torch.empty(n, dtype=prec.torch_dtype, device="cuda")
-        (torch.view_as_real(x) if x.is_complex() else x).uniform_(-1, 1, generator=g)
-        y = torch.empty(n, dtype=prec.torch_dtype, device="cuda")
-        (torch.view_as_real(y) if y.is_complex() else y).uniform_(-1, 1, generator=g)
+        x = gen.vector_torch(tag, n, 10 + it, dev)
+        y = gen.vector_torch(tag, n, 20 + it, dev)
         beta = 0.0 if it % 2 == 0 else -0.5
         res = p2p_mv(prec, kind, op, n, n, 0.75, panel, x, beta, y, nb, ex, hermitian=herm)
         if rank == 0:

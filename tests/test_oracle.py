@@ -167,3 +167,79 @@ def test_streamed_unreferenced_triangle_never_read():
         got = streamed.symv(uplo, 1.0, poisoned, x, 0.0, y)
         assert np.all(np.isfinite(got))
         assert naive.max_abs_error(got, naive.naive_symv_hemv(1.0, clean, uplo, x, 0.0, y)) <= 1e-12
+
+
+# ------------------------------------------------ generated operands
+# oracle/gen.py + streamed.c's generated source: the large-N parity tests
+# (tests/test_gpu_baseline_configs.py) never copy the operand to the host;
+# both sides regenerate it from (seed, row, column).  Pin that the three
+# restatements agree bit for bit and that the generated-source oracle is
+# the memory-source oracle (pinned above against blockmv) on the same data.
+from oracle import gen  # noqa: E402
+
+
+@pytest.mark.parametrize("tag", "sdcz")
+def test_generator_numpy_c_torch_bit_identical(tag):
+    import torch
+
+    for (m, n, gld, ro, co) in [(37, 23, 100, 3, 7), (64, 64, 64, 0, 0), (5, 200, 1 << 17, 99, 1 << 16)]:
+        a_np = gen.matrix_np(tag, m, n, 5, gld, ro, co)
+        a_c = streamed.gen_fill(tag, m, n, 5, gld, ro, co)
+        t = torch.empty(n, m + 3, dtype=getattr(torch, gen.DT[tag]))
+        gen.fill_columns(t, tag, 5, gld, m, 0, ro, co)
+        a_t = t[:, :m].numpy().T
+        assert a_np.dtype == a_c.dtype == a_t.dtype == naive.DTYPES[tag]
+        assert np.array_equal(a_np, a_c) and np.array_equal(a_np, a_t)
+    v = gen.vector_np(tag, 1000, 3)
+    assert np.array_equal(v, gen.vector_torch(tag, 1000, 3, "cpu").numpy())
+    assert np.all(np.abs(v.real) <= 1.0) and abs(float(np.mean(v.real))) < 0.1
+
+
+def test_generator_triangle_poison():
+    import torch
+
+    t = torch.empty(8, 8, dtype=torch.float64)
+    gen.fill_columns(t, "d", 1, 8, 8, tri="l")
+    a = t.numpy().T  # a[i, c]
+    assert np.all(np.isnan(a[np.triu_indices(8, 1)])) and not np.any(np.isnan(a[np.tril_indices(8)]))
+    # a block of columns written on its own equals the same columns of the whole
+    part = torch.empty(3, 8, dtype=torch.float64)
+    gen.fill_columns(part, "d", 1, 8, 8, col0=4, tri="l")
+    assert np.array_equal(part.numpy(), t.numpy()[4:7], equal_nan=True)
+
+
+@pytest.mark.parametrize("tag", "sdcz")
+def test_generated_oracle_equals_memory_oracle(tag):
+    n, seed = 257, 9
+    for off in (0, 13):
+        a = streamed.gen_fill(tag, n, n, seed, n + off, off, off)
+        x, y = gen.vector_np(tag, n, 10), gen.vector_np(tag, n, 11)
+        for uplo in "lu":
+            want = streamed.symv(uplo, 0.5, a, x, 0.25, y, nthreads=1)
+            got, norm = streamed.symv_gen(tag, uplo, n, seed, n + off, off, 0.5, x, 0.25, y, nthreads=1)
+            assert np.array_equal(got, want)
+            assert norm == pytest.approx(streamed.symv_norm_inf(uplo, a), rel=1e-12)
+            ref = naive.naive_symv_hemv(0.5, a, uplo, x, 0.25, y)
+            dense = np.abs(naive.dense_from_triangle(a, uplo, tag in "cz"))
+            assert naive.max_abs_error(got, ref) <= naive.run_bound(tag, 0.5, dense, x, 0.25, y)
+        for trans in "ntc":
+            want = streamed.gemv(trans, -1.5, a, x, 0.25, y, nthreads=1)
+            got, norm = streamed.gemv_gen(tag, trans, n, n, seed, n + off, off, off, -1.5, x, 0.25, y, nthreads=1)
+            assert np.array_equal(got, want)
+            aw = np.abs(naive.wide(a))
+            opa = aw if trans == "n" else aw.T
+            assert norm == pytest.approx(float(np.max(opa.sum(axis=1))), rel=1e-12)
+
+
+def test_generated_oracle_rectangular_offsets():
+    """gemv_gen on an offset window equals the memory oracle on the same
+    window of the materialised parent (configs[3] shape family)."""
+    N, i, j = 300, 7, 3
+    parent = streamed.gen_fill("z", N, N, 4, N)
+    sub = parent[i:, j:]
+    x_n, x_t = gen.vector_np("z", N - j, 1), gen.vector_np("z", N - i, 1)
+    y_n, y_t = gen.vector_np("z", N - i, 2), gen.vector_np("z", N - j, 2)
+    for trans, x, y in (("n", x_n, y_n), ("t", x_t, y_t), ("c", x_t, y_t)):
+        want = streamed.gemv(trans, 1.0, sub, x, 0.5, y, nthreads=1)
+        got, _ = streamed.gemv_gen("z", trans, N - i, N - j, 4, N, i, j, 1.0, x, 0.5, y, nthreads=1)
+        assert np.array_equal(got, want)
