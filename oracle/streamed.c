@@ -21,7 +21,7 @@
  *     k = (j + co) * gen_ld + (i + ro)        real types,
  *     re = u(2k), im = u(2k + 1)              complex types,
  * rounded to float for s / c.  Every step is exact in IEEE double, so the
- * tests' torch restatement (tests/genmat.py) produces bit-identical device
+ * tests' torch restatement (oracle/gen.py) produces bit-identical device
  * operands; the value depends only on (seed, global row, global column),
  * not on the block-column layout, so mgpu panels regenerate per block
  * column j from (seed, j).
@@ -319,6 +319,31 @@ int oracle_gen_fill(char p, int m, int n, unsigned long long seed, long long gen
     for (int i = 0; i < m; ++i) {
       double re, im;
       gen_elem(p, seed, ((long long)j + co) * gen_ld + (i + ro), &re, &im);
+      const long long k = (long long)j * ld_out + i;
+      switch (p) {
+        case 's': ((float *)out)[k] = (float)re; break;
+        case 'd': ((double *)out)[k] = re; break;
+        case 'c': ((float *)out)[2 * k] = (float)re; ((float *)out)[2 * k + 1] = (float)im; break;
+        default: ((double *)out)[2 * k] = re; ((double *)out)[2 * k + 1] = im; break;
+      }
+    }
+  }
+  return 0;
+}
+
+/* Only the stored triangle ('l': i >= j, 'u': i <= j) of the generated
+ * n x n operand, into a column-major buffer: the other triangle is never
+ * touched (the bench's host operand for N = 100000 backs only those pages). */
+int oracle_gen_fill_tri(char p, char uplo, int n, unsigned long long seed, long long gen_ld, void *out,
+                        long long ld_out, int nthreads) {
+  const int nt = nthreads_of(nthreads);
+  const int lower = uplo == 'l';
+#pragma omp parallel for schedule(dynamic, 64) num_threads(nt)
+  for (int j = 0; j < n; ++j) {
+    const int i0 = lower ? j : 0, i1 = lower ? n : j + 1;
+    for (int i = i0; i < i1; ++i) {
+      double re, im;
+      gen_elem(p, seed, (long long)j * gen_ld + i, &re, &im);
       const long long k = (long long)j * ld_out + i;
       switch (p) {
         case 's': ((float *)out)[k] = (float)re; break;

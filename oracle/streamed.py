@@ -47,6 +47,8 @@ def load():
         lib.oracle_gen_fill.argtypes = [ctypes.c_char, ctypes.c_int, ctypes.c_int, u64, ll, ll, ll, vp, ll,
                                         ctypes.c_int]
         lib.oracle_gen_fill.restype = ctypes.c_int
+        lib.oracle_gen_fill_tri.argtypes = [ctypes.c_char, ctypes.c_char, ctypes.c_int, u64, ll, vp, ll, ctypes.c_int]
+        lib.oracle_gen_fill_tri.restype = ctypes.c_int
         _lib = lib
     return _lib
 
