@@ -776,7 +776,7 @@ def single_block(res, hbm_peak, peak_src, workload):
            "pct_of_copy_peak": round(100 * res["gbs"] / hbm_peak, 2),
            "gflops": round(res["nflops"] / (res["ms_step"] * 1e-3) / 1e9, 2),
            "roofline": roofline_of(res["nbytes"], res["kern_avg_ms"], hbm_peak, peak_src,
-                                   res["plan"].split()[0] + "_kernel", f"{res['opname']}_{res['n']}"),
+                                   "kblas_" + res["plan"].split()[0] + "_kernel", f"{res['opname']}_{res['n']}"),
            "gpu_launches": res["launches"], "plan": res["plan"],
            "l2": ("inputs > 126 MB L2 (A streamed from HBM every step), no flush" if res["ncopies"] == 1 else
                   f"{res['ncopies']} rotating copies of A (>= 512 MB together, > 4x the L2)")}
@@ -836,7 +836,7 @@ def run_northstar(args, dev, rank, world, hbm_peak, peak_src):
             "pct_of_copy_peak": round(100 * res["gbs"] / (hbm_peak * world), 2),
             "gflops": round(alg_flops("d", "symv", n, n, "l") / (res["ms_step"] * 1e-3) / 1e9, 2),
             "roofline": roofline_of(res["per_rank"]["kernel_bytes"][kr], kern, hbm_peak, peak_src,
-                                    "symv_kernel", f"mgpu_dsymv_{n}_G{world}"),
+                                    "kblas_symv_kernel", f"mgpu_dsymv_{n}_G{world}"),
             "clocks": res["clocks"],
             "gpu_launches": res["launches"],
             "plan": res["plan"],
@@ -860,7 +860,7 @@ def run_northstar(args, dev, rank, world, hbm_peak, peak_src):
                     "value": round(zres["gbs"], 2), "unit": "GB/s", "ms_per_step": round(zres["ms_step"], 5),
                     "exchange": zres["exchange"], "per_rank": zres["per_rank"], "plan": zres["plan"],
                     "roofline": roofline_of(zres["per_rank"]["kernel_bytes"][zr], zk, hbm_peak, peak_src,
-                                            "symv_kernel", f"mgpu_zhemv_{n}_G{world}"),
+                                            "kblas_symv_kernel", f"mgpu_zhemv_{n}_G{world}"),
                     "e2e": zres.get("e2e")}
         elif rank == 0:
             line["zhemv_100k"] = {"skipped": f"needs {need / 2**30:.0f} GiB of HBM per GPU"}
@@ -930,7 +930,7 @@ def main():
                     "config": {"workload": f"mgpu {args.op} N={n} nb={args.nb} over {world} GPU(s), {args.reduce}",
                                "n": n, "nb": args.nb},
                     "roofline": roofline_of(res["per_rank"]["kernel_bytes"][kr], kern, hbm_peak, peak_src,
-                                            "symv_kernel", f"mgpu_{args.op}_{n}_G{world}"),
+                                            "kblas_symv_kernel", f"mgpu_{args.op}_{n}_G{world}"),
                     "clocks": res["clocks"], "gpu_launches": res["launches"], "plan": res["plan"],
                     "exchange": res["exchange"], "per_rank": res["per_rank"], "e2e": res.get("e2e")}
             print(json.dumps(line), flush=True)

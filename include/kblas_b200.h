@@ -437,7 +437,7 @@ int kblas_set_symv_variant(int variant);
 /* Select the GEMV-N form: -1 (default) = automatic (the split form,   */
 /* narrow row blocks reduced inside one kernel, for small and short    */
 /* matrices; the stacked-rows stream-K form otherwise), 1 = always the */
-/* split form, 0 = never, 3 = the row-owning form (gemv_ro_kernel).     */
+/* split form, 0 = never, 3 = the row-owning form (kblas_gemv_ro_kernel).     */
 /* Returns the previous mode.                                          */
 int kblas_set_gemv_split(int mode);
 /* Row-owning GEMV-N configuration 0..7 (tuning hook; -1 = from the     */

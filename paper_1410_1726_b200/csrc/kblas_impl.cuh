@@ -240,14 +240,14 @@ template <class T> struct Cfg {
 };
 
 // ============================================================= knobs
-// Split-form GEMV-N (gemv_ns_kernel) choice: -1 auto, 0 never, 1 always
+// Split-form GEMV-N (kblas_gemv_ns_kernel) choice: -1 auto, 0 never, 1 always
 // (kblas_set_gemv_split, for the tuner).
 inline int g_gemv_split = -1;
 inline int g_gemv_variant = 0;  // 0: tuned default shape (kblas_set_gemv_variant)
 inline int g_split_waves = 1;   // split-form GEMV-N: CTAs per row block sized for this many waves
-// cluster split form (gemv_nc_kernel): -1 auto, 0 never, 1 always
+// cluster split form (kblas_gemv_nc_kernel): -1 auto, 0 never, 1 always
 inline int g_gemv_cluster = -1;
-// column-owning form (gemv_tc_kernel) choice: -1 auto, 0 never, 1 always
+// column-owning form (kblas_gemv_tc_kernel) choice: -1 auto, 0 never, 1 always
 inline int g_gemv_tc = -1;
 inline int g_symv_variant = -1;  // -1: per-precision default variant
 inline int g_gemv_ro_cfg = -1;   // row-owning GEMV-N configuration (kblas_set_gemv_rowown; -1: from the table)
@@ -336,7 +336,7 @@ template <class T, int V, int NW, int CW>
 cudaError_t run_gemv_ns(const Path<T> &pa, long long lda, int m, int n, const T *x, ColMap cm, T *y, T alpha,
                         T beta, bool beta_zero, cudaStream_t st, long long S, long long nrb) {
   constexpr int RB = 32 * V;
-  auto kfn = gemv_ns_kernel<T, V, NW, CW>;
+  auto kfn = kblas_gemv_ns_kernel<T, V, NW, CW>;
   void *ws = nullptr;
   cudaError_t e = workspace(align256((size_t)S * m * sizeof(T)), st, &ws);
   if (e != cudaSuccess) return e;
@@ -360,7 +360,7 @@ template <class T, int V, int NW, int CW>
 cudaError_t run_gemv_nc(const Path<T> &pa, long long lda, int m, int n, const T *x, ColMap cm, T *y, T alpha,
                         T beta, bool beta_zero, cudaStream_t st, int S, long long nrb) {
   constexpr int RB = 32 * V;
-  auto kfn = gemv_nc_kernel<T, V, NW, CW>;
+  auto kfn = kblas_gemv_nc_kernel<T, V, NW, CW>;
   {
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
@@ -408,7 +408,7 @@ bool run_gemv_ro(const Path<T> &pa, long long lda, int m, int n, const T *x, Col
                y, nullptr, widen(alpha), widen(beta), beta_zero ? 1 : 0, (long long)m};
   {
     TimedScope ts(st);
-    gemv_ro_kernel<T, V, NW, LR, U><<<(unsigned)P, NW * 32, 0, st>>>(p);
+    kblas_gemv_ro_kernel<T, V, NW, LR, U><<<(unsigned)P, NW * 32, 0, st>>>(p);
   }
   launched(1);
   char buf[256];
@@ -443,7 +443,7 @@ template <class T, int V, int NW, int CW, int R, int MINB = 2>
 cudaError_t run_gemv_n(const Path<T> &pa, long long lda, int m, int n, const T *x, ColMap cm, T *y,
                        T alpha, T beta, bool beta_zero, cudaStream_t st) {
   constexpr int RB = NW * 32 * V * R;
-  auto kfn = gemv_n_kernel<T, V, NW, CW, R, MINB>;
+  auto kfn = kblas_gemv_n_kernel<T, V, NW, CW, R, MINB>;
   const long long nrb = cdiv((long long)pa.lead + m, RB);
   const long long KS = cdiv(n, CW);
   const long long total = nrb * KS;
@@ -464,7 +464,7 @@ cudaError_t run_gemv_n(const Path<T> &pa, long long lda, int m, int n, const T *
     // few CTAs share one, and reduces them in the same kernel
     constexpr int NWs = 8, CWs = 4, RBs = 32 * V;
     const long long nrb_s = cdiv((long long)pa.lead + m, RBs);
-    const long long Ps = (long long)dev_sms() * occupancy((const void *)gemv_ns_kernel<T, V, NWs, CWs>, NWs * 32);
+    const long long Ps = (long long)dev_sms() * occupancy((const void *)kblas_gemv_ns_kernel<T, V, NWs, CWs>, NWs * 32);
     const long long S = std::max<long long>(1, std::min<long long>({cdiv((long long)t_k.gwaves * Ps, nrb_s),
                                                                      kSplitMaxSlots,
                                                                      std::max<long long>(1, n / (NWs * CWs))}));
@@ -503,7 +503,7 @@ cudaError_t run_gemv_n(const Path<T> &pa, long long lda, int m, int n, const T *
   }
   launched(1);
   if (!fused) {
-    launch_pdl(gemv_n_epilogue<T, 8>, (unsigned)cdiv(m, 32), 256, st, y, (const T *)ws, (long long)m, m, pa.lead,
+    launch_pdl(kblas_gemv_n_epilogue<T, 8>, (unsigned)cdiv(m, 32), 256, st, y, (const T *)ws, (long long)m, m, pa.lead,
                (int)RB, (int)KS, total, (int)P, alpha, beta, (int)beta_zero);
     launched(1);
   }
@@ -520,7 +520,7 @@ inline long long g_gemv_tc_max_bytes = 80LL << 20;
 template <class T, int V, int NW, int CB, bool CONJ>
 cudaError_t run_gemv_tc(const Path<T> &pa, long long lda, int m, int n, long long nglob, const T *x, ColMap cm,
                         T *y, T alpha, T beta, bool beta_zero, cudaStream_t st) {
-  auto kfn = gemv_tc_kernel<T, V, NW, CB, CONJ>;
+  auto kfn = kblas_gemv_tc_kernel<T, V, NW, CB, CONJ>;
   if (cm.G > 1) {
     // mgpu partial: columns this GPU does not own stay zero
     cudaError_t e = cudaMemsetAsync(y, 0, (size_t)nglob * sizeof(T), st);
@@ -560,7 +560,7 @@ cudaError_t run_gemv_t(const Path<T> &pa, long long lda, int m, int n, long long
       return run_gemv_tc<T, V, 8, CBc, CONJ>(pa, lda, m, n, nglob, x, cm, y, alpha, beta, beta_zero, st);
   }
   constexpr int H = 32 * V * R, CBW = NW * CW;
-  auto kfn = gemv_t_kernel<T, V, NW, CW, R, CONJ, MINB>;
+  auto kfn = kblas_gemv_t_kernel<T, V, NW, CW, R, CONJ, MINB>;
   const long long ncb = cdiv(n, CBW);
   const long long KS = cdiv((long long)pa.lead + m, H);
   const long long total = ncb * KS;
@@ -588,7 +588,7 @@ cudaError_t run_gemv_t(const Path<T> &pa, long long lda, int m, int n, long long
   }
   launched(1);
   if (!fused) {
-    launch_pdl(gemv_t_epilogue<T, 8>, (unsigned)cdiv(nglob, 32), 256, st, y, (const T *)ws, ws_ld, nglob, (int)CBW,
+    launch_pdl(kblas_gemv_t_epilogue<T, 8>, (unsigned)cdiv(nglob, 32), 256, st, y, (const T *)ws, ws_ld, nglob, (int)CBW,
                (int)KS, total, (int)P, cm, alpha, beta, (int)beta_zero);
     launched(1);
   }
@@ -692,7 +692,7 @@ cudaError_t run_symv(const Path<T> &pa, long long lda, int d, const T *x, ColMap
                      T alpha, T beta, bool beta_zero, cudaStream_t st) {
   constexpr int H = 32 * V * R, W = NW * CW;
   constexpr size_t smem = 2 * (size_t)NW * H * sizeof(T);
-  auto kfn = symv_kernel<T, V, NW, CW, R, LOWER, HERM, MINB, XS>;
+  auto kfn = kblas_symv_kernel<T, V, NW, CW, R, LOWER, HERM, MINB, XS>;
   {
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
@@ -706,7 +706,7 @@ cudaError_t run_symv(const Path<T> &pa, long long lda, int d, const T *x, ColMap
   cudaError_t e = tile_table(d, pa.lead, LOWER, W, H, cm, ncols_local, Pmax, &tt);
   if (e != cudaSuccess) return e;
   if (tt.ntiles == 0 || tt.total == 0) {  // idle GPU: partial is zero
-    scal_kernel<T><<<(unsigned)cdiv(d, 256), 256, 0, st>>>(y, d, zero<T>(), 1);
+    kblas_scal_kernel<T><<<(unsigned)cdiv(d, 256), 256, 0, st>>>(y, d, zero<T>(), 1);
     launched();
     return cudaGetLastError();
   }
@@ -722,7 +722,7 @@ cudaError_t run_symv(const Path<T> &pa, long long lda, int d, const T *x, ColMap
     TimedScope ts(st);
     kfn<<<(unsigned)P, NW * 32, smem, st>>>(p);
   }
-  launch_pdl(symv_epilogue<T, LOWER, 16>, (unsigned)cdiv(d, 32), 512, st, y, p, alpha, beta, (int)beta_zero,
+  launch_pdl(kblas_symv_epilogue<T, LOWER, 16>, (unsigned)cdiv(d, 32), 512, st, y, p, alpha, beta, (int)beta_zero,
              cm.xg ? *cm.xg : kb::Xchg{});
   launched(2);
   char buf[256];
@@ -783,7 +783,7 @@ cudaError_t run_symv_tma(const T *A00, long long lda, int d, const T *x, ColMap 
   constexpr int HS = Stage<T, RS>::HS, W = NC * CW;
   constexpr size_t smem = symv_tma_smem<T, NC, CW, RS, S>();
   static_assert(smem <= 227 * 1024, "shared memory budget");
-  auto kfn = symv_tma_kernel<T, NC, CW, RS, S, LOWER, HERM>;
+  auto kfn = kblas_symv_tma_kernel<T, NC, CW, RS, S, LOWER, HERM>;
   {
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
@@ -812,7 +812,7 @@ cudaError_t run_symv_tma(const T *A00, long long lda, int d, const T *x, ColMap 
   cudaError_t e = tile_table(d, lead, LOWER, W, HS, cm, ncols_local, Pmax, &tt);
   if (e != cudaSuccess) return e;
   if (tt.ntiles == 0 || tt.total == 0) {
-    scal_kernel<T><<<(unsigned)cdiv(d, 256), 256, 0, st>>>(y, d, zero<T>(), 1);
+    kblas_scal_kernel<T><<<(unsigned)cdiv(d, 256), 256, 0, st>>>(y, d, zero<T>(), 1);
     launched();
     return cudaGetLastError();
   }
@@ -830,7 +830,7 @@ cudaError_t run_symv_tma(const T *A00, long long lda, int d, const T *x, ColMap 
     TimedScope ts(st);
     kfn<<<(unsigned)P, (NC + 2) * 32, smem, st>>>(map, tp);
   }
-  launch_pdl(symv_epilogue<T, LOWER, 16>, (unsigned)cdiv(d, 32), 512, st, y, tp.sp, alpha, beta,
+  launch_pdl(kblas_symv_epilogue<T, LOWER, 16>, (unsigned)cdiv(d, 32), 512, st, y, tp.sp, alpha, beta,
              (int)beta_zero, cm.xg ? *cm.xg : kb::Xchg{});
   launched(2);
   char buf[256];
@@ -958,7 +958,7 @@ inline int code(cudaError_t e) { return e == cudaSuccess ? 0 : (int)e; }
 
 template <class T>
 int scal_only(T *y, long long len, T beta, cudaStream_t st) {
-  scal_kernel<T><<<(unsigned)cdiv(len, 256), 256, 0, st>>>(y, len, beta, is_zero(beta) ? 1 : 0);
+  kblas_scal_kernel<T><<<(unsigned)cdiv(len, 256), 256, 0, st>>>(y, len, beta, is_zero(beta) ? 1 : 0);
   launched();
   g_last_plan = std::string("scal ") + tname<T>();
   return code(cudaGetLastError());
@@ -1117,7 +1117,7 @@ int mgpu_entry(bool is_gemv, char op, bool herm, int m, int n, T alpha, T *const
       parts.p[g] = slot;
     }
   }
-  mgpu_combine_kernel<T><<<(unsigned)cdiv(ylen, 256), 256, 0, rst>>>(dy[0], parts, ngpus, ylen, beta,
+  kblas_mgpu_combine_kernel<T><<<(unsigned)cdiv(ylen, 256), 256, 0, rst>>>(dy[0], parts, ngpus, ylen, beta,
                                                                      is_zero(beta) ? 1 : 0);
   launched();
   e = cudaGetLastError();
@@ -1244,12 +1244,12 @@ int partial_p2p(bool is_gemv, char op, bool herm, int m, int n, T alpha, const T
   }
   // general path: wait for the slot, partial into it, signal; root combines
   if (g != 0 && seq > 1) {
-    p2p_wait_kernel<<<1, 32, 0, st>>>(consumed, seq - 1);
+    kblas_p2p_wait_kernel<<<1, 32, 0, st>>>(consumed, seq - 1);
     launched();
   }
   int rc = partial_entry<T>(is_gemv, op, herm, m, n, alpha, dA, lda, dx, slots + (long long)g * slot_ld, G, g, nb, st);
   if (rc) return rc;
-  p2p_signal_kernel<<<1, 32, 0, st>>>(flags + g, seq);
+  kblas_p2p_signal_kernel<<<1, 32, 0, st>>>(flags + g, seq);
   launched();
   if (g != 0) return code(cudaGetLastError());
   if (!is_zero(beta) && y_out != y_in) {
@@ -1257,7 +1257,7 @@ int partial_p2p(bool is_gemv, char op, bool herm, int m, int n, T alpha, const T
     if (e != cudaSuccess) return (int)e;
   }
   const unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>(cdiv(plen, 256), 4LL * dev_sms()));
-  p2p_combine_kernel<T><<<grid, 256, 0, st>>>(slots, slot_ld, G, flags, seq, y_out, plen, beta, is_zero(beta) ? 1 : 0,
+  kblas_p2p_combine_kernel<T><<<grid, 256, 0, st>>>(slots, slot_ld, G, flags, seq, y_out, plen, beta, is_zero(beta) ? 1 : 0,
                                               consumed, counter);
   launched();
   return code(cudaGetLastError());

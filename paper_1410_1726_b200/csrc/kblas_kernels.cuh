@@ -3,10 +3,10 @@
 // Three streaming kernels, one per product shape, each followed by a tiny
 // fixed-order epilogue that sums cross-CTA partials and applies alpha/beta:
 //
-//   gemv_n_kernel  y = A x        (reference: _gemv_accumulate transposed=False,
+//   kblas_gemv_n_kernel  y = A x        (reference: _gemv_accumulate transposed=False,
 //                                  kernels.py:149-201 via run_gemv_n 209-221)
-//   gemv_t_kernel  y = A^T x / A^H x  (run_gemv_t, kernels.py:224-236)
-//   symv_kernel    y = A x from one stored triangle; every element is read
+//   kblas_gemv_t_kernel  y = A^T x / A^H x  (run_gemv_t, kernels.py:224-236)
+//   kblas_symv_kernel    y = A x from one stored triangle; every element is read
 //                  once and used twice: t1 = A_blk x_col -> rows, and
 //                  t2 = A_blk^T|H x_row -> columns (_symv_offdiag_accumulate
 //                  kernels.py:239-284 and _diag_accumulate 316-359 fused;
@@ -147,7 +147,7 @@ __device__ __forceinline__ void cta_slot_sum(const T *ws, long long ld, long lon
 // its two half-block buffers).
 // ---------------------------------------------------------------------------
 template <class T, int V, int NW, int CW, int R, int MINB = 2>
-__global__ void __launch_bounds__(NW * 32, MINB) gemv_n_kernel(const GemvParams p) {
+__global__ void __launch_bounds__(NW * 32, MINB) kblas_gemv_n_kernel(const GemvParams p) {
   griddep_launch_dependents();
   constexpr int WR = 32 * V * R;  // rows per warp
   constexpr int RB = NW * WR;     // rows per CTA row block
@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) gemv_n_kernel(const GemvParams 
     const int nslots = sk_owner(rb_first + p.KS - 1, p.total, p.P) - first + 1;
     T *y = static_cast<T *>(p.y);
     if (p.counters == nullptr) {
-      // unfused: partial slots only, gemv_n_epilogue sums them
+      // unfused: partial slots only, kblas_gemv_n_epilogue sums them
       const long long slot = (long long)blockIdx.x - first;
 #pragma unroll
       for (int r = 0; r < R; ++r)
@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) gemv_n_kernel(const GemvParams 
 // deterministic).  Grid: (row block, split) = blockIdx.x / KS, % KS.
 // ---------------------------------------------------------------------------
 template <class T, int V, int NW, int CW>
-__global__ void __launch_bounds__(NW * 32, 2) gemv_ns_kernel(const GemvParams p) {
+__global__ void __launch_bounds__(NW * 32, 2) kblas_gemv_ns_kernel(const GemvParams p) {
   constexpr int RB = 32 * V;
   __shared__ T red[NW][RB];
   const T *__restrict__ A = static_cast<const T *>(p.A);
@@ -346,7 +346,7 @@ __global__ void __launch_bounds__(NW * 32, 2) gemv_ns_kernel(const GemvParams p)
 // work identical, which wins while the call is latency-bound.
 // ---------------------------------------------------------------------------
 template <class T, int V, int NW, int LR, int U>
-__global__ void __launch_bounds__(NW * 32) gemv_ro_kernel(const GemvParams p) {
+__global__ void __launch_bounds__(NW * 32) kblas_gemv_ro_kernel(const GemvParams p) {
   constexpr int CPI = 32 / LR, RBo = LR * V, STEP = NW * CPI;
   __shared__ T red[NW][RBo];
   const T *__restrict__ A = static_cast<const T *>(p.A);
@@ -398,14 +398,14 @@ __global__ void __launch_bounds__(NW * 32) gemv_ro_kernel(const GemvParams p) {
 // ---------------------------------------------------------------------------
 // GEMV-N split form over a thread-block cluster.  The S CTAs sharing a
 // 32*V-row block form one cluster (S = cluster size, up to 16): each CTA
-// reduces its warps in shared memory as gemv_ns_kernel does, then the
+// reduces its warps in shared memory as kblas_gemv_ns_kernel does, then the
 // cluster exchanges the S partial row blocks through distributed shared
 // memory (CTA rank r sums rows [r*RB/S, (r+1)*RB/S) over ranks 0..S-1 in
 // order and writes y).  No global slots, fences or atomics: the cross-CTA
 // step is two cluster barriers and on-chip DSMEM reads.
 // ---------------------------------------------------------------------------
 template <class T, int V, int NW, int CW>
-__global__ void __launch_bounds__(NW * 32, 2) gemv_nc_kernel(const GemvParams p) {
+__global__ void __launch_bounds__(NW * 32, 2) kblas_gemv_nc_kernel(const GemvParams p) {
   namespace cg = cooperative_groups;
   constexpr int RB = 32 * V;
   __shared__ T red[NW][RB];
@@ -484,7 +484,7 @@ __global__ void __launch_bounds__(NW * 32, 2) gemv_nc_kernel(const GemvParams p)
 // parent's neighbouring rows (possibly NaN) never enter a sum.
 // ---------------------------------------------------------------------------
 template <class T, int V, int NW, int CW, int R, bool CONJ, int MINB = 2>
-__global__ void __launch_bounds__(NW * 32, MINB) gemv_t_kernel(const GemvParams p) {
+__global__ void __launch_bounds__(NW * 32, MINB) kblas_gemv_t_kernel(const GemvParams p) {
   griddep_launch_dependents();
   constexpr int H = 32 * V * R;
   constexpr int CBW = NW * CW;
@@ -604,11 +604,11 @@ __global__ void __launch_bounds__(NW * 32, MINB) gemv_t_kernel(const GemvParams 
 // H-row chunks round robin (register double buffered), reduce each column
 // across lanes with shuffles and across warps through shared memory in
 // fixed order, and write y.  No cross-CTA partials, no fences, no second
-// kernel: the split-K reduction tail of gemv_t_kernel is what bounds a
+// kernel: the split-K reduction tail of kblas_gemv_t_kernel is what bounds a
 // small call (ncu: SMs active ~54 % of a 16 us N = 2048 call).
 // ---------------------------------------------------------------------------
 template <class T, int V, int NW, int CB, bool CONJ>
-__global__ void __launch_bounds__(NW * 32, 2) gemv_tc_kernel(const GemvParams p) {
+__global__ void __launch_bounds__(NW * 32, 2) kblas_gemv_tc_kernel(const GemvParams p) {
   constexpr int H = 32 * V;
   __shared__ T part[NW][CB];
   const T *__restrict__ x = static_cast<const T *>(p.x);
@@ -736,7 +736,7 @@ __device__ __forceinline__ int sym_start_tile(const SymParams &p, long long) {
 // slots, so no extra barrier) instead of CW registers per thread, which
 // frees registers for wider per-warp column sets.
 template <class T, int V, int NW, int CW, int R, bool LOWER, bool HERM, int MINB = 1, bool XS = false>
-__global__ void __launch_bounds__(NW * 32, MINB) symv_kernel(const SymParams p) {
+__global__ void __launch_bounds__(NW * 32, MINB) kblas_symv_kernel(const SymParams p) {
   griddep_launch_dependents();
   constexpr int NT = NW * 32;
   constexpr int H = 32 * V * R;
@@ -948,7 +948,7 @@ __device__ __forceinline__ T slot_sum(const T *__restrict__ ws, long long ws_ld,
 }
 
 template <class T, int EW>
-__global__ void __launch_bounds__(EW * 32) gemv_n_epilogue(T *y, const T *__restrict__ ws, long long ws_ld, int m,
+__global__ void __launch_bounds__(EW * 32) kblas_gemv_n_epilogue(T *y, const T *__restrict__ ws, long long ws_ld, int m,
                                                           int lead, int RB, int KS, long long total, int P,
                                                           T alpha, T beta, int beta_zero) {
   griddep_wait();
@@ -967,7 +967,7 @@ __global__ void __launch_bounds__(EW * 32) gemv_n_epilogue(T *y, const T *__rest
 // y indexed by global column c in [0, nglob); columns not owned by this GPU
 // (mgpu partial mode) are written as zero.
 template <class T, int EW>
-__global__ void __launch_bounds__(EW * 32) gemv_t_epilogue(T *y, const T *__restrict__ ws, long long ws_ld,
+__global__ void __launch_bounds__(EW * 32) kblas_gemv_t_epilogue(T *y, const T *__restrict__ ws, long long ws_ld,
                                                           long long nglob, int CBW, int KS, long long total, int P,
                                                           ColMap cm, T alpha, T beta, int beta_zero) {
   griddep_wait();
@@ -1010,7 +1010,7 @@ struct Xchg {
 };
 
 template <class T, bool LOWER, int EW>
-__global__ void __launch_bounds__(EW * 32) symv_epilogue(T *y, const SymParams p, T alpha, T beta, int beta_zero,
+__global__ void __launch_bounds__(EW * 32) kblas_symv_epilogue(T *y, const SymParams p, T alpha, T beta, int beta_zero,
                                                          const Xchg xg) {
   griddep_wait();
   if (xg.G > 0 && xg.rank != 0 && xg.seq > 1) {
@@ -1115,7 +1115,7 @@ __global__ void __launch_bounds__(EW * 32) symv_epilogue(T *y, const SymParams p
 
 // y <- beta * y (beta == 0: zero fill); run_scal semantics (kernels.py:127-146)
 template <class T>
-__global__ void scal_kernel(T *y, long long n, T beta, int beta_zero) {
+__global__ void kblas_scal_kernel(T *y, long long n, T beta, int beta_zero) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   y[i] = beta_zero ? zero<T>() : mul_(beta, y[i]);
@@ -1127,7 +1127,7 @@ __global__ void scal_kernel(T *y, long long n, T beta, int beta_zero) {
 constexpr int kMaxGpus = 16;
 template <class T> struct PartList { const T *p[kMaxGpus]; };
 template <class T>
-__global__ void mgpu_combine_kernel(T *y, PartList<T> parts, int G, long long n, T beta, int beta_zero) {
+__global__ void kblas_mgpu_combine_kernel(T *y, PartList<T> parts, int G, long long n, T beta, int beta_zero) {
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   T s = parts.p[0][i];
@@ -1148,7 +1148,7 @@ __global__ void mgpu_combine_kernel(T *y, PartList<T> parts, int G, long long n,
 // ---------------------------------------------------------------------------
 // rank side: its partial (written by the preceding kernels on this stream)
 // becomes visible system-wide, then flags[rank] = seq
-static __global__ void p2p_signal_kernel(unsigned long long *flag, unsigned long long seq) {
+static __global__ void kblas_p2p_signal_kernel(unsigned long long *flag, unsigned long long seq) {
   if (threadIdx.x == 0) {
     __threadfence_system();
     st_release_sys(flag, seq);
@@ -1156,13 +1156,13 @@ static __global__ void p2p_signal_kernel(unsigned long long *flag, unsigned long
 }
 
 // wait until *flag >= seq (e.g. the root has consumed the previous call)
-static __global__ void p2p_wait_kernel(const unsigned long long *flag, unsigned long long seq) {
+static __global__ void kblas_p2p_wait_kernel(const unsigned long long *flag, unsigned long long seq) {
   if (threadIdx.x == 0) spin_until(flag, seq);
   __syncthreads();
 }
 
 template <class T>
-__global__ void p2p_combine_kernel(const T *__restrict__ slots, long long slot_ld, int G,
+__global__ void kblas_p2p_combine_kernel(const T *__restrict__ slots, long long slot_ld, int G,
                                    const unsigned long long *flags, unsigned long long seq, T *y, long long n,
                                    T beta, int beta_zero, unsigned long long *consumed, unsigned *counter) {
   if (threadIdx.x == 0) {

@@ -193,14 +193,14 @@ int kblas_ipc_close(void *dptr) { return code(cudaIpcCloseMemHandle(dptr)); }
 
 int kblas_p2p_signal_async(unsigned long long *flag, unsigned long long seq, cudaStream_t stream) {
   if (flag == nullptr) return -1;
-  p2p_signal_kernel<<<1, 32, 0, stream>>>(flag, seq);
+  kblas_p2p_signal_kernel<<<1, 32, 0, stream>>>(flag, seq);
   launched();
   return code(cudaGetLastError());
 }
 
 int kblas_p2p_wait_async(const unsigned long long *flag, unsigned long long seq, cudaStream_t stream) {
   if (flag == nullptr) return -1;
-  p2p_wait_kernel<<<1, 32, 0, stream>>>(flag, seq);
+  kblas_p2p_wait_kernel<<<1, 32, 0, stream>>>(flag, seq);
   launched();
   return code(cudaGetLastError());
 }
@@ -241,7 +241,7 @@ int kblas_p2p_combine_async(char prec, int nranks, const void *slots, long long 
 #define KB_P2P(CH, T)                                                                                         \
   case CH: {                                                                                                  \
     const T b = *static_cast<const T *>(beta);                                                                \
-    p2p_combine_kernel<T><<<grid, 256, 0, stream>>>(static_cast<const T *>(slots), slot_ld, nranks, flags, seq, \
+    kblas_p2p_combine_kernel<T><<<grid, 256, 0, stream>>>(static_cast<const T *>(slots), slot_ld, nranks, flags, seq, \
                                                     static_cast<T *>(y), n, b, is_zero(b) ? 1 : 0, consumed,      \
                                                     counter);                                                 \
     break;                                                                                                    \

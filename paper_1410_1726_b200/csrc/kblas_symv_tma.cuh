@@ -1,6 +1,6 @@
 // kblas_symv_tma.cuh — SYMV / HEMV streaming kernel fed by TMA.
 //
-// Same tiling and stream-K item split as symv_kernel (kblas_kernels.cuh):
+// Same tiling and stream-K item split as kblas_symv_kernel (kblas_kernels.cuh):
 // a tile is W = NC*CW stored columns with all their stored rows, an item
 // is one HS-row chunk of a tile.  What changes is how bytes reach the
 // FMAs.  Instead of each warp loading its own columns into registers (the
@@ -13,7 +13,7 @@
 //   warps 0..NC-1  consumers: wait full[s], read their CW columns of the
 //                  box from shared memory (conflict-free, 8/16 B per lane),
 //                  form t1 (row sums, A x_col) and t2 (column sums, op(A)
-//                  x_row) exactly as symv_kernel, drop the t1 partial into
+//                  x_row) exactly as kblas_symv_kernel, drop the t1 partial into
 //                  red[s][warp], arrive redfull[s] and empty[s]
 //   warp NC        producer: waits empty[s], arms full[s] with the box
 //                  byte count and issues the TMA for the next item
@@ -61,7 +61,7 @@ struct SymTmaParams {
 
 template <class T, int NC, int CW, int RS, int S, bool LOWER, bool HERM>
 __global__ void __launch_bounds__((NC + 2) * 32, 1)
-    symv_tma_kernel(const __grid_constant__ CUtensorMap tmap, const SymTmaParams tp) {
+    kblas_symv_tma_kernel(const __grid_constant__ CUtensorMap tmap, const SymTmaParams tp) {
   griddep_launch_dependents();
   constexpr int VE = Stage<T, RS>::VE;
   constexpr int HS = Stage<T, RS>::HS;
