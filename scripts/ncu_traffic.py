@@ -136,7 +136,7 @@ def run():
             partial_mv(p, "s", "l", n, n, 1.0, v, x, out, 1, 0, nb, herm)
 
         emit(f"mgpu_{'dsymv' if tag == 'd' else 'zhemv'}_{n}_G1", fn, roofline.symv_bytes(p, n))
-        del A, v
+        del A, v, fn, x, out
         torch.cuda.empty_cache()
 
 
@@ -155,7 +155,7 @@ def parse(csv_path, seq_path):
             order.append(lid)
         val = float(str(r["Metric Value"]).replace(",", ""))
         unit = r.get("Metric Unit", "")
-        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "ns": 1e-9, "usecond": 1e-6, "us": 1e-6, "ms": 1e-3,
                  "msecond": 1e-3, "second": 1}.get(unit, 1)
         launches[lid][r["Metric Name"]] = val * scale
     seq = [json.loads(line) for line in open(seq_path) if line.strip().startswith("{")]
