@@ -506,6 +506,16 @@ int kblas_set_symv_narrow(int max_order);
 /* and up to max_order use 8-warp CTAs at 2 per SM.  Returns the        */
 /* previous threshold (default 12288).                                  */
 int kblas_set_symv_mid(int max_order);
+/* Register and TMA SYMV/HEMV kernels: work schedule.  items > 0 deals   */
+/* segments of `items` consecutive row chunks to the CTAs round robin   */
+/* (neighbouring CTAs stream neighbouring chunks of the same tiles);    */
+/* items <= 0 gives each CTA one contiguous range (stream-K).  Returns  */
+/* the previous value (default 6).                                      */
+int kblas_set_symv_segment(int items);
+/* Register SYMV/HEMV kernel (orders above the mid threshold): row      */
+/* chunks per CTA barrier window (1, 2 or 4; the warps' t1 partials of  */
+/* a window are reduced together).  Returns the previous value (2).      */
+int kblas_set_symv_window(int items);
 /* Description of the last plan chosen for a call on this thread      */
 /* (kernel family, grid, items, workspace bytes) as a NUL-terminated   */
 /* string; for reports and tests.                                      */

@@ -184,6 +184,10 @@ def load():
         lib.kblas_set_gemv_split.restype = c_int
         lib.kblas_set_symv_mid.argtypes = [c_int]
         lib.kblas_set_symv_mid.restype = c_int
+        lib.kblas_set_symv_window.argtypes = [c_int]
+        lib.kblas_set_symv_window.restype = c_int
+        lib.kblas_set_symv_segment.argtypes = [c_int]
+        lib.kblas_set_symv_segment.restype = c_int
         lib.kblas_set_symv_narrow.argtypes = [c_int]
         lib.kblas_set_symv_narrow.restype = c_int
         LL = ctypes.c_longlong
@@ -267,6 +271,18 @@ def set_gemv_split(mode) -> int:
     Returns the previous mode."""
     m = -1 if mode == -1 else (1 if mode else 0)
     return int(load().kblas_set_gemv_split(m))
+
+
+def set_symv_window(items: int) -> int:
+    """Register SYMV/HEMV kernel: row chunks per CTA barrier window (1, 2
+    or 4).  Returns the previous value."""
+    return int(load().kblas_set_symv_window(int(items)))
+
+
+def set_symv_segment(items: int) -> int:
+    """SYMV/HEMV schedule: segments of `items` row chunks round robin over
+    the CTAs (<= 0: contiguous stream-K).  Returns the previous value."""
+    return int(load().kblas_set_symv_segment(int(items)))
 
 
 def set_symv_narrow(max_order: int) -> int:

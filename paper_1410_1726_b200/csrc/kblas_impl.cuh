@@ -603,22 +603,34 @@ cudaError_t run_gemv_t(const Path<T> &pa, long long lda, int m, int n, long long
 // ============================================================= SYMV/HEMV
 struct TileTable {
   SymTile *dev = nullptr;
-  int *start = nullptr;  // per CTA (of min(P, total)): tile holding its first item
+  int *seg_tile = nullptr;  // per segment: tile of its first item
   int ntiles = 0;
   long long total = 0;
-  long long maxslots = 0;
+  int P = 1;                // CTAs the schedule was cut for (min(P, total))
+  int K = 1, rounds = 0;
+  long long base = 0, rem = 0, nseg = 0;
+  long long nslots = 0;     // ws2 slot rows (sum over tiles of the segments touching them)
 };
 inline std::map<std::vector<long long>, TileTable> g_tiles;
+
+// SYMV segment length K (items dealt round robin per CTA, see SymParams);
+// <= 0: contiguous stream-K.  kblas_set_symv_segment.
+inline int g_symv_seg = 6;
+// register SYMV/HEMV (wide kernel): items per CTA barrier window, 1, 2 or
+// 4 (kblas_set_symv_window)
+inline int g_symv_window = 2;
 
 // Tiles for the local panel of GPU g under the block-cyclic layout (G=1,
 // nb=d for a single GPU): every owned block column is cut into W-wide tiles.
 // exact: chunks start at each tile's first stored row (TMA path); else on
-// the physical H-row grid (vector-load path, 32-byte granules).
+// the physical H-row grid (vector-load path, 32-byte granules).  The item
+// schedule (segments of K items round robin over P CTAs, then a
+// contiguous tail) and each tile's ws2 slot rows are fixed here too.
 inline cudaError_t tile_table(int d, int lead, bool lower, int W, int H, ColMap cm, int ncols_local, long long P,
-                       TileTable *out, bool exact = false) {
+                              int K, TileTable *out, bool exact = false) {
   int dev = 0;
   cudaGetDevice(&dev);
-  std::vector<long long> key{dev, d, lead, lower, W, H, cm.G, cm.g, cm.nb, ncols_local, P, exact};
+  std::vector<long long> key{dev, d, lead, lower, W, H, cm.G, cm.g, cm.nb, ncols_local, P, K, exact};
   {
     std::lock_guard<std::mutex> lk(g_mu);
     auto it = g_tiles.find(key);
@@ -649,36 +661,51 @@ inline cudaError_t tile_table(int d, int lead, bool lower, int W, int H, ColMap 
     }
     l0 = (b + 1) * cm.nb;
   }
+  if (prefix >= (1LL << 31) - 1) return cudaErrorInvalidValue;  // item indices are 32-bit in the kernels
   TileTable tt;
   tt.ntiles = (int)tiles.size();
   tt.total = prefix;
   const long long Pe = std::min<long long>(P, std::max<long long>(prefix, 1));
-  tt.maxslots = 1;
+  tt.P = (int)Pe;
+  tt.K = K > 0 ? K : 1;
+  // the tail keeps >= 1 item per CTA, so no segment is empty and every
+  // slot row a tile owns is written
+  tt.rounds = K > 0 ? (int)(std::max<long long>(0, prefix - Pe) / (Pe * K)) : 0;
+  tt.base = (long long)tt.rounds * Pe * tt.K;
+  tt.rem = prefix - tt.base;
+  tt.nseg = (long long)tt.rounds * Pe + Pe;
+  auto seg_of = [&](long long q) { return sym_seg_of(q, tt.K, tt.rounds, (int)Pe, tt.base, tt.rem); };
+  auto seg_lo = [&](long long sg) { return sym_seg_lo(sg, tt.K, tt.rounds, (int)Pe, tt.base, tt.rem); };
+  long long slots = 0;
   for (size_t k = 0; k < tiles.size(); ++k) {
     const long long a = tiles[k].prefix;
     const long long bnext = (k + 1 < tiles.size()) ? tiles[k + 1].prefix : prefix;
-    if (bnext > a)
-      tt.maxslots = std::max<long long>(tt.maxslots, sk_owner(bnext - 1, prefix, Pe) - sk_owner(a, prefix, Pe) + 1);
+    tiles[k].seg0 = (int)seg_of(a);
+    tiles[k].nseg = bnext > a ? (int)(seg_of(bnext - 1) - tiles[k].seg0 + 1) : 0;
+    tiles[k].slot0 = (int)slots;
+    slots += tiles[k].nseg;
   }
+  tt.nslots = std::max<long long>(slots, 1);
   if (!tiles.empty()) {
-    // per-CTA start tiles: CTA c's first item sk_start(c) lies in the last
-    // tile whose prefix <= it (saves the kernels a binary search)
-    std::vector<int> start((size_t)Pe);
+    // per segment: the tile holding its first item (empty tail segments: 0)
+    std::vector<int> segt((size_t)tt.nseg, 0);
     size_t k = 0;
-    for (long long c = 0; c < Pe; ++c) {
-      const long long it = sk_start(c, prefix, Pe);
+    for (long long sg = 0; sg < tt.nseg; ++sg) {
+      const long long it = seg_lo(sg);
+      if (it >= prefix) continue;
       while (k + 1 < tiles.size() && tiles[k + 1].prefix <= it) ++k;
-      start[(size_t)c] = (int)k;
+      if (tiles[k].prefix > it) k = 0;
+      segt[(size_t)sg] = (int)k;
     }
     const size_t tb = align256(tiles.size() * sizeof(SymTile));
     void *mem = nullptr;
-    cudaError_t e = cudaMalloc(&mem, tb + start.size() * sizeof(int));
+    cudaError_t e = cudaMalloc(&mem, tb + segt.size() * sizeof(int));
     if (e != cudaSuccess) return e;
     tt.dev = static_cast<SymTile *>(mem);
-    tt.start = reinterpret_cast<int *>(static_cast<char *>(mem) + tb);
+    tt.seg_tile = reinterpret_cast<int *>(static_cast<char *>(mem) + tb);
     e = cudaMemcpy(tt.dev, tiles.data(), tiles.size() * sizeof(SymTile), cudaMemcpyHostToDevice);
     if (e != cudaSuccess) return e;
-    e = cudaMemcpy(tt.start, start.data(), start.size() * sizeof(int), cudaMemcpyHostToDevice);
+    e = cudaMemcpy(tt.seg_tile, segt.data(), segt.size() * sizeof(int), cudaMemcpyHostToDevice);
     if (e != cudaSuccess) return e;
   }
   std::lock_guard<std::mutex> lk(g_mu);
@@ -687,12 +714,45 @@ inline cudaError_t tile_table(int d, int lead, bool lower, int W, int H, ColMap 
   return cudaSuccess;
 }
 
-template <class T, int V, int NW, int CW, int R, bool LOWER, bool HERM, int MINB = 1, bool XS = false>
+// kernel parameters of a tile table (ws1 rows of d, ws2 slot rows of W)
+template <class T>
+SymParams sym_params(const T *A, long long lda, int d, int lead, const T *x, void *ws, int W, const TileTable &tt,
+                     bool uniform) {
+  const size_t b1 = align256((size_t)tt.ntiles * d * sizeof(T));
+  SymParams p{};
+  p.A = A;
+  p.lda = lda;
+  p.d = d;
+  p.lead = lead;
+  p.x = x;
+  p.ws1 = ws;
+  p.ws1_ld = d;
+  p.ws2 = static_cast<char *>(ws) + b1;
+  p.ws2_ld = W;
+  p.tiles = tt.dev;
+  p.ntiles = tt.ntiles;
+  p.total = tt.total;
+  p.P = tt.P;
+  p.tile_w = uniform ? W : 0;
+  p.K = tt.K;
+  p.rounds = tt.rounds;
+  p.base = tt.base;
+  p.rem = tt.rem;
+  p.nseg = tt.nseg;
+  p.seg_tile = tt.seg_tile;
+  return p;
+}
+template <class T>
+size_t sym_ws_bytes(int d, int W, const TileTable &tt) {
+  return align256((size_t)tt.ntiles * d * sizeof(T)) + align256((size_t)tt.nslots * W * sizeof(T));
+}
+
+template <class T, int V, int NW, int CW, int R, bool LOWER, bool HERM, int MINB = 1, bool XS = false, int B = 1>
 cudaError_t run_symv(const Path<T> &pa, long long lda, int d, const T *x, ColMap cm, int ncols_local, T *y,
                      T alpha, T beta, bool beta_zero, cudaStream_t st) {
   constexpr int H = 32 * V * R, W = NW * CW;
-  constexpr size_t smem = 2 * (size_t)NW * H * sizeof(T);
-  auto kfn = kblas_symv_kernel<T, V, NW, CW, R, LOWER, HERM, MINB, XS>;
+  constexpr size_t smem = 2 * (size_t)B * NW * H * sizeof(T);
+  auto kfn = kblas_symv_kernel<T, V, NW, CW, R, LOWER, HERM, MINB, XS, B>;
   {
     static std::once_flag once;
     static cudaError_t attr_err = cudaSuccess;
@@ -703,21 +763,18 @@ cudaError_t run_symv(const Path<T> &pa, long long lda, int d, const T *x, ColMap
   }
   const long long Pmax = (long long)dev_sms() * occupancy((const void *)kfn, NW * 32, smem);
   TileTable tt;
-  cudaError_t e = tile_table(d, pa.lead, LOWER, W, H, cm, ncols_local, Pmax, &tt);
+  cudaError_t e = tile_table(d, pa.lead, LOWER, W, H, cm, ncols_local, Pmax, g_symv_seg, &tt);
   if (e != cudaSuccess) return e;
   if (tt.ntiles == 0 || tt.total == 0) {  // idle GPU: partial is zero
     kblas_scal_kernel<T><<<(unsigned)cdiv(d, 256), 256, 0, st>>>(y, d, zero<T>(), 1);
     launched();
     return cudaGetLastError();
   }
-  const long long P = std::min<long long>(tt.total, Pmax);
-  const size_t b1 = align256((size_t)tt.ntiles * d * sizeof(T));
-  const size_t b2 = align256((size_t)tt.maxslots * d * sizeof(T));
+  const long long P = tt.P;
   void *ws = nullptr;
-  e = workspace(b1 + b2, st, &ws);
+  e = workspace(sym_ws_bytes<T>(d, W, tt), st, &ws);
   if (e != cudaSuccess) return e;
-  SymParams p{pa.base, lda, d, pa.lead, x, ws, (long long)d, (char *)ws + b1, (long long)d,
-              tt.dev, tt.ntiles, tt.total, (int)P, (cm.G == 1 && cm.nb >= d) ? W : 0, tt.start};
+  const SymParams p = sym_params(pa.base, lda, d, pa.lead, x, ws, W, tt, cm.G == 1 && cm.nb >= d);
   {
     TimedScope ts(st);
     kfn<<<(unsigned)P, NW * 32, smem, st>>>(p);
@@ -726,9 +783,9 @@ cudaError_t run_symv(const Path<T> &pa, long long lda, int d, const T *x, ColMap
              cm.xg ? *cm.xg : kb::Xchg{});
   launched(2);
   char buf[256];
-  snprintf(buf, sizeof buf, "symv %s %s %s%s lead=%d d=%d W=%d H=%d tiles=%d items=%lld P=%lld slots=%lld",
-           tname<T>(), V > 1 ? "v256" : "scalar", LOWER ? "L" : "U", HERM ? " herm" : "", pa.lead, d, W, H,
-           tt.ntiles, tt.total, P, tt.maxslots);
+  snprintf(buf, sizeof buf, "symv %s %s %s%s lead=%d d=%d W=%d H=%d B=%d tiles=%d items=%lld P=%lld K=%d rounds=%d slots=%lld",
+           tname<T>(), V > 1 ? "v256" : "scalar", LOWER ? "L" : "U", HERM ? " herm" : "", pa.lead, d, W, H, B,
+           tt.ntiles, tt.total, P, tt.K, tt.rounds, tt.nslots);
   g_last_plan = buf;
   return cudaGetLastError();
 }
@@ -809,22 +866,19 @@ cudaError_t run_symv_tma(const T *A00, long long lda, int d, const T *x, ColMap 
   if (cr != CUDA_SUCCESS) return cudaErrorInvalidValue;
   const long long Pmax = dev_sms();
   TileTable tt;
-  cudaError_t e = tile_table(d, lead, LOWER, W, HS, cm, ncols_local, Pmax, &tt);
+  cudaError_t e = tile_table(d, lead, LOWER, W, HS, cm, ncols_local, Pmax, g_symv_seg, &tt);
   if (e != cudaSuccess) return e;
   if (tt.ntiles == 0 || tt.total == 0) {
     kblas_scal_kernel<T><<<(unsigned)cdiv(d, 256), 256, 0, st>>>(y, d, zero<T>(), 1);
     launched();
     return cudaGetLastError();
   }
-  const long long P = std::min<long long>(tt.total, Pmax);
-  const size_t b1 = align256((size_t)tt.ntiles * d * sizeof(T));
-  const size_t b2 = align256((size_t)tt.maxslots * d * sizeof(T));
+  const long long P = tt.P;
   void *ws = nullptr;
-  e = workspace(b1 + b2, st, &ws);
+  e = workspace(sym_ws_bytes<T>(d, W, tt), st, &ws);
   if (e != cudaSuccess) return e;
   SymTmaParams tp;
-  tp.sp = SymParams{base, lda, d, lead, x, ws, (long long)d, (char *)ws + b1, (long long)d,
-                    tt.dev, tt.ntiles, tt.total, (int)P, (cm.G == 1 && cm.nb >= d) ? W : 0, tt.start};
+  tp.sp = sym_params(base, lda, d, lead, x, ws, W, tt, cm.G == 1 && cm.nb >= d);
   tp.unit_per_elem = upe;
   {
     TimedScope ts(st);
@@ -834,9 +888,9 @@ cudaError_t run_symv_tma(const T *A00, long long lda, int d, const T *x, ColMap 
              (int)beta_zero, cm.xg ? *cm.xg : kb::Xchg{});
   launched(2);
   char buf[256];
-  snprintf(buf, sizeof buf, "symv_tma %s %s%s lead=%d d=%d W=%d H=%d S=%d tiles=%d items=%lld P=%lld slots=%lld smem=%zu",
+  snprintf(buf, sizeof buf, "symv_tma %s %s%s lead=%d d=%d W=%d H=%d S=%d tiles=%d items=%lld P=%lld K=%d rounds=%d slots=%lld smem=%zu",
            tname<T>(), LOWER ? "L" : "U", HERM ? " herm" : "", lead, d, W, HS, S, tt.ntiles, tt.total, P,
-           tt.maxslots, (size_t)smem);
+           tt.K, tt.rounds, tt.nslots, (size_t)smem);
   g_last_plan = buf;
   return cudaGetLastError();
 }
@@ -937,10 +991,17 @@ cudaError_t dispatch_symv_h(bool lower, const Path<T> &pa, long long lda, int d,
                    : run_symv<T, C::V, 8, (sizeof(T) == 16 ? 4 : 8), 1, false, HERM, 2>(
                          pa, lda, d, x, cm, ncols_local, y, alpha, beta, beta_zero, st);
     default:
-      return lower ? run_symv<T, C::V, C::S_NW, C::S_CW, C::S_R, true, HERM, 1, C::S_XS>(
-                         pa, lda, d, x, cm, ncols_local, y, alpha, beta, beta_zero, st)
-                   : run_symv<T, C::V, C::S_NW, C::S_CW, C::S_R, false, HERM, 1, C::S_XS>(
-                         pa, lda, d, x, cm, ncols_local, y, alpha, beta, beta_zero, st);
+#define KB_WIDE(B)                                                                                      \
+  return lower ? run_symv<T, C::V, C::S_NW, C::S_CW, C::S_R, true, HERM, 1, C::S_XS, B>(                \
+                     pa, lda, d, x, cm, ncols_local, y, alpha, beta, beta_zero, st)                     \
+               : run_symv<T, C::V, C::S_NW, C::S_CW, C::S_R, false, HERM, 1, C::S_XS, B>(               \
+                     pa, lda, d, x, cm, ncols_local, y, alpha, beta, beta_zero, st)
+      switch (g_symv_window) {
+        case 1: KB_WIDE(1);
+        case 2: KB_WIDE(2);
+        default: KB_WIDE(4);
+      }
+#undef KB_WIDE
   }
 #undef KB_REG
 }

@@ -691,9 +691,22 @@ __global__ void __launch_bounds__(NW * 32, 2) kblas_gemv_tc_kernel(const GemvPar
 //
 // t1 for a chunk is complete after a shared-memory reduction over the warps
 // and is written to ws1[tile][row] (each (tile, row) exactly once).  t2
-// stays in registers for the tile and is written to ws2[slot][column] once
-// per (tile, CTA).  The epilogue sums ws1 over the tiles covering each row
-// and ws2 over the slots of the row's own tile, in fixed order.
+// stays in registers while a CTA walks consecutive items of one tile and
+// is written once per (tile, segment) to its own slot row of ws2.  The
+// epilogue sums ws1 over the tiles covering each row and ws2 over the slots
+// of the row's own tile, in fixed order.
+//
+// Schedule ("segments").  The T items are cut into segments of K
+// consecutive items dealt round robin to the P CTAs (segment s belongs to
+// CTA s mod P) for `rounds` full rounds; the remaining items are split into
+// P contiguous tail segments (classic stream-K), so every CTA streams the
+// same bytes to within one item.  With K small, the CTAs resident at any
+// moment stream NEIGHBOURING row chunks of the same few tiles: the DRAM
+// sees 128 columns x (P K / #tiles) KiB runs instead of 148 x 128 scattered
+// 1 KiB pages, which removes the column-stride aliasing of ld = N
+// operands (profiles/r2_stream_probe*.jsonl: 128 x 1 KiB items at ld =
+// 40960 stream at 6.83 TB/s contiguous, 7.05 TB/s interleaved with K = 4,
+// the same as with a padded ld).  rounds = 0 is contiguous stream-K.
 //
 // Tiles come from a host-built table so the same kernel serves the
 // single-GPU path, diagonal submatrices (offset API) and the local
@@ -706,6 +719,9 @@ struct SymTile {
   int row0, row1;   // stored logical rows [row0, row1)
   int chunk0;       // first physical H-row chunk
   long long prefix; // items before this tile
+  int seg0;         // segment holding the tile's first item
+  int slot0;        // first ws2 slot row of the tile (one per segment touching it)
+  int nseg;         // segments touching the tile
 };
 
 struct SymParams {
@@ -717,32 +733,102 @@ struct SymParams {
   void *ws1;
   long long ws1_ld;
   void *ws2;
-  long long ws2_ld;
+  long long ws2_ld;  // slot row width (= W)
   const SymTile *tiles;
   int ntiles;
   long long total;
   int P;
   int tile_w;  // > 0: tiles are uniform, tile k = columns [k*tile_w, (k+1)*tile_w) (single GPU)
-  const int *start_tile;  // per CTA: the tile holding its first item (host-built)
+  int K;        // items per interleaved segment
+  int rounds;   // full rounds of P interleaved segments
+  long long base, rem;  // first tail item (rounds * P * K) and tail length
+  long long nseg;       // rounds * P + P
+  const int *seg_tile;  // per segment: tile of its first item (host-built)
 };
 
-// The tile holding CTA blockIdx.x's first item: one load from the per-CTA
-// start table the host builds with the tile table.
-__device__ __forceinline__ int sym_start_tile(const SymParams &p, long long) {
-  return p.start_tile[blockIdx.x];
+// first item of segment s (s == nseg gives total)
+__host__ __device__ __forceinline__ long long sym_seg_lo(long long s, int K, int rounds, int P, long long base,
+                                                         long long rem) {
+  const long long full = (long long)rounds * P;
+  return s < full ? s * K : base + (s - full) * rem / P;
 }
+// segment holding item q
+__host__ __device__ __forceinline__ long long sym_seg_of(long long q, int K, int rounds, int P, long long base,
+                                                         long long rem) {
+  return q < base ? q / K : (long long)rounds * P + sk_owner(q - base, rem, P);
+}
+
+// Walks one CTA's items in order: segments blockIdx.x, +P, +2P, ...; k is
+// the tile of item q.  The next segment's start tile is fetched one
+// segment ahead so a segment switch does not wait on it.  Item and segment
+// indices fit in 32 bits (the host checks total < 2^31).
+struct SymCursor {
+  int s, q, hi, tnext;
+  int k, knext;
+  bool done;
+  __device__ __forceinline__ int lo_of(const SymParams &p, int seg) const {
+    return (int)sym_seg_lo(seg, p.K, p.rounds, p.P, p.base, p.rem);
+  }
+  __device__ __forceinline__ void set_tile(const SymParams &p, int kk) {
+    k = kk;
+    tnext = (k + 1 < p.ntiles) ? (int)p.tiles[k + 1].prefix : (int)p.total;
+  }
+  // first non-empty segment at or after seg (stepping by P)
+  __device__ __forceinline__ bool seek(const SymParams &p, int seg) {
+    for (; seg < p.nseg; seg += p.P) {
+      const int a = lo_of(p, seg), b = lo_of(p, seg + 1);
+      if (a < b) {
+        s = seg;
+        q = a;
+        hi = b;
+        return true;
+      }
+    }
+    done = true;
+    return false;
+  }
+  __device__ __forceinline__ bool init(const SymParams &p) {
+    done = false;
+    if (!seek(p, blockIdx.x)) return false;
+    set_tile(p, p.seg_tile[s]);
+    knext = s + p.P < p.nseg ? p.seg_tile[s + p.P] : 0;
+    return true;
+  }
+  __device__ __forceinline__ void advance(const SymParams &p) {
+    if (++q < hi) {
+      if (q >= tnext) set_tile(p, k + 1);
+      return;
+    }
+    const int prev = s;
+    if (!seek(p, s + p.P)) return;
+    set_tile(p, s == prev + p.P ? knext : p.seg_tile[s]);
+    knext = s + p.P < p.nseg ? p.seg_tile[s + p.P] : 0;
+  }
+};
+
+// t1 window record: the tile, first physical row and stored row range of
+// an item whose t1 partials wait in shared memory for the window barrier
+struct SymT1Meta { int k, p0, clo, chi; };
 
 // XS: keep the tile's x_col values in shared memory (each warp its own CW
 // slots, so no extra barrier) instead of CW registers per thread, which
 // frees registers for wider per-warp column sets.
-template <class T, int V, int NW, int CW, int R, bool LOWER, bool HERM, int MINB = 1, bool XS = false>
+// B: items per barrier window.  Each warp drops the t1 partials of B
+// consecutive items into shared memory and the CTA meets at one barrier per
+// B items, where all NT threads reduce the B x H rows in warp order; warps
+// drift freely inside a window, so one late load no longer stalls all 16
+// warps at every item (ncu: barrier stalls were ~46 % of warp samples with
+// B = 1, profiles/r2a_ncu_summary.md).
+template <class T, int V, int NW, int CW, int R, bool LOWER, bool HERM, int MINB = 1, bool XS = false, int B = 1>
 __global__ void __launch_bounds__(NW * 32, MINB) kblas_symv_kernel(const SymParams p) {
   griddep_launch_dependents();
   constexpr int NT = NW * 32;
   constexpr int H = 32 * V * R;
-  // t1 partials, double-buffered: red[buf][warp][row] (dynamic: 2*NW*H*sizeof(T))
+  // t1 partials, double-buffered windows: red[buf][item][warp][row]
+  // (dynamic: 2*B*NW*H*sizeof(T)), and the window's item records
   extern __shared__ __align__(16) unsigned char symv_smem[];
-  T(*red)[NW][H] = reinterpret_cast<T(*)[NW][H]>(symv_smem);
+  T(*red)[B][NW][H] = reinterpret_cast<T(*)[B][NW][H]>(symv_smem);
+  __shared__ SymT1Meta meta[2][B];
 
   const T *__restrict__ A = static_cast<const T *>(p.A);
   const T *__restrict__ x = static_cast<const T *>(p.x);
@@ -751,19 +837,16 @@ __global__ void __launch_bounds__(NW * 32, MINB) kblas_symv_kernel(const SymPara
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const uint64_t pol = policy_evict_first();
   const uint64_t keep = policy_evict_last();
-  const long long it0 = sk_start(blockIdx.x, p.total, p.P);
-  const long long end = sk_start(blockIdx.x + 1, p.total, p.P);
-  if (it0 >= end) return;
+  SymCursor c;
+  if (!c.init(p)) return;
   const int cl = warp * CW;
   const bool xvec = V > 1 && p.lead == 0 && (reinterpret_cast<uintptr_t>(x) % (V * sizeof(T))) == 0;
 
-  // tile holding item it0: the last tile whose prefix <= it0
-  int k = sym_start_tile(p, it0);
-
-  // Software pipeline over the CTA's items: the loads of item q+1 (possibly
-  // in the next tile) are issued right after item q's FMAs, so they are in
-  // flight while item q's t1 partial goes through shared memory, the
-  // barrier and the fixed-order cross-warp reduction.
+  // Software pipeline over the CTA's items: the loads of the next item
+  // (possibly in the next tile or segment) are issued right after this
+  // item's FMAs, so they are in flight while this item's t1 partial goes
+  // through shared memory, the barrier and the fixed-order cross-warp
+  // reduction.
   Pack<T, V> a[CW][R];
   T xr[R][V];
   auto load = [&](const SymTile &t, long long q) {
@@ -794,13 +877,13 @@ __global__ void __launch_bounds__(NW * 32, MINB) kblas_symv_kernel(const SymPara
     }
   };
 
-  SymTile tl = p.tiles[k];
-  long long tnext = (k + 1 < p.ntiles) ? p.tiles[k + 1].prefix : p.total;
+  SymTile tl = p.tiles[c.k];
   T t2[CW];
   __shared__ T xs_buf[XS ? NW * CW : 1];
   T xr_c[XS ? 1 : CW];  // x_col in registers (!XS)
   auto set_xc = [&](const SymTile &t) {
     if constexpr (XS) {
+      __syncwarp();
       if (lane < CW) xs_buf[cl + lane] = (cl + lane < t.ncols) ? __ldg(x + t.gcol0 + cl + lane) : zero<T>();
       __syncwarp();
     } else {
@@ -814,10 +897,10 @@ __global__ void __launch_bounds__(NW * 32, MINB) kblas_symv_kernel(const SymPara
   set_xc(tl);
 #pragma unroll
   for (int j = 0; j < CW; ++j) t2[j] = zero<T>();
-  load(tl, it0);
-  int buf = 0;
-  for (long long q = it0; q < end; ++q) {
-    const int p0 = (tl.chunk0 + (int)(q - tl.prefix)) * H;
+  load(tl, c.q);
+  int buf = 0, wi = 0;  // window buffer, item index inside the window
+  for (;;) {
+    const int p0 = (tl.chunk0 + (int)(c.q - tl.prefix)) * H;
     const int vlo = tl.row0 + p.lead, vhi = tl.row1 + p.lead;
     const int g0 = p0 - p.lead;  // logical row of the chunk's first physical row
     T acc[R][V];
@@ -857,7 +940,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) kblas_symv_kernel(const SymPara
     } else {
 #pragma unroll
       for (int j = 0; j < CW; ++j) {
-        const int c = tl.gcol0 + cl + j;
+        const int cc = tl.gcol0 + cl + j;
 #pragma unroll
         for (int r = 0; r < R; ++r)
 #pragma unroll
@@ -865,57 +948,61 @@ __global__ void __launch_bounds__(NW * 32, MINB) kblas_symv_kernel(const SymPara
             const int ps = p0 + r * 32 * V + lane * V + v;
             const int i = ps - p.lead;
             const bool ok = ps >= vlo && ps < vhi;
-            const bool in1 = ok && (LOWER ? i >= c : i <= c);
-            const bool in2 = ok && (LOWER ? i > c : i < c);
+            const bool in1 = ok && (LOWER ? i >= cc : i <= cc);
+            const bool in2 = ok && (LOWER ? i > cc : i < cc);
             T e1 = sel(in1, a[j][r].v(v));
-            if (HERM && i == c) e1 = realify(e1);
+            if (HERM && i == cc) e1 = realify(e1);
             acc[r][v] = fma_(e1, xcj(j), acc[r][v]);
             t2[j] = fmax_<HERM>(sel(in2, a[j][r].v(v)), xr[r][v], t2[j]);
           }
       }
     }
 
-    // tile boundary: flush this tile's column sums (t2) once
-    const bool last_of_tile = q + 1 >= tnext || q + 1 >= end;
-    if (last_of_tile) {
-      const long long slot = (long long)blockIdx.x - sk_owner(tl.prefix, p.total, p.P);
+    const int s_cur = c.s, kcur = c.k;
+    c.advance(p);
+    // end of this CTA's run through the tile (tile, segment or work ends):
+    // flush the tile's column sums (t2) into the segment's slot row
+    if (c.done || c.k != kcur || c.s != s_cur) {
+      T *row = ws2 + (long long)(tl.slot0 + (s_cur - tl.seg0)) * p.ws2_ld;
 #pragma unroll
       for (int j = 0; j < CW; ++j) {
         const T sum = warp_sum(t2[j]);
-        if (lane == 0 && cl + j < tl.ncols) ws2[slot * p.ws2_ld + tl.gcol0 + cl + j] = sum;
+        if (lane == 0 && cl + j < tl.ncols) row[cl + j] = sum;
         t2[j] = zero<T>();
       }
     }
     const SymTile cur = tl;  // the tile this chunk's t1 belongs to
-    const int kcur = k;
-    if (q + 1 < end) {
-      if (q + 1 >= tnext) {
-        ++k;
-        tl = p.tiles[k];
-        tnext = (k + 1 < p.ntiles) ? p.tiles[k + 1].prefix : p.total;
+    if (!c.done) {
+      if (c.k != kcur) {
+        tl = p.tiles[c.k];
         set_xc(tl);
       }
-      load(tl, q + 1);  // in flight during the reduction below
+      load(tl, c.q);  // in flight during the reduction below
     }
 
 #pragma unroll
     for (int r = 0; r < R; ++r)
 #pragma unroll
-      for (int v = 0; v < V; ++v) red[buf][warp][r * 32 * V + lane * V + v] = acc[r][v];
-    __syncthreads();
-    {
-      const int clo = cur.row0 + p.lead, chi = cur.row1 + p.lead;
-      for (int t = threadIdx.x; t < H; t += NT) {
-        const int ps = p0 + t;
-        if (ps >= clo && ps < chi) {
-          T s = red[buf][0][t];
+      for (int v = 0; v < V; ++v) red[buf][wi][warp][r * 32 * V + lane * V + v] = acc[r][v];
+    if (threadIdx.x == 0) meta[buf][wi] = SymT1Meta{kcur, p0, cur.row0 + p.lead, cur.row1 + p.lead};
+    if (++wi == B || c.done) {
+      __syncthreads();
+      // fixed-order (warp 0..NW-1) sum of every row of the window's items
+      for (int t = threadIdx.x; t < wi * H; t += NT) {
+        const int it = t / H, row = t - it * H;
+        const SymT1Meta m = meta[buf][it];
+        const int ps = m.p0 + row;
+        if (ps >= m.clo && ps < m.chi) {
+          T sm = red[buf][it][0][row];
 #pragma unroll
-          for (int w = 1; w < NW; ++w) s = add_(s, red[buf][w][t]);
-          st_keep(ws1 + (long long)kcur * p.ws1_ld + (ps - p.lead), s, keep);
+          for (int w = 1; w < NW; ++w) sm = add_(sm, red[buf][it][w][row]);
+          st_keep(ws1 + (long long)m.k * p.ws1_ld + (ps - p.lead), sm, keep);
         }
       }
+      buf ^= 1;
+      wi = 0;
     }
-    buf ^= 1;
+    if (c.done) break;
   }
 }
 
@@ -1036,13 +1123,9 @@ __global__ void __launch_bounds__(EW * 32) kblas_symv_epilogue(T *y, const SymPa
     }
     nle = lo;
   }
-  // the tile owning column i (if any on this GPU) and the next tile's prefix
+  // the tile owning column i (if any on this GPU)
   SymTile own{};
-  long long tnext = 0;
-  if (nle > 0) {
-    own = p.tiles[nle - 1];
-    tnext = (nle < p.ntiles) ? p.tiles[nle].prefix : p.total;
-  }
+  if (nle > 0) own = p.tiles[nle - 1];
   int kb, ke;
   if (LOWER) {
     kb = 0;
@@ -1062,10 +1145,10 @@ __global__ void __launch_bounds__(EW * 32) kblas_symv_epilogue(T *y, const SymPa
     for (int u = 0; u < 8; ++u)
       if (k + u * EW < ke) acc = add_(acc, t[u]);
   }
-  // t2: the slots of the tile owning column i
-  if (valid && nle > 0 && i < (long long)own.gcol0 + own.ncols && tnext > own.prefix) {
-    const int nsl = sk_owner(tnext - 1, p.total, p.P) - sk_owner(own.prefix, p.total, p.P) + 1;
-    for (int sl = warp; sl < nsl; sl += EW) acc = add_(acc, ws2[(long long)sl * p.ws2_ld + i]);
+  // t2: the slot rows of the tile owning column i (one per segment)
+  if (valid && nle > 0 && i < (long long)own.gcol0 + own.ncols) {
+    const T *col = ws2 + (long long)own.slot0 * p.ws2_ld + (i - own.gcol0);
+    for (int sl = warp; sl < own.nseg; sl += EW) acc = add_(acc, col[(long long)sl * p.ws2_ld]);
   }
   part[warp][lane] = acc;
   __syncthreads();

@@ -332,6 +332,18 @@ int kblas_set_symv_mid(int max_order) {
   return prev;
 }
 
+int kblas_set_symv_window(int items) {
+  const int prev = g_symv_window;
+  g_symv_window = items;
+  return prev;
+}
+
+int kblas_set_symv_segment(int items) {
+  const int prev = g_symv_seg;
+  g_symv_seg = items;
+  return prev;
+}
+
 int kblas_set_symv_narrow(int max_order) {
   const int prev = g_symv_narrow_max;
   g_symv_narrow_max = max_order;

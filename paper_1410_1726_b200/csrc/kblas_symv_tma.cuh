@@ -75,9 +75,8 @@ __global__ void __launch_bounds__((NC + 2) * 32, 1)
 
   const SymParams &p = tp.sp;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  long long it0 = sk_start(blockIdx.x, p.total, p.P);
-  const long long end = sk_start(blockIdx.x + 1, p.total, p.P);
-  if (it0 >= end) return;
+  SymCursor c0;
+  if (!c0.init(p)) return;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
@@ -90,24 +89,16 @@ __global__ void __launch_bounds__((NC + 2) * 32, 1)
   }
   __syncthreads();
 
-  // tile holding item it0
-  const int k0 = sym_start_tile(p, it0);
-
   if (warp == NC) {
     // ---------------------------------------------------------- producer
     if (lane == 0) {
-      int k = k0;
-      long long tnext = (k + 1 < p.ntiles) ? p.tiles[k + 1].prefix : p.total;
-      for (long long q = it0, qi = 0; q < end; ++q, ++qi) {
-        while (q >= tnext) {
-          ++k;
-          tnext = (k + 1 < p.ntiles) ? p.tiles[k + 1].prefix : p.total;
-        }
-        const SymTile &tl = p.tiles[k];
+      SymCursor c = c0;
+      for (long long qi = 0; !c.done; c.advance(p), ++qi) {
+        const SymTile &tl = p.tiles[c.k];
         const int s = (int)(qi % S);
         const uint32_t round = (uint32_t)(qi / S);
         if (round > 0) mbar_wait(&empty[s], (round - 1) & 1);
-        const int row = (tl.chunk0 + (int)(q - tl.prefix)) * HS;  // tensor row (lead included)
+        const int row = (tl.chunk0 + (int)(c.q - tl.prefix)) * HS;  // tensor row (lead included)
         mbar_arrive_expect_tx(&full[s], BOX_BYTES);
         tma_load_2d(boxes + (size_t)s * W * HS, &tmap, row * tp.unit_per_elem, tl.lcol0, &full[s]);
       }
@@ -119,18 +110,14 @@ __global__ void __launch_bounds__((NC + 2) * 32, 1)
   if (warp == NC + 1) {
     // ----------------------------------------------------------- reducer
     const uint64_t keep = policy_evict_last();
-    int k = k0;
-    long long tnext = (k + 1 < p.ntiles) ? p.tiles[k + 1].prefix : p.total;
-    for (long long q = it0, qi = 0; q < end; ++q, ++qi) {
-      while (q >= tnext) {
-        ++k;
-        tnext = (k + 1 < p.ntiles) ? p.tiles[k + 1].prefix : p.total;
-      }
+    SymCursor c = c0;
+    for (long long qi = 0; !c.done; c.advance(p), ++qi) {
+      const int k = c.k;
       const SymTile &tl = p.tiles[k];
       const int s = (int)(qi % S);
       mbar_wait(&redfull[s], (uint32_t)(qi / S) & 1);
       const T *rs = red + (size_t)s * NC * HS;
-      const long long r0 = (long long)(tl.chunk0 + (q - tl.prefix)) * HS - p.lead;
+      const long long r0 = (long long)(tl.chunk0 + (c.q - tl.prefix)) * HS - p.lead;
 #pragma unroll
       for (int t0 = 0; t0 < HS; t0 += 32) {
         const int t = t0 + lane;
@@ -152,19 +139,21 @@ __global__ void __launch_bounds__((NC + 2) * 32, 1)
   const T *__restrict__ x = static_cast<const T *>(p.x);
   T *__restrict__ ws2 = static_cast<T *>(p.ws2);
   const int cl = warp * CW;
-  int k = k0;
-  long long q = it0, qi = 0;
-  while (q < end) {
+  SymCursor c = c0;
+  long long qi = 0;
+  while (!c.done) {
+    // one run: consecutive items of one tile within one segment
+    const int k = c.k;
+    const long long seg = c.s;
     const SymTile tl = p.tiles[k];
-    const long long tnext = (k + 1 < p.ntiles) ? p.tiles[k + 1].prefix : p.total;
-    const long long stop = min(end, tnext);
     T xc[CW], t2[CW];
 #pragma unroll
     for (int j = 0; j < CW; ++j) {
       xc[j] = (cl + j < tl.ncols) ? __ldg(x + tl.gcol0 + cl + j) : zero<T>();
       t2[j] = zero<T>();
     }
-    for (; q < stop; ++q, ++qi) {
+    for (; !c.done && c.k == k && c.s == seg; c.advance(p), ++qi) {
+      const long long q = c.q;
       const int s = (int)(qi % S);
       // logical row of box row 0; piece (r, lane) holds rows r0 + (r*32 + lane)*VE + v
       const long long r0 = (long long)(tl.chunk0 + (q - tl.prefix)) * HS - p.lead;
@@ -239,13 +228,12 @@ __global__ void __launch_bounds__((NC + 2) * 32, 1)
         mbar_arrive(&empty[s]);
       }
     }
-    const long long slot = (long long)blockIdx.x - sk_owner(tl.prefix, p.total, p.P);
+    T *row = ws2 + (long long)(tl.slot0 + (int)(seg - tl.seg0)) * p.ws2_ld;
 #pragma unroll
     for (int j = 0; j < CW; ++j) {
       const T sum = warp_sum(t2[j]);
-      if (lane == 0 && cl + j < tl.ncols) ws2[slot * p.ws2_ld + tl.gcol0 + cl + j] = sum;
+      if (lane == 0 && cl + j < tl.ncols) row[cl + j] = sum;
     }
-    ++k;
   }
 }
 
