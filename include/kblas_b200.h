@@ -253,8 +253,10 @@ int kblas_zsymv_mgpu(char uplo, int n, cuDoubleComplex alpha, cuDoubleComplex *c
                      const int *device_ids);
 /* _async forms (every routine has one): streams[g] is */
 /* the stream on GPU g; the root's combine runs on streams[0] after     */
-/* events from the others; nothing is waited for on the host.  A       */
-/* non-NULL streams array is required (last argument index).           */
+/* events from the others, and every streams[g] then waits for the      */
+/* combine, so dy[g] may be reused by the next call at once; nothing is */
+/* waited for on the host.  A non-NULL streams array is required (last  */
+/* argument index).                                                     */
 int kblas_sgemv_mgpu_async(char trans, int m, int n, float alpha, float *const *dA, int lda,
                            float *const *dx, int incx, float beta, float *const *dy, int incy,
                            int ngpus, int nb, const int *device_ids, cudaStream_t const *streams);
@@ -303,6 +305,16 @@ int kblas_mv_mgpu_partial_async(char prec, char kind, char op, int m, int n,
                                 const void *alpha, const void *dA_local, int lda,
                                 const void *dx, void *dy_partial, int ngpus, int gpu,
                                 int nb, int hermitian, cudaStream_t stream);
+
+/* Root combine of per-GPU partials: y = beta * y + sum_g parts[g],     */
+/* summed in g order (the reference's device-order sum,                */
+/* multidevice.py:176,276, then beta, 282-283) by one kernel on the    */
+/* current device; parts[g] are length-n device vectors on this device  */
+/* or peer-accessible.  beta points to a host scalar of the precision's */
+/* type (beta == 0: y is written, not read).  For callers that reduce   */
+/* partials themselves (e.g. NCCL) and fuse beta here.                 */
+int kblas_mv_mgpu_combine_async(char prec, long long n, int nparts, const void *const *parts,
+                                const void *beta, void *y, cudaStream_t stream);
 
 /* One-process-per-GPU exchange over peer memory, replacing the host-  */
 /* side device-order sum of the partials (multidevice.py:276, 282-283)  */

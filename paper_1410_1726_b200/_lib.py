@@ -106,6 +106,9 @@ def load():
                 getattr(lib, f"kblas_{name}_mgpu_async").argtypes = (_mgpu_argtypes("symv", tag)
                                                                      + [POINTER(c_void_p)])
                 getattr(lib, f"kblas_{name}_mgpu_async").restype = c_int
+        lib.kblas_mv_mgpu_combine_async.argtypes = [c_char, ctypes.c_longlong, c_int, POINTER(c_void_p), c_void_p,
+                                                     c_void_p, c_void_p]
+        lib.kblas_mv_mgpu_combine_async.restype = c_int
         lib.kblas_mv_mgpu_partial_async.argtypes = [
             c_char, c_char, c_char, c_int, c_int, c_void_p, c_void_p, c_int, c_void_p, c_void_p,
             c_int, c_int, c_int, c_int, c_void_p,

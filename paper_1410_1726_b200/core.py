@@ -202,7 +202,12 @@ def view_of(array, prec: Precision | None = None, ld: int | None = None) -> Matr
         prec = prec or precision_of(array.dtype)
         m, n = array.shape
         ld = ld or max(array.stride(1), m)
-        flat = torch.as_strided(array, ((n - 1) * ld + m,), (1,), array.storage_offset())
+        # the reference's view covers n whole columns of ld elements
+        # (core.py:92-94); a padded column-major tensor has them whenever its
+        # storage extends past the last column's padding
+        avail = array.untyped_storage().nbytes() // array.element_size() - array.storage_offset()
+        length = n * ld if avail >= n * ld else (n - 1) * ld + m
+        flat = torch.as_strided(array, (length,), (1,), array.storage_offset())
         return MatrixView(data=flat, rows=m, cols=n, ld=ld, precision=prec)
     a = np.asfortranarray(array)
     prec = prec or precision_of(a.dtype)

@@ -127,6 +127,35 @@ inline cudaError_t workspace(size_t bytes, cudaStream_t st, void **out) {
   return cudaSuccess;
 }
 
+// One call's acquire-and-launch sequence (workspace, main kernel,
+// epilogue) must not interleave with another host thread's on the same
+// stream: the workspace is per (device, stream), so main1 main2 epi1 epi2
+// would let call 2 overwrite call 1's partials.  Every entry point holds
+// this (recursive: entries nest) lock of its (device, stream) for the
+// whole sequence; calls on different streams never contend.
+inline std::map<std::pair<int, cudaStream_t>, std::unique_ptr<std::recursive_mutex>> g_stream_mu;
+
+inline std::recursive_mutex &stream_mutex(cudaStream_t st) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  thread_local int c_dev = -1;
+  thread_local cudaStream_t c_st = nullptr;
+  thread_local std::recursive_mutex *c_mu = nullptr;
+  if (c_mu && c_dev == dev && c_st == st) return *c_mu;
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto &slot = g_stream_mu[{dev, st}];
+  if (!slot) slot = std::make_unique<std::recursive_mutex>();
+  c_dev = dev;
+  c_st = st;
+  c_mu = slot.get();
+  return *c_mu;
+}
+
+struct StreamLock {
+  std::unique_lock<std::recursive_mutex> lk;
+  explicit StreamLock(cudaStream_t st) : lk(stream_mutex(st)) {}
+};
+
 // Arrival counters for the fused GEMV epilogue: one per row/column block,
 // zero between calls (the finishing CTA resets its counter), zeroed when
 // (re)allocated.  Cached per (device, stream) like the workspace.
@@ -1044,6 +1073,7 @@ int gemv_entry(char trans, int m, int n, T alpha, const T *dA, int lda, const T 
     return scal_only(dy, ylen, beta, st);
   }
   if (is_zero(alpha) && is_one(beta)) return 0;  // quick return (kernels.py:427-428)
+  StreamLock slk(st);
   if (is_zero(alpha)) return scal_only(dy, ylen, beta, st);  // kernels.py:431-432
   const T *A = dA + (long long)offset_c * lda + offset_r;
   Path<T> pa;
@@ -1064,6 +1094,7 @@ int symv_entry(char uplo, bool herm, int n, T alpha, const T *dA, int lda, const
   if (incy != 1) return -10;
   if (n == 0) return 0;
   if (is_zero(alpha) && is_one(beta)) return 0;
+  StreamLock slk(st);
   if (is_zero(alpha)) return scal_only(dy, n, beta, st);
   const T *A = dA + (long long)offset * lda + offset;
   Path<T> pa;
@@ -1092,6 +1123,7 @@ int partial_entry(bool is_gemv, char op, bool herm, int m, int n, T alpha, const
                   T *dpart, int G, int g, int nb, cudaStream_t st) {
   const long long lc = local_cols(n, nb, G, g);
   const long long plen = is_gemv ? ((op == 'n') ? m : n) : n;
+  StreamLock slk(st);
   if (lc == 0 || is_zero(alpha)) return scal_only(dpart, plen, zero<T>(), st);
   Path<T> pa;
   if (make_path(dA, lda, &pa) != 0) return -5;
@@ -1129,6 +1161,7 @@ int mgpu_entry(bool is_gemv, char op, bool herm, int m, int n, T alpha, T *const
   }
   // root's own partial lives in a workspace slot (dy[0] holds the input y)
   cudaSetDevice(root);
+  StreamLock rlk(rst);
   void *rootbuf = nullptr;
   // separate from the kernel workspace: allocated once per (device, root stream)
   {
@@ -1182,9 +1215,41 @@ int mgpu_entry(bool is_gemv, char op, bool herm, int m, int n, T alpha, T *const
                                                                      is_zero(beta) ? 1 : 0);
   launched();
   e = cudaGetLastError();
+  if (e == cudaSuccess && !sync) {
+    // the next call's partial on GPU g (g > 0) overwrites dy[g]: make each
+    // GPU's stream wait until this combine has read it (no WAR race when a
+    // caller reuses dy across _async calls)
+    cudaEvent_t combined = nullptr;
+    e = cudaEventCreateWithFlags(&combined, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventRecord(combined, rst);
+    for (int g = 1; g < ngpus && e == cudaSuccess; ++g) {
+      if (stof(g) == rst) continue;
+      cudaSetDevice(devof(g));
+      e = cudaStreamWaitEvent(stof(g), combined, 0);
+    }
+    if (combined) cudaEventDestroy(combined);
+  }
   if (e == cudaSuccess && sync) e = cudaStreamSynchronize(rst);
   for (auto ev : done) if (ev) cudaEventDestroy(ev);  // released once complete
   return code(e);
+}
+
+// y = beta * y + sum_g parts[g] in device order on the current device
+// (parts on this device or peer-accessible): the root combine of the
+// single-process mgpu API after an NCCL reduce (multidevice.py:276,
+// 282-283)
+template <class T>
+int combine_entry(long long n, int nparts, const void *const *parts, T beta, T *y, cudaStream_t st) {
+  if (n < 0 || nparts < 1 || nparts > kMaxGpus || parts == nullptr || y == nullptr) return -1;
+  if (n == 0) return 0;
+  PartList<T> pl{};
+  for (int g = 0; g < nparts; ++g) {
+    if (parts[g] == nullptr) return -3;
+    pl.p[g] = static_cast<const T *>(parts[g]);
+  }
+  kblas_mgpu_combine_kernel<T><<<(unsigned)cdiv(n, 256), 256, 0, st>>>(y, pl, nparts, n, beta, is_zero(beta) ? 1 : 0);
+  launched();
+  return code(cudaGetLastError());
 }
 
 // per-GPU panels of the 1D block-column-cyclic layout
@@ -1246,6 +1311,7 @@ int hostvec_entry(bool is_gemv, char op, bool herm, int m, int n, T alpha, const
   if (xlen < 0 || ylen < 0 || hx == nullptr || hy_out == nullptr) return -1;
   const bool bz = is_zero(beta);
   if (!bz && hy_in == nullptr) return -1;
+  StreamLock slk(st);
   void *stage = nullptr;
   const size_t xb = align256((size_t)std::max<long long>(xlen, 1) * sizeof(T));
   cudaError_t e = vec_staging(xb + (size_t)std::max<long long>(ylen, 1) * sizeof(T), st, &stage);
@@ -1286,6 +1352,7 @@ int partial_p2p(bool is_gemv, char op, bool herm, int m, int n, T alpha, const T
                        const T *y_in, T *y_out, cudaStream_t st) {
   const long long plen = is_gemv ? ((op == 'n') ? m : n) : n;
   if (slot_ld < plen) return -1;
+  StreamLock slk(st);
   const bool fused = !is_gemv && local_cols(n, nb, G, g) > 0 && !is_zero(alpha);
   if (fused) {
     // the exchange rides in the SYMV epilogue: one launch pair per call

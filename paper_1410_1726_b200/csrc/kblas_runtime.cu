@@ -56,6 +56,18 @@ int kblas_mv_mgpu_partial_async(char prec, char kind, char op, int m, int n, con
   return -1;
 }
 
+int kblas_mv_mgpu_combine_async(char prec, long long n, int nparts, const void *const *parts, const void *beta,
+                                void *y, cudaStream_t stream) {
+  if (beta == nullptr) return -5;
+  switch (prec | 0x20) {
+    case 's': return combine_entry<float>(n, nparts, parts, *(const float *)beta, (float *)y, stream);
+    case 'd': return combine_entry<double>(n, nparts, parts, *(const double *)beta, (double *)y, stream);
+    case 'c': return combine_entry<float2>(n, nparts, parts, *(const float2 *)beta, (float2 *)y, stream);
+    case 'z': return combine_entry<double2>(n, nparts, parts, *(const double2 *)beta, (double2 *)y, stream);
+  }
+  return -1;
+}
+
 int kblas_mgpu_local_cols(int n, int nb, int ngpus, int gpu) {
   if (n < 0 || nb < 1 || ngpus < 1 || gpu < 0 || gpu >= ngpus) return -1;
   return (int)local_cols(n, nb, ngpus, gpu);

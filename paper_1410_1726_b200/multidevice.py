@@ -3,17 +3,22 @@
 Layout: block column j of width nb lives on GPU j mod G,
 packed contiguously into that GPU's local panel whose ld is the row count
 padded to 32 elements (multidevice.py:72-93).  Each GPU runs the same
-sm_100a kernels on its panel through `kblas_mv_mgpu_partial_async`: a
-column map turns local columns into global ones, so GEMV-N and SYMV/HEMV
-produce a full-length partial y and GEMV-T produces its own disjoint
-segments (zeros elsewhere).  Partials are then combined on the root GPU:
+sm_100a kernels on its panel: a column map turns local columns into
+global ones, so GEMV-N and SYMV/HEMV produce a full-length partial y and
+GEMV-T produces its own disjoint segments (zeros elsewhere).  Partials are
+then combined on the root GPU, by library kernels only:
 
-  reduce="ordered" (default): partials are pulled to the root over NVLink
-      (peer copies) and summed in device order by one fused kernel with
-      beta*y, matching multidevice.py:161,176,276,282-283 bit-for-bit in
-      summation order, so results are deterministic;
-  reduce="nccl": one `ncclReduce(sum)` of the partials onto the root
-      (torch.cuda.nccl, the torch-bundled NCCL), then the same beta fusion.
+  reduce="ordered" (default): one `kblas_x*_mgpu_async` call -- every
+      GPU's partial on its own stream, then a root kernel that reads the
+      partials in device order over NVLink peer memory and fuses beta*y
+      (multidevice.py:161,176,276,282-283), so results are deterministic;
+  reduce="nccl": the per-GPU partial kernels, one `ncclReduce(sum)` onto
+      the root (torch.cuda.nccl, the torch-bundled NCCL), then the root
+      combine kernel (`kblas_mv_mgpu_combine_async`) for beta*y.
+
+The x copies and the non-root partial buffers are cached per device and
+reused across calls (stream-ordered: every GPU's stream waits for the
+root's combine before the next partial overwrites its buffer).
 
 Logical GPUs may share a physical device (e.g. G=8 on a 1-GPU box maps
 every logical GPU to cuda:0); the math is identical, only the placement
@@ -167,46 +172,84 @@ def partial_mv(prec: Precision, kind: str, op: str, m: int, n: int, alpha, local
     _lib.check(rc, "kblas_mv_mgpu_partial_async")
 
 
-def _combine(parts: list, y_root: torch.Tensor, beta, beta_zero: bool, reduce: str) -> torch.Tensor:
-    """beta*y + sum_g parts[g] on the root, device order (multidevice.py:276,282-283)."""
-    root = y_root.device
-    if reduce == "nccl" and len(parts) > 1 and len({p.device for p in parts}) == len(parts):
-        out = torch.empty_like(parts[0])
-        torch.cuda.nccl.reduce(parts, output=out, root=0)
-        acc = out
-    else:
-        acc = parts[0]
-        for p in parts[1:]:
-            acc = acc + (p if p.device == root else p.to(root, non_blocking=True))
-    if beta_zero:
-        return acc
-    return y_root * torch.as_tensor(beta, dtype=y_root.dtype, device=root) + acc
+_scratch: dict = {}
+
+
+def _buffer(dev: torch.device, dtype: torch.dtype, n: int, role) -> torch.Tensor:
+    """A cached length-n device vector (x copies, non-root partials): reused
+    across calls, ordered by the streams (see the module docstring)."""
+    key = (dev.index, dtype, role)
+    t = _scratch.get(key)
+    if t is None or t.numel() < n:
+        t = torch.empty(n, dtype=dtype, device=dev)
+        _scratch[key] = t
+    return t[:n]
+
+
+def _mgpu_name(prec: Precision, kind: str, hermitian: bool) -> str:
+    if kind == "g":
+        return f"{prec.tag}gemv"
+    return {"s": "ssymv", "d": "dsymv", "c": "chemv" if hermitian else "csymv",
+            "z": "zhemv" if hermitian else "zsymv"}[prec.tag]
+
+
+def _ptr_array(vals):
+    return (ctypes.c_void_p * len(vals))(*[v if v else None for v in vals])
 
 
 def _mgpu_common(kind: str, op: str, alpha, dist: DistributedMatrix, x, beta, y, x_len: int, y_len: int,
                  hermitian: bool, reduce: str):
     prec = dist.precision
     root = dist.devices[0]
+    G = dist.device_count
+    lib = _lib.load()
     xd = _ops.vector_in(x, x_len, prec, "x", root)
     yd = _ops.vector_in(y, y_len, prec, "y", root)
     bz = _is_zero(beta)
-    if _is_zero(alpha):
-        out = torch.zeros_like(yd) if bz else yd * torch.as_tensor(beta, dtype=yd.dtype, device=root)
-        return out
-    parts = []
-    for g in range(dist.device_count):
-        dev = dist.devices[g]
-        local = dist.local_views[g]
-        if local is None:
+    # dy[0]: y on input, the result on output (a fresh vector, as in the reference)
+    out = torch.empty_like(yd) if bz else yd.clone()
+    # x on every physical device (one cached copy per device)
+    xs = {}
+    for dev in dist.devices:
+        if dev.index in xs:
             continue
-        xg = xd if dev == root else xd.to(dev, non_blocking=True)
-        part = torch.empty(y_len, dtype=prec.torch_dtype, device=dev)
-        partial_mv(prec, kind, op, dist.global_m, dist.global_n, alpha, local, xg, part,
-                   dist.device_count, g, dist.nb_cols, hermitian)
-        parts.append(part)
-    if not parts:
-        return torch.zeros_like(yd) if bz else yd * torch.as_tensor(beta, dtype=yd.dtype, device=root)
-    return _combine(parts, yd, beta, bz, reduce)
+        if dev == root:
+            xs[dev.index] = xd
+        else:
+            with _ops._on_device(dev):
+                xs[dev.index] = _buffer(dev, prec.torch_dtype, x_len, "x").copy_(xd, non_blocking=True)
+    eb = prec.element_bytes
+    a_ptrs = [(v.data.data_ptr() + v.linear_index(0, 0) * eb) if v is not None else 0 for v in dist.local_views]
+    lda = next((v.ld for v in dist.local_views if v is not None), local_ld(dist.global_m))
+    streams = [_ops.stream_handle(dev) for dev in dist.devices]
+    distinct = len({d.index for d in dist.devices}) == G
+    al, be = _lib.scalar(prec.tag, alpha), _lib.scalar(prec.tag, beta)
+    if reduce == "nccl" and G > 1 and distinct and not _is_zero(alpha):
+        # per-GPU partials, NCCL reduce(sum) onto the root, root combine with beta
+        parts = [_buffer(dev, prec.torch_dtype, y_len, ("part", g)) for g, dev in enumerate(dist.devices)]
+        for g, dev in enumerate(dist.devices):
+            partial_mv(prec, kind, op, dist.global_m, dist.global_n, alpha, dist.local_views[g], xs[dev.index],
+                       parts[g], G, g, dist.nb_cols, hermitian)
+        torch.cuda.nccl.reduce(parts, output=parts[0], root=0)
+        with _ops._on_device(root):
+            rc = lib.kblas_mv_mgpu_combine_async(prec.tag.encode(), y_len, 1, _ptr_array([parts[0].data_ptr()]),
+                                                 ctypes.addressof(be), out.data_ptr(), streams[0])
+        _lib.check(rc, "kblas_mv_mgpu_combine_async")
+        return out
+    dys = [out.data_ptr()] + [_buffer(dist.devices[g], prec.torch_dtype, y_len, ("part", g)).data_ptr()
+                              for g in range(1, G)]
+    ids = (ctypes.c_int * G)(*[d.index for d in dist.devices])
+    sts = (ctypes.c_void_p * G)(*streams)
+    name = f"kblas_{_mgpu_name(prec, kind, hermitian)}_mgpu_async"
+    args = [_ptr_array(a_ptrs), lda, _ptr_array([xs[d.index].data_ptr() for d in dist.devices]), 1, be,
+            _ptr_array(dys), 1, G, dist.nb_cols, ids, sts]
+    with _ops._on_device(root):
+        if kind == "g":
+            rc = getattr(lib, name)(op.encode(), dist.global_m, dist.global_n, al, *args)
+        else:
+            rc = getattr(lib, name)(op.encode(), dist.global_n, al, *args)
+    _lib.check(rc, name)
+    return out
 
 
 def _device_reports(dist: DistributedMatrix, kind: str, trans_or_uplo: str, alpha) -> list:

@@ -208,3 +208,19 @@ class TestCAbi:
 
         with pytest.raises(RuntimeError):
             gemv("n", 1.0, MatrixView(np.zeros(64), 8, 8, 8, precision("d")), np.zeros(8), 0.0, np.zeros(8))
+
+
+def test_view_of_padded_column_major_tensor():
+    """a padded column-major torch tensor (ld > rows) is accepted
+    when its storage holds n whole columns (the reference's rule,
+    core.py:92-94)."""
+    import torch
+
+    import paper_1410_1726_b200 as kb
+
+    t = torch.zeros(4, 10).T[:6]  # 6 x 4, ld 10
+    v = kb.view_of(t)
+    assert (v.rows, v.cols, v.ld) == (6, 4, 10)
+    assert v.data.numel() == 40
+    t[2, 3] = 5.0
+    assert float(v.array()[2, 3]) == 5.0
