@@ -21,7 +21,7 @@ from .core import (
     precision_of,
     view_of,
 )
-from .kernels import SEGMENT_BYTES, ExecutionReport, Op, gemv, hemv, symv, symv_hemv
+from .kernels import SEGMENT_BYTES, ExecutionReport, Op, gemv, gemv_async, hemv, symv, symv_hemv, symv_hemv_async
 from .multidevice import (
     CommandQueue,
     DistributedMatrix,
@@ -62,6 +62,7 @@ __all__ = [
     "flop_count",
     "gather",
     "gemv",
+    "gemv_async",
     "gemv_mgpu",
     "gemv_mgpu_async",
     "gemv_offset",
@@ -75,6 +76,7 @@ __all__ = [
     "required_local_elements",
     "symv",
     "symv_hemv",
+    "symv_hemv_async",
     "symv_hemv_mgpu",
     "symv_hemv_mgpu_async",
     "symv_hemv_offset",

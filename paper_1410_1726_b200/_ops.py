@@ -249,12 +249,18 @@ _PINNED = _PinnedResults()
 
 def call_hostvec(prec: Precision, kind: str, op: str, hermitian: bool, m: int, n: int, alpha, a_ptr: int,
                  lda: int, x, x_len: int, beta, y, y_len: int, device, off_r: int = 0, off_c: int = 0,
-                 while_running=None):
+                 while_running=None, keep: list | None = None):
     """One FFI crossing for a numpy-vector call: H2D of x (and y when beta
     != 0), the kernels, D2H of the result into a page-locked buffer
     (_PinnedResults), then the wait.  `while_running()` (the caller's
     report bookkeeping) runs between the enqueue and the wait, overlapped
-    with the kernels.  Returns (numpy result, while_running's result)."""
+    with the kernels.  Returns (numpy result, while_running's result).
+
+    keep is not None: asynchronous (a CommandQueue submission): no wait;
+    the operands the copies and kernels still read are appended to `keep`,
+    which the caller holds until its queue synchronises.  The result
+    buffer comes from the same pool; it is not handed out again while the
+    returned array (held by the queue's handle) is alive."""
     xa = np.ascontiguousarray(np.asarray(x, dtype=prec.dtype))
     if xa.ndim != 1 or xa.size != x_len:
         raise ValueError(f"x must be a vector of length {x_len}")
@@ -281,9 +287,11 @@ def call_hostvec(prec: Precision, kind: str, op: str, hermitian: bool, m: int, n
                 extra = while_running()
         finally:
             # x, y_in and the result buffer stay referenced until the wait
-            rc_sync = _fn("kblas_stream_sync")(sh)
+            rc_sync = _fn("kblas_stream_sync")(sh) if keep is None else 0
     _lib.check(rc, "kblas_mv_hostvec_async")
     _lib.check(rc_sync, "kblas_stream_sync")
+    if keep is not None:
+        keep.extend((xa, ya, out))
     del xa, ya
     return out_np, extra
 

@@ -127,7 +127,7 @@ def _scal_report(prec: Precision, y_len: int, beta_zero: bool) -> ExecutionRepor
 
 
 def gemv(trans: str, alpha, a: MatrixView, x, beta, y, config: KernelConfig = DEFAULT_CONFIG,
-         inplace: bool = False) -> ExecutionReport:
+         inplace: bool = False, _keep: list | None = None) -> ExecutionReport:
     """y = alpha * op(A) x + beta * y, op in {n, t, c} (kernels.py:402-440)."""
     trans = trans.lower()
     if trans not in ("n", "t", "c"):
@@ -140,7 +140,7 @@ def gemv(trans: str, alpha, a: MatrixView, x, beta, y, config: KernelConfig = DE
     x_len, y_len = (a.cols, a.rows) if trans == "n" else (a.rows, a.cols)
     dev = _ops.device_for(a, y, x)
     if _ops.host_vectors(x, y, inplace) and not _is_zero(alpha):
-        return _gemv_hostvec(trans, alpha, a, x, beta, y, prec, x_len, y_len, dev)
+        return _gemv_hostvec(trans, alpha, a, x, beta, y, prec, x_len, y_len, dev, _keep)
     xd = _ops.vector_in(x, x_len, prec, "x", dev)
     if _is_zero(alpha) and _is_one(beta):
         yd = _ops.vector_in(y, y_len, prec, "y", dev)
@@ -165,8 +165,9 @@ def gemv(trans: str, alpha, a: MatrixView, x, beta, y, config: KernelConfig = DE
     return rep
 
 
-def _gemv_hostvec(trans, alpha, a: MatrixView, x, beta, y, prec, x_len, y_len, dev) -> ExecutionReport:
-    """numpy x and y: one kblas_mv_hostvec call (copies, kernels, result)."""
+def _gemv_hostvec(trans, alpha, a: MatrixView, x, beta, y, prec, x_len, y_len, dev, keep_list=None) -> ExecutionReport:
+    """numpy x and y: one kblas_mv_hostvec call (copies, kernels, result);
+    keep_list not None: no wait (a queue submission, see gemv_async)."""
     ptr, lda, keep = _ops.matrix_in(a, dev)
 
     def report():  # built while the kernels run
@@ -177,14 +178,16 @@ def _gemv_hostvec(trans, alpha, a: MatrixView, x, beta, y, prec, x_len, y_len, d
         return rep
 
     y_out, rep = _ops.call_hostvec(prec, "g", trans, False, a.rows, a.cols, alpha, ptr, lda, x, x_len, beta, y,
-                                   y_len, dev, while_running=report)
+                                   y_len, dev, while_running=report, keep=keep_list)
     rep.y_out = y_out
+    if keep_list is not None:
+        keep_list.append(keep)
     del keep
     return rep
 
 
 def symv_hemv(uplo: str, alpha, a: HermitianView, x, beta, y, config: KernelConfig = DEFAULT_CONFIG,
-              hermitian: bool | None = None, inplace: bool = False) -> ExecutionReport:
+              hermitian: bool | None = None, inplace: bool = False, _keep: list | None = None) -> ExecutionReport:
     """y = alpha * A x + beta * y from one stored triangle (kernels.py:443-486)."""
     if not isinstance(a, HermitianView):
         raise ValueError("symv/hemv requires a HermitianView")
@@ -211,8 +214,10 @@ def symv_hemv(uplo: str, alpha, a: HermitianView, x, beta, y, config: KernelConf
             return rep
 
         y_out, rep = _ops.call_hostvec(prec, "s", uplo, hermitian, d, d, alpha, ptr, lda, x, d, beta, y, d, dev,
-                                       while_running=report)
+                                       while_running=report, keep=_keep)
         rep.y_out = y_out
+        if _keep is not None:
+            _keep.append(keep)
         del keep
         return rep
     xd = _ops.vector_in(x, d, prec, "x", dev)
@@ -248,3 +253,37 @@ def hemv(uplo, alpha, a, x, beta, y, config: KernelConfig = DEFAULT_CONFIG, **kw
     if not a.base.precision.is_complex:
         raise ValueError("hemv supports complex precisions; use symv for real matrices")
     return symv_hemv(uplo, alpha, a, x, beta, y, config, hermitian=True, **kw)
+
+
+# ---------------------------------------------------------------------------
+# Queued single-GPU calls (the reference's CommandQueue contract,
+# multidevice.py:287-332, applied to gemv / symv_hemv): the call is enqueued
+# on the queue's CUDA stream and returns a handle; `queue.synchronize()`
+# waits, and `handle.result()` is the ExecutionReport.  With numpy x and y
+# the per-call host wait disappears, so back-to-back calls pipeline (the
+# copies, kernels and result writes of call i+1 are queued behind call i
+# instead of each waiting on the host).  x must not be modified and the
+# result not read before the queue has synchronised.
+# ---------------------------------------------------------------------------
+def gemv_async(trans, alpha, a, x, beta, y, config: KernelConfig = DEFAULT_CONFIG, queue=None):
+    """gemv on `queue` (a multidevice.CommandQueue); returns its handle."""
+    return _submit(queue, gemv, trans, alpha, a, x, beta, y, config)
+
+
+def symv_hemv_async(uplo, alpha, a, x, beta, y, config: KernelConfig = DEFAULT_CONFIG, queue=None,
+                    hermitian=None):
+    """symv_hemv on `queue` (a multidevice.CommandQueue); returns its handle."""
+    return _submit(queue, symv_hemv, uplo, alpha, a, x, beta, y, config, hermitian)
+
+
+def _submit(queue, fn, *args):
+    if queue is None:
+        raise ValueError("an async call needs a CommandQueue")
+    keep: list = []
+
+    def run():
+        rep = fn(*args, _keep=keep)
+        rep._keepalive = keep  # operands the queued work still reads
+        return rep
+
+    return queue.submit(run)

@@ -326,6 +326,43 @@ class TestCAbi:
         check(ys[0], want, "d", 0.5, np.abs(naive.dense_from_triangle(a, "l", False)), x, -1.0, y)
 
 
+    def test_mgpu_async_reused_partials_back_to_back(self):
+        """two kblas_dsymv_mgpu_async calls in a row on separate
+        per-GPU streams reuse the same dy[g]; GPU g's stream must wait for
+        the first call's root combine before its next partial overwrites
+        dy[g].  A long first call (big operand, small second) makes the race
+        visible if the wait were missing."""
+        lib = _lib.load()
+        rng = np.random.default_rng(44)
+        n, G, nb = 4096, 2, 128
+        arr = ctypes.c_void_p * G
+        ids = (ctypes.c_int * G)(*([0] * G))
+        dA = arr()
+        ldda = ctypes.c_int(0)
+        assert lib.kblas_malloc_mgpu_1d(n, n, 8, dA, ctypes.byref(ldda), G, nb, ids) == 0
+        a = np.asfortranarray(naive.fill(rng, (n, n), "d"))
+        assert lib.kblas_setmatrix_mgpu_1d(n, n, 8, a.ctypes.data, n, dA, ldda.value, G, nb, ids) == 0
+        streams = [torch.cuda.Stream() for _ in range(G)]
+        pst = arr(*[s_.cuda_stream for s_ in streams])
+        outs, wants = [], []
+        y_part = [torch.empty(n, dtype=torch.float64, device="cuda") for _ in range(G - 1)]
+        torch.cuda.synchronize()
+        for it in range(6):
+            x = naive.fill(rng, n, "d")
+            xs = [dvec(x) for _ in range(G)]
+            y0 = torch.zeros(n, dtype=torch.float64, device="cuda")
+            py = arr(*([y0.data_ptr()] + [t.data_ptr() for t in y_part]))
+            px = arr(*[t.data_ptr() for t in xs])
+            rc = lib.kblas_dsymv_mgpu_async(b"L", n, 1.0, dA, ldda.value, px, 1, 0.0, py, 1, G, nb, ids, pst)
+            assert rc == 0
+            outs.append((y0, xs))
+            wants.append(naive.naive_symv_hemv(1.0, np.tril(a), "l", x, 0.0, np.zeros(n)))
+        torch.cuda.synchronize()
+        dense = np.abs(naive.dense_from_triangle(np.tril(a), "l", False))
+        for (y0, xs), want, in zip(outs, wants):
+            check(y0, want, "d", 1.0, dense, xs[0].cpu().numpy(), 0.0, np.zeros(n))
+        assert lib.kblas_free_mgpu(dA, G, ids) == 0
+
     @pytest.mark.parametrize("kind", ["zhemv", "sgemv_t", "dgemv_n"])
     def test_mgpu_async_c_entries_and_allocation(self, kind):
         """kblas_malloc_mgpu_1d + kblas_setmatrix_mgpu_1d + the _mgpu_async

@@ -128,6 +128,47 @@ class TestCommandQueue:
         assert np.allclose(merged.y_out, naive.naive_symv_hemv(1.0, a, "l", x, 1.0, y))
 
 
+class TestQueuedSingleGpu:
+    """gemv_async / symv_hemv_async: the reference's queue contract on
+    single-GPU calls.  numpy x and y are not waited for per call, so several
+    calls are in flight with distinct results until synchronize()."""
+
+    @pytest.mark.parametrize("tag", "dz")
+    def test_numpy_calls_pipelined(self, tag):
+        rng = np.random.default_rng(92)
+        n = 1500
+        v, a = dev_matrix(rng, n, n, tag)
+        q = kb.CommandQueue()
+        xs = [naive.fill(rng, n, tag) for _ in range(12)]
+        y = naive.fill(rng, n, tag)
+        hs = [kb.gemv_async("n", 1.0, v, x, 0.0, y, queue=q) for x in xs]
+        hs += [kb.symv_hemv_async("l", 0.5, kb.HermitianView(v, "l"), x, -1.0, y, queue=q) for x in xs[:4]]
+        with pytest.raises(RuntimeError):
+            hs[0].result()
+        q.synchronize()
+        for x, h in zip(xs, hs[:12]):
+            want = naive.naive_gemv("n", 1.0, a, x, 0.0, y)
+            assert naive.max_abs_error(h.result().y_out, want) <= naive.run_bound(tag, 1.0, np.abs(a), x, 0.0, y)
+        dense = np.abs(naive.dense_from_triangle(a, "l", tag in "cz"))
+        for x, h in zip(xs[:4], hs[12:]):
+            want = naive.naive_symv_hemv(0.5, a, "l", x, -1.0, y)
+            assert naive.max_abs_error(h.result().y_out, want) <= naive.run_bound(tag, 0.5, dense, x, -1.0, y)
+        # results are distinct buffers
+        assert len({id(h.result().y_out) for h in hs}) == len(hs)
+
+    def test_device_tensors_on_queue_stream(self):
+        rng = np.random.default_rng(93)
+        v, a = dev_matrix(rng, 640, 512, "s")
+        x = torch.from_numpy(naive.fill(rng, 512, "s")).cuda()
+        q = kb.CommandQueue()
+        h = kb.gemv_async("n", 2.0, v, x, 0.0, torch.zeros(640, device="cuda"), queue=q)
+        q.synchronize()
+        want = naive.naive_gemv("n", 2.0, a, x.cpu().numpy(), 0.0, np.zeros(640, np.float32))
+        got = h.result().y_out.cpu().numpy()
+        assert naive.max_abs_error(got, want) <= naive.run_bound("s", 2.0, np.abs(a), x.cpu().numpy(), 0.0,
+                                                                  np.zeros(640))
+
+
 class TestFullSizeConfig5:
     """BASELINE configs[4] at its full size, N = 100000, where no host oracle
     fits: DSYMV lower over 2 logical GPUs (both on device 0), panels
