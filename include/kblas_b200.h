@@ -422,6 +422,11 @@ int kblas_mv_hostvec_async(char prec, char kind, char op, int hermitian, int m, 
                            const void *y_in, void *y_out, cudaStream_t stream);
 /* cudaStreamSynchronize(stream); 0 or the CUDA error. */
 int kblas_stream_sync(cudaStream_t stream);
+/* Make `waiter` wait (on the device) for the work enqueued on          */
+/* `signaler` so far (event record + stream wait on the current         */
+/* device); 0 or the CUDA error.  Used by the Python CommandQueue to    */
+/* order a submission after the caller's stream without a host wait.   */
+int kblas_stream_order(cudaStream_t waiter, cudaStream_t signaler);
 /* Free every cached device buffer (per-stream workspaces, counters,   */
 /* vector staging, mgpu root buffers, SYMV tile tables) after waiting   */
 /* for the devices that own them.  The next call re-creates what it     */

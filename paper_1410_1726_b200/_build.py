@@ -9,6 +9,7 @@ from __future__ import annotations
 import os
 import subprocess
 import sys
+import sysconfig
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
@@ -20,6 +21,9 @@ SOURCES = [os.path.join(CSRC, f) for f in ("kblas_runtime.cu", "kblas_s.cu", "kb
 HEADERS = [os.path.join(CSRC, f) for f in ("kblas_impl.cuh", "kblas_entry_macros.cuh", "kblas_kernels.cuh",
                                            "kblas_device.cuh", "kblas_symv_tma.cuh", "kblas_tuned_b200.inc")]
 DEPS = SOURCES + HEADERS + [os.path.join(os.path.dirname(HERE), "include", "kblas_b200.h")]
+# CPython fast path for numpy-vector calls (links libkblas_b200.so, rpath $ORIGIN)
+HOSTCALL_SRC = os.path.join(CSRC, "kblas_hostcall.cpp")
+HOSTCALL = os.path.join(HERE, "_hostcall" + (sysconfig.get_config_var("EXT_SUFFIX") or ".so"))
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -42,8 +46,32 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(p) <= t for p in DEPS)
 
 
+def cuda_include() -> str:
+    return os.path.join(os.path.dirname(os.path.dirname(os.path.realpath(nvcc()))), "include")
+
+
+def build_hostcall(force: bool = False, verbose: bool = False) -> str:
+    deps = [HOSTCALL_SRC, LIB, os.path.join(os.path.dirname(HERE), "include", "kblas_b200.h")]
+    if not force and os.path.exists(HOSTCALL) and all(os.path.getmtime(p) <= os.path.getmtime(HOSTCALL)
+                                                      for p in deps):
+        return HOSTCALL
+    tmp = HOSTCALL + ".tmp"
+    cmd = [os.environ.get("CXX", "g++"), "-O2", "-std=c++17", "-shared", "-fPIC", "-Wall",
+           f"-I{sysconfig.get_paths()['include']}", f"-I{cuda_include()}", HOSTCALL_SRC,
+           f"-L{HERE}", "-l:libkblas_b200.so", "-Wl,-rpath,$ORIGIN", "-o", tmp]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        sys.stderr.write(res.stdout + res.stderr)
+        raise RuntimeError(f"hostcall build failed ({res.returncode}): {' '.join(cmd)}")
+    os.replace(tmp, HOSTCALL)
+    if verbose:
+        print(f"built {HOSTCALL}")
+    return HOSTCALL
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
+        build_hostcall(verbose=verbose)
         return LIB
     objs, procs = [], []
     for src in SOURCES:
@@ -65,7 +93,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     with open(os.path.join(CSRC, "ptxas_report.txt"), "w") as fh:
         fh.write("".join(reports))
     tmp = LIB + ".tmp"
-    link = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", *objs, "-o", tmp]
+    link = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xlinker", "-soname=libkblas_b200.so",
+            *objs, "-o", tmp]
     res = subprocess.run(link, capture_output=True, text=True)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
@@ -75,6 +104,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         os.remove(obj)
     if verbose:
         print(f"built {LIB}")
+    build_hostcall(force=True, verbose=verbose)
     return LIB
 
 

@@ -141,6 +141,8 @@ def load():
         lib.kblas_mv_hostvec_async.restype = c_int
         lib.kblas_stream_sync.argtypes = [c_void_p]
         lib.kblas_stream_sync.restype = c_int
+        lib.kblas_stream_order.argtypes = [c_void_p, c_void_p]
+        lib.kblas_stream_order.restype = c_int
         lib.kblas_mgpu_local_cols.argtypes = [c_int, c_int, c_int, c_int]
         lib.kblas_mgpu_local_cols.restype = c_int
         lib.kblas_malloc_mgpu_1d.argtypes = [c_int, c_int, c_size_t, POINTER(c_void_p), POINTER(c_int), c_int,

@@ -8,13 +8,13 @@ points on the current torch stream.
 
 from __future__ import annotations
 
-import ctypes
 import sys
 import threading
 
 import numpy as np
 import torch
 
+from . import _hostcall as _HC
 from . import _lib
 from .core import MatrixView, Precision, _is_torch
 
@@ -40,7 +40,7 @@ def device_for(*objs) -> torch.device:
         d = o.data if isinstance(o, MatrixView) else o
         if _is_torch(d) and d.is_cuda:
             return d.device
-    return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cuda", torch._C._cuda_getDevice())
 
 
 _raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
@@ -66,7 +66,7 @@ class _on_device:
         self.prev = None
 
     def __enter__(self):
-        cur = torch.cuda.current_device()
+        cur = torch._C._cuda_getDevice()
         if self.dev is not None and cur != self.dev:
             self.prev = cur
             torch.cuda.set_device(self.dev)
@@ -214,10 +214,12 @@ class _PinnedResults:
     array is returned, so the GPU no longer touches a buffer the caller can
     see or release."""
 
-    KEEP = 8  # tracked buffers per (dtype, length); beyond that, untracked allocations
+    KEEP_BYTES = 32 << 20  # tracked page-locked bytes per (dtype, length) ...
+    KEEP_MIN, KEEP_MAX = 8, 64  # ... as 8..64 buffers; beyond that, untracked allocations
 
     def __init__(self):
         self._bufs: dict = {}
+        self._next: dict = {}  # round-robin scan start per key
         self._lock = threading.Lock()
         # reference count of an array held only by its pool entry, measured
         # the way get() measures it (interpreter-version independent)
@@ -232,66 +234,84 @@ class _PinnedResults:
         key = (dtype, n)
         with self._lock:
             lst = self._bufs.setdefault(key, [])
-            for entry in lst:
+            k = len(lst)
+            # round robin from the buffer after the last one handed out: with
+            # results released in call order (a queue of pending calls) the
+            # first candidate is free
+            start = self._next.get(key, 0)
+            for i in range(k):
+                j = (start + i) % k
+                entry = lst[j]
                 if self._refs(entry) <= self._free_refs:
+                    self._next[key] = j + 1
                     # a new tuple: it holds the array (count above free)
                     # before the lock is released
                     return entry[0], entry[1]
             t = torch.empty(n, dtype=dtype, pin_memory=True)
             entry = (t, t.numpy())
-            if len(lst) < self.KEEP:
+            keep = max(self.KEEP_MIN, min(self.KEEP_MAX, self.KEEP_BYTES // max(1, t.numel() * t.element_size())))
+            if k < keep:
                 lst.append(entry)
+                self._next[key] = k + 1
             return entry[0], entry[1]
 
 
 _PINNED = _PinnedResults()
 
 
-def call_hostvec(prec: Precision, kind: str, op: str, hermitian: bool, m: int, n: int, alpha, a_ptr: int,
-                 lda: int, x, x_len: int, beta, y, y_len: int, device, off_r: int = 0, off_c: int = 0,
-                 while_running=None, keep: list | None = None):
-    """One FFI crossing for a numpy-vector call: H2D of x (and y when beta
-    != 0), the kernels, D2H of the result into a page-locked buffer
-    (_PinnedResults), then the wait.  `while_running()` (the caller's
-    report bookkeeping) runs between the enqueue and the wait, overlapped
-    with the kernels.  Returns (numpy result, while_running's result).
-
-    keep is not None: asynchronous (a CommandQueue submission): no wait;
-    the operands the copies and kernels still read are appended to `keep`,
-    which the caller holds until its queue synchronises.  The result
-    buffer comes from the same pool; it is not handed out again while the
-    returned array (held by the queue's handle) is alive."""
+def _hostvec_operands(prec: Precision, x, x_len: int, alpha, beta, y, y_len: int, placeholder):
+    """Slow path of call_hostvec: convert and validate the operands the way
+    kernels.py:395-399 does (same exceptions and messages)."""
     xa = np.ascontiguousarray(np.asarray(x, dtype=prec.dtype))
     if xa.ndim != 1 or xa.size != x_len:
         raise ValueError(f"x must be a vector of length {x_len}")
-    bz = complex(beta) == 0
-    ya = None
-    if bz:
+    a_c, b_c = _lib.scalar(prec.tag, alpha), _lib.scalar(prec.tag, beta)
+    if prec.is_complex:
+        alpha, beta = complex(a_c.re, a_c.im), complex(b_c.re, b_c.im)
+    else:
+        alpha, beta = float(a_c.value), float(b_c.value)
+    if complex(beta) == 0:
         if length_of(y) != y_len:
             raise ValueError(f"y must be a vector of length {y_len}")
+        ya = placeholder  # never read: any vector of the right length
     else:
         ya = np.ascontiguousarray(np.asarray(y, dtype=prec.dtype))
         if ya.ndim != 1 or ya.size != y_len:
             raise ValueError(f"y must be a vector of length {y_len}")
+    return xa, alpha, beta, ya
+
+
+def call_hostvec(prec: Precision, kind: str, op: str, hermitian: bool, m: int, n: int, alpha, a_ptr: int,
+                 lda: int, x, x_len: int, beta, y, y_len: int, device, off_r: int = 0, off_c: int = 0,
+                 keep: list | None = None):
+    """One call of the numpy-vector path through the CPython binding of
+    kblas_mv_hostvec[_async] (csrc/kblas_hostcall.cpp): a copy-in grid
+    stages x (and y when beta != 0) from page-locked memory, the kernels
+    run, the result lands in a page-locked buffer from _PinnedResults, and
+    the call waits.  Returns (numpy result, launch plan).
+
+    Operands that are not already 1-D contiguous arrays of the operand
+    dtype are converted and validated here first (_hostvec_operands).
+
+    keep is not None: asynchronous (a CommandQueue submission): no wait;
+    the operands the copy-in grid and kernels still read are appended to
+    `keep`, which the caller holds until its queue synchronises.  The
+    result buffer comes from the same pool; it is not handed out again
+    while the returned array (held by the queue's handle) is alive."""
     out, out_np = _PINNED.get(y_len, prec.torch_dtype)
-    a_c, b_c = _lib.scalar(prec.tag, alpha), _lib.scalar(prec.tag, beta)
-    extra = None
+    sync = keep is None
+    herm = 1 if hermitian else 0
     with _on_device(device):
         sh = stream_handle(device)
-        rc = _fn("kblas_mv_hostvec_async")(prec.tag.encode(), kind.encode(), op.encode(), 1 if hermitian else 0,
-                                           m, n, ctypes.addressof(a_c), a_ptr, lda, off_r, off_c, xa.ctypes.data,
-                                           ctypes.addressof(b_c), None if ya is None else ya.ctypes.data,
-                                           out.data_ptr(), sh)
-        try:
-            if rc == 0 and while_running is not None:
-                extra = while_running()
-        finally:
-            # x, y_in and the result buffer stay referenced until the wait
-            rc_sync = _fn("kblas_stream_sync")(sh) if keep is None else 0
-    _lib.check(rc, "kblas_mv_hostvec_async")
-    _lib.check(rc_sync, "kblas_stream_sync")
+        rc = _HC.mv_hostvec(prec.tag, kind, op, herm, m, n, alpha, a_ptr, lda, off_r, off_c, x, x_len, beta, y,
+                            y_len, out.data_ptr(), sh, sync)
+        if rc == _HC.SLOW_PATH:
+            x, alpha, beta, y = _hostvec_operands(prec, x, x_len, alpha, beta, y, y_len, out_np)
+            rc = _HC.mv_hostvec(prec.tag, kind, op, herm, m, n, alpha, a_ptr, lda, off_r, off_c, x, x_len, beta,
+                                y, y_len, out.data_ptr(), sh, sync)
+            if rc == _HC.SLOW_PATH:
+                raise RuntimeError("kblas_mv_hostvec: converted operands rejected by the fast path")
+    _lib.check(rc, "kblas_mv_hostvec" if sync else "kblas_mv_hostvec_async")
     if keep is not None:
-        keep.extend((xa, ya, out))
-    del xa, ya
-    return out_np, extra
-
+        keep.extend((x, y, out))
+    return out_np, _HC.last_plan()

@@ -145,6 +145,11 @@ template <class T, int V> struct Pack {
   }
 };
 
+// L2 prefetch of the 32-byte segment at p (no register destination)
+__device__ __forceinline__ void prefetch_l2(const void *p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 template <class T, int V>
 __device__ __forceinline__ void ld_pack(Pack<T, V> &a, const T *p, bool pred, uint64_t pol) {
   constexpr int W = Pack<T, V>::W;

@@ -235,6 +235,31 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, cu
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
+// One-shot flag set by hostvec_entry right after it launches the copy-in
+// grid that stages x (and y) from page-locked host memory: the next main
+// kernel (or scal) of this thread's call is launched with programmatic
+// stream serialization, so it starts streaming A while the copy-in grid
+// still reads over PCIe; every main kernel executes griddepcontrol.wait
+// before its first x / y access (a no-op for an ordinary launch).
+inline thread_local bool t_pdl_next = false;
+
+template <class... KArgs, class... Args>
+cudaError_t launch_main(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t st,
+                        Args &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = t_pdl_next ? 1 : 0;
+  t_pdl_next = false;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 // ---------------------------------------------------------- load path
 // vec: 256-bit loads; needs lda*esize % 32 == 0.  The submatrix start is
 // realigned down to its 32-byte granule and the lead rows are masked.
@@ -375,8 +400,9 @@ cudaError_t run_gemv_ns(const Path<T> &pa, long long lda, int m, int n, const T 
                y, cnt, widen(alpha), widen(beta), beta_zero ? 1 : 0, (long long)m};
   {
     TimedScope ts(st);
-    kfn<<<(unsigned)(nrb * S), NW * 32, 0, st>>>(p);
+    e = launch_main(kfn, (unsigned)(nrb * S), NW * 32, 0, st, p);
   }
+  if (e != cudaSuccess) return e;
   launched(1);
   char buf[256];
   snprintf(buf, sizeof buf, "gemv_ns %s %s lead=%d m=%d n=%d RB=%d P=%lld slots=%lld", tname<T>(),
@@ -404,13 +430,16 @@ cudaError_t run_gemv_nc(const Path<T> &pa, long long lda, int m, int n, const T 
   cfg.gridDim = dim3((unsigned)(nrb * S));
   cfg.blockDim = dim3(NW * 32);
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = (unsigned)S;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = t_pdl_next ? 2 : 1;
+  t_pdl_next = false;
   cudaError_t e;
   {
     TimedScope ts(st);
@@ -437,8 +466,9 @@ bool run_gemv_ro(const Path<T> &pa, long long lda, int m, int n, const T *x, Col
                y, nullptr, widen(alpha), widen(beta), beta_zero ? 1 : 0, (long long)m};
   {
     TimedScope ts(st);
-    kblas_gemv_ro_kernel<T, V, NW, LR, U><<<(unsigned)P, NW * 32, 0, st>>>(p);
+    *err = launch_main(kblas_gemv_ro_kernel<T, V, NW, LR, U>, (unsigned)P, NW * 32, 0, st, p);
   }
+  if (*err != cudaSuccess) return true;
   launched(1);
   char buf[256];
   snprintf(buf, sizeof buf, "gemv_ro %s %s lead=%d m=%d n=%d RB=%d NW=%d LR=%d U=%d P=%lld slots=1", tname<T>(),
@@ -528,8 +558,9 @@ cudaError_t run_gemv_n(const Path<T> &pa, long long lda, int m, int n, const T *
                y, cnt, widen(alpha), widen(beta), beta_zero ? 1 : 0, (long long)m};
   {
     TimedScope ts(st);
-    kfn<<<(unsigned)P, NW * 32, 0, st>>>(p);
+    e = launch_main(kfn, (unsigned)P, NW * 32, 0, st, p);
   }
+  if (e != cudaSuccess) return e;
   launched(1);
   if (!fused) {
     launch_pdl(kblas_gemv_n_epilogue<T, 8>, (unsigned)cdiv(m, 32), 256, st, y, (const T *)ws, (long long)m, m, pa.lead,
@@ -550,9 +581,10 @@ template <class T, int V, int NW, int CB, bool CONJ>
 cudaError_t run_gemv_tc(const Path<T> &pa, long long lda, int m, int n, long long nglob, const T *x, ColMap cm,
                         T *y, T alpha, T beta, bool beta_zero, cudaStream_t st) {
   auto kfn = kblas_gemv_tc_kernel<T, V, NW, CB, CONJ>;
+  cudaError_t e = cudaSuccess;
   if (cm.G > 1) {
     // mgpu partial: columns this GPU does not own stay zero
-    cudaError_t e = cudaMemsetAsync(y, 0, (size_t)nglob * sizeof(T), st);
+    e = cudaMemsetAsync(y, 0, (size_t)nglob * sizeof(T), st);
     if (e != cudaSuccess) return e;
   }
   const long long P = cdiv(n, CB);
@@ -560,8 +592,9 @@ cudaError_t run_gemv_tc(const Path<T> &pa, long long lda, int m, int n, long lon
                y, nullptr, widen(alpha), widen(beta), beta_zero ? 1 : 0, nglob};
   {
     TimedScope ts(st);
-    kfn<<<(unsigned)P, NW * 32, 0, st>>>(p);
+    e = launch_main(kfn, (unsigned)P, NW * 32, 0, st, p);
   }
+  if (e != cudaSuccess) return e;
   launched(1);
   char buf[256];
   snprintf(buf, sizeof buf, "gemv_tc %s %s%s lead=%d m=%d n=%d H=%d CB=%d P=%lld slots=1", tname<T>(),
@@ -613,8 +646,9 @@ cudaError_t run_gemv_t(const Path<T> &pa, long long lda, int m, int n, long long
                y, cnt, widen(alpha), widen(beta), beta_zero ? 1 : 0, nglob};
   {
     TimedScope ts(st);
-    kfn<<<(unsigned)P, NW * 32, 0, st>>>(p);
+    e = launch_main(kfn, (unsigned)P, NW * 32, 0, st, p);
   }
+  if (e != cudaSuccess) return e;
   launched(1);
   if (!fused) {
     launch_pdl(kblas_gemv_t_epilogue<T, 8>, (unsigned)cdiv(nglob, 32), 256, st, y, (const T *)ws, ws_ld, nglob, (int)CBW,
@@ -806,8 +840,9 @@ cudaError_t run_symv(const Path<T> &pa, long long lda, int d, const T *x, ColMap
   const SymParams p = sym_params(pa.base, lda, d, pa.lead, x, ws, W, tt, cm.G == 1 && cm.nb >= d);
   {
     TimedScope ts(st);
-    kfn<<<(unsigned)P, NW * 32, smem, st>>>(p);
+    e = launch_main(kfn, (unsigned)P, NW * 32, smem, st, p);
   }
+  if (e != cudaSuccess) return e;
   launch_pdl(kblas_symv_epilogue<T, LOWER, 16>, (unsigned)cdiv(d, 32), 512, st, y, p, alpha, beta, (int)beta_zero,
              cm.xg ? *cm.xg : kb::Xchg{});
   launched(2);
@@ -911,8 +946,9 @@ cudaError_t run_symv_tma(const T *A00, long long lda, int d, const T *x, ColMap 
   tp.unit_per_elem = upe;
   {
     TimedScope ts(st);
-    kfn<<<(unsigned)P, (NC + 2) * 32, smem, st>>>(map, tp);
+    e = launch_main(kfn, (unsigned)P, (NC + 2) * 32, smem, st, map, tp);
   }
+  if (e != cudaSuccess) return e;
   launch_pdl(kblas_symv_epilogue<T, LOWER, 16>, (unsigned)cdiv(d, 32), 512, st, y, tp.sp, alpha, beta,
              (int)beta_zero, cm.xg ? *cm.xg : kb::Xchg{});
   launched(2);
@@ -1048,7 +1084,9 @@ inline int code(cudaError_t e) { return e == cudaSuccess ? 0 : (int)e; }
 
 template <class T>
 int scal_only(T *y, long long len, T beta, cudaStream_t st) {
-  kblas_scal_kernel<T><<<(unsigned)cdiv(len, 256), 256, 0, st>>>(y, len, beta, is_zero(beta) ? 1 : 0);
+  const cudaError_t e = launch_main(kblas_scal_kernel<T>, (unsigned)cdiv(len, 256), 256, 0, st, y, len, beta,
+                                    is_zero(beta) ? 1 : 0);
+  if (e != cudaSuccess) return code(e);
   launched();
   g_last_plan = std::string("scal ") + tname<T>();
   return code(cudaGetLastError());
@@ -1300,6 +1338,19 @@ inline cudaError_t vec_staging(size_t bytes, cudaStream_t st, void **out) {
   return cudaSuccess;
 }
 
+// page-locked host memory (mapped into the device address space under UVA):
+// its device-side address
+inline bool mapped_host(const void *h, const void **dev) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, h) == cudaSuccess && at.type == cudaMemoryTypeHost &&
+      at.devicePointer != nullptr) {
+    *dev = at.devicePointer;
+    return true;
+  }
+  cudaGetLastError();
+  return false;
+}
+
 template <class T>
 int hostvec_entry(bool is_gemv, char op, bool herm, int m, int n, T alpha, const T *dA, int lda,
                          int off_r, int off_c, const T *hx, T beta, const T *hy_in, T *hy_out, cudaStream_t st,
@@ -1318,26 +1369,37 @@ int hostvec_entry(bool is_gemv, char op, bool herm, int m, int n, T alpha, const
   if (e != cudaSuccess) return (int)e;
   T *dx = static_cast<T *>(stage);
   T *dy = reinterpret_cast<T *>(static_cast<char *>(stage) + xb);
-  if (xlen > 0 && (e = cudaMemcpyAsync(dx, hx, xlen * sizeof(T), cudaMemcpyHostToDevice, st)) != cudaSuccess)
-    return (int)e;
-  if (!bz && ylen > 0 &&
-      (e = cudaMemcpyAsync(dy, hy_in, ylen * sizeof(T), cudaMemcpyHostToDevice, st)) != cudaSuccess)
-    return (int)e;
+  // page-locked inputs are read by a copy-in grid that overlaps the main
+  // kernel's first A loads (t_pdl_next); pageable ones go through the
+  // copy engine
+  const bool xin = xlen > 0, yin = !bz && ylen > 0;
+  const void *dhx = nullptr, *dhy = nullptr;
+  if ((xin || yin) && (!xin || mapped_host(hx, &dhx)) && (!yin || mapped_host(hy_in, &dhy))) {
+    const long long units = cdiv(std::max(xin ? xlen : 0LL, yin ? ylen : 0LL) * (long long)sizeof(T), 16);
+    const unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>(cdiv(units, 256), 2LL * dev_sms()));
+    kblas_hostvec_in_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<char *>(dx), static_cast<const char *>(dhx),
+                                                   xin ? xlen * (long long)sizeof(T) : 0, reinterpret_cast<char *>(dy),
+                                                   static_cast<const char *>(dhy),
+                                                   yin ? ylen * (long long)sizeof(T) : 0);
+    launched();
+    if ((e = cudaGetLastError()) != cudaSuccess) return (int)e;
+    t_pdl_next = true;
+  } else {
+    if (xin && (e = cudaMemcpyAsync(dx, hx, xlen * sizeof(T), cudaMemcpyHostToDevice, st)) != cudaSuccess)
+      return (int)e;
+    if (yin && (e = cudaMemcpyAsync(dy, hy_in, ylen * sizeof(T), cudaMemcpyHostToDevice, st)) != cudaSuccess)
+      return (int)e;
+  }
   // a page-locked result buffer (e.g. from torch's pinned allocator) is
   // mapped into the device address space: with beta == 0 the kernels write
   // y straight into it over PCIe, overlapping the transfer with the last
   // kernel instead of a D2H copy after it
   T *dyk = dy;
-  if (bz && ylen > 0) {
-    cudaPointerAttributes at{};
-    if (cudaPointerGetAttributes(&at, hy_out) == cudaSuccess && at.type == cudaMemoryTypeHost &&
-        at.devicePointer != nullptr)
-      dyk = static_cast<T *>(at.devicePointer);
-    else
-      cudaGetLastError();
-  }
+  const void *dho = nullptr;
+  if (bz && ylen > 0 && mapped_host(hy_out, &dho)) dyk = static_cast<T *>(const_cast<void *>(dho));
   const int rc = is_gemv ? gemv_entry<T>(o, m, n, alpha, dA, lda, dx, 1, beta, dyk, 1, off_r, off_c, st)
                          : symv_entry<T>(o, herm, n, alpha, dA, lda, dx, 1, beta, dyk, 1, off_r, st);
+  t_pdl_next = false;  // not consumed when the entry returned before launching
   if (rc != 0) return rc;
   if (dyk == dy && ylen > 0 &&
       (e = cudaMemcpyAsync(hy_out, dy, ylen * sizeof(T), cudaMemcpyDeviceToHost, st)) != cudaSuccess)

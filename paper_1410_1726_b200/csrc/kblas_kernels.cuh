@@ -149,6 +149,7 @@ __device__ __forceinline__ void cta_slot_sum(const T *ws, long long ld, long lon
 template <class T, int V, int NW, int CW, int R, int MINB = 2>
 __global__ void __launch_bounds__(NW * 32, MINB) kblas_gemv_n_kernel(const GemvParams p) {
   griddep_launch_dependents();
+  griddep_wait();  // x / y staged by a hostvec copy-in grid (no-op otherwise)
   constexpr int WR = 32 * V * R;  // rows per warp
   constexpr int RB = NW * WR;     // rows per CTA row block
   const T *__restrict__ A = static_cast<const T *>(p.A);
@@ -270,6 +271,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) kblas_gemv_n_kernel(const GemvP
 // ---------------------------------------------------------------------------
 template <class T, int V, int NW, int CW>
 __global__ void __launch_bounds__(NW * 32, 2) kblas_gemv_ns_kernel(const GemvParams p) {
+  griddep_wait();  // x / y staged by a hostvec copy-in grid (no-op otherwise)
   constexpr int RB = 32 * V;
   __shared__ T red[NW][RB];
   const T *__restrict__ A = static_cast<const T *>(p.A);
@@ -360,6 +362,15 @@ __global__ void __launch_bounds__(NW * 32) kblas_gemv_ro_kernel(const GemvParams
   T acc[V];
 #pragma unroll
   for (int v = 0; v < V; ++v) acc[v] = zero<T>();
+  // the first two steps' A segments are prefetched into L2 before
+  // griddepcontrol.wait, so a hostvec call streams A while its copy-in grid
+  // is still fetching x (no registers held across the wait)
+#pragma unroll
+  for (int u = 0; u < 2 * U; ++u) {
+    const int col = warp * CPI + cl + u * STEP;
+    if (col < p.n && rok) prefetch_l2(A + (long long)col * p.lda + pw);
+  }
+  griddep_wait();
   for (int c = warp * CPI + cl; c - cl < p.n; c += U * STEP) {
     Pack<T, V> a[U];
     T xv[U];
@@ -406,6 +417,7 @@ __global__ void __launch_bounds__(NW * 32) kblas_gemv_ro_kernel(const GemvParams
 // ---------------------------------------------------------------------------
 template <class T, int V, int NW, int CW>
 __global__ void __launch_bounds__(NW * 32, 2) kblas_gemv_nc_kernel(const GemvParams p) {
+  griddep_wait();  // x / y staged by a hostvec copy-in grid (no-op otherwise)
   namespace cg = cooperative_groups;
   constexpr int RB = 32 * V;
   __shared__ T red[NW][RB];
@@ -486,6 +498,7 @@ __global__ void __launch_bounds__(NW * 32, 2) kblas_gemv_nc_kernel(const GemvPar
 template <class T, int V, int NW, int CW, int R, bool CONJ, int MINB = 2>
 __global__ void __launch_bounds__(NW * 32, MINB) kblas_gemv_t_kernel(const GemvParams p) {
   griddep_launch_dependents();
+  griddep_wait();  // x / y staged by a hostvec copy-in grid (no-op otherwise)
   constexpr int H = 32 * V * R;
   constexpr int CBW = NW * CW;
   const T *__restrict__ A = static_cast<const T *>(p.A);
@@ -609,6 +622,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) kblas_gemv_t_kernel(const GemvP
 // ---------------------------------------------------------------------------
 template <class T, int V, int NW, int CB, bool CONJ>
 __global__ void __launch_bounds__(NW * 32, 2) kblas_gemv_tc_kernel(const GemvParams p) {
+  griddep_wait();  // x / y staged by a hostvec copy-in grid (no-op otherwise)
   constexpr int H = 32 * V;
   __shared__ T part[NW][CB];
   const T *__restrict__ x = static_cast<const T *>(p.x);
@@ -849,7 +863,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) kblas_symv_kernel(const SymPara
   // reduction.
   Pack<T, V> a[CW][R];
   T xr[R][V];
-  auto load = [&](const SymTile &t, long long q) {
+  auto load_x = [&](const SymTile &t, long long q) {
     const int p0 = (t.chunk0 + (int)(q - t.prefix)) * H;
     const int vlo = t.row0 + p.lead, vhi = t.row1 + p.lead;
 #pragma unroll
@@ -865,6 +879,10 @@ __global__ void __launch_bounds__(NW * 32, MINB) kblas_symv_kernel(const SymPara
         }
       }
     }
+  };
+  auto load_a = [&](const SymTile &t, long long q) {
+    const int p0 = (t.chunk0 + (int)(q - t.prefix)) * H;
+    const int vlo = t.row0 + p.lead, vhi = t.row1 + p.lead;
     const T *Aw = A + (long long)(t.lcol0 + cl) * p.lda;
 #pragma unroll
     for (int j = 0; j < CW; ++j) {
@@ -875,6 +893,10 @@ __global__ void __launch_bounds__(NW * 32, MINB) kblas_symv_kernel(const SymPara
         ld_pack(a[j][r], Aw + (long long)j * p.lda + vs, cok && vs < vhi && vs + V > vlo, pol);
       }
     }
+  };
+  auto load = [&](const SymTile &t, long long q) {
+    load_x(t, q);
+    load_a(t, q);
   };
 
   SymTile tl = p.tiles[c.k];
@@ -894,6 +916,22 @@ __global__ void __launch_bounds__(NW * 32, MINB) kblas_symv_kernel(const SymPara
   auto xcj = [&](int j) -> T {
     if constexpr (XS) return xs_buf[cl + j]; else return xr_c[j];
   };
+  // the first item's A segments are prefetched into L2 before
+  // griddepcontrol.wait, so a hostvec call streams A while its copy-in grid
+  // is still fetching x (no registers held across the wait)
+  {
+    const int p0 = (tl.chunk0 + (int)(c.q - tl.prefix)) * H;
+    const int vlo = tl.row0 + p.lead, vhi = tl.row1 + p.lead;
+    const T *Aw = A + (long long)(tl.lcol0 + cl) * p.lda;
+#pragma unroll
+    for (int j = 0; j < CW; ++j)
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int vs = p0 + r * 32 * V + lane * V;
+        if (cl + j < tl.ncols && vs < vhi && vs + V > vlo) prefetch_l2(Aw + (long long)j * p.lda + vs);
+      }
+  }
+  griddep_wait();
   set_xc(tl);
 #pragma unroll
   for (int j = 0; j < CW; ++j) t2[j] = zero<T>();
@@ -1196,9 +1234,39 @@ __global__ void __launch_bounds__(EW * 32) kblas_symv_epilogue(T *y, const SymPa
   }
 }
 
+// Stages a numpy-vector call's x (and y when beta != 0) from page-locked
+// host memory, mapped into the device address space, into the call's
+// device staging buffer (replaces two cudaMemcpyAsync H2D copies and their
+// copy-engine round trips).  It releases its dependents at once: the main
+// kernel, launched with programmatic stream serialization, streams A
+// meanwhile and waits in griddepcontrol.wait before it reads x or y.
+__device__ __forceinline__ void hostvec_copy(char *dst, const char *src, long long bytes, long long tid,
+                                             long long nt) {
+  if (bytes <= 0) return;
+  long long done = 0;
+  if (((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0) {
+    const long long n16 = bytes >> 4;
+    for (long long i = tid; i < n16; i += nt)
+      reinterpret_cast<uint4 *>(dst)[i] = reinterpret_cast<const uint4 *>(src)[i];
+    done = n16 << 4;
+  }
+  // element sizes are multiples of 4 bytes
+  for (long long i = (done >> 2) + tid; i < (bytes >> 2); i += nt)
+    reinterpret_cast<unsigned *>(dst)[i] = reinterpret_cast<const unsigned *>(src)[i];
+}
+
+static __global__ void kblas_hostvec_in_kernel(char *dx, const char *hx, long long xbytes, char *dy, const char *hy,
+                                        long long ybytes) {
+  griddep_launch_dependents();
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x, nt = (long long)gridDim.x * blockDim.x;
+  hostvec_copy(dx, hx, xbytes, tid, nt);
+  hostvec_copy(dy, hy, ybytes, tid, nt);
+}
+
 // y <- beta * y (beta == 0: zero fill); run_scal semantics (kernels.py:127-146)
 template <class T>
 __global__ void kblas_scal_kernel(T *y, long long n, T beta, int beta_zero) {
+  griddep_wait();  // y staged by a hostvec copy-in grid (no-op otherwise)
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   y[i] = beta_zero ? zero<T>() : mul_(beta, y[i]);

@@ -3,6 +3,7 @@
 // host-vector calls, the peer-memory exchange), mgpu allocation and
 // layout helpers, panel copies, timing / tuning hooks and the version.
 // The per-precision templates are instantiated in kblas_<p>.cu.
+#include <map>
 #include <cctype>
 #include <cstring>
 #include "kblas_impl.cuh"
@@ -183,6 +184,23 @@ int kblas_mv_hostvec_async(char prec, char kind, char op, int hermitian, int m, 
 }
 
 int kblas_stream_sync(cudaStream_t stream) { return code(cudaStreamSynchronize(stream)); }
+
+int kblas_stream_order(cudaStream_t waiter, cudaStream_t signaler) {
+  if (waiter == signaler) return 0;
+  // one reusable event per (thread, device): a wait captures the event's
+  // state when it is enqueued, so re-recording it later is safe
+  thread_local std::map<int, cudaEvent_t> evs;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return (int)e;
+  cudaEvent_t &ev = evs[dev];
+  if (ev == nullptr && (e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) {
+    ev = nullptr;
+    return (int)e;
+  }
+  if ((e = cudaEventRecord(ev, signaler)) != cudaSuccess) return (int)e;
+  return code(cudaStreamWaitEvent(waiter, ev, 0));
+}
 
 // ------------------------------------------------ peer-memory exchange
 int kblas_ipc_get_handle(const void *dptr, void *handle_out) {

@@ -63,6 +63,7 @@ template <class T, int NC, int CW, int RS, int S, bool LOWER, bool HERM>
 __global__ void __launch_bounds__((NC + 2) * 32, 1)
     kblas_symv_tma_kernel(const __grid_constant__ CUtensorMap tmap, const SymTmaParams tp) {
   griddep_launch_dependents();
+  griddep_wait();  // x staged by a hostvec copy-in grid (no-op otherwise)
   constexpr int VE = Stage<T, RS>::VE;
   constexpr int HS = Stage<T, RS>::HS;
   constexpr int W = NC * CW;

@@ -29,7 +29,7 @@ from __future__ import annotations
 
 import enum
 import re
-from dataclasses import dataclass
+from dataclasses import dataclass, fields
 
 from . import _lib, _ops, roofline
 from .core import HermitianView, MatrixView, Precision
@@ -73,6 +73,42 @@ class ExecutionReport:
         self.tb_count += other.tb_count
         self.reduction_events += other.reduction_events
         self.scal_invocations += other.scal_invocations
+
+
+class _DeferredReport(ExecutionReport):
+    """ExecutionReport of a numpy-vector call whose counters are computed on
+    first access (the call itself only records the launch plan), so the
+    bookkeeping costs nothing on the call path when nobody reads it."""
+
+    def __init__(self, y_out, fill):
+        self.__dict__["_fill"] = fill
+        self.y_out = y_out
+
+    def _materialize(self):
+        fill = self.__dict__.pop("_fill", None)
+        if fill is not None:
+            rep = fill()
+            for name in _COUNTER_FIELDS:
+                self.__dict__.setdefault(name, rep.__dict__[name])
+
+
+def _deferred_field(name):
+    def get(self):
+        d = self.__dict__
+        if name not in d:
+            self._materialize()
+        return d[name]
+
+    def put(self, value):
+        self._materialize()
+        self.__dict__[name] = value
+
+    return property(get, put)
+
+
+_COUNTER_FIELDS = [f.name for f in fields(ExecutionReport) if f.name != "y_out"]
+for _name in _COUNTER_FIELDS:
+    setattr(_DeferredReport, _name, _deferred_field(_name))
 
 
 def _segs(nbytes: int) -> int:
@@ -169,17 +205,17 @@ def _gemv_hostvec(trans, alpha, a: MatrixView, x, beta, y, prec, x_len, y_len, d
     """numpy x and y: one kblas_mv_hostvec call (copies, kernels, result);
     keep_list not None: no wait (a queue submission, see gemv_async)."""
     ptr, lda, keep = _ops.matrix_in(a, dev)
+    y_out, plan = _ops.call_hostvec(prec, "g", trans, False, a.rows, a.cols, alpha, ptr, lda, x, x_len, beta, y,
+                                    y_len, dev, keep=keep_list)
 
-    def report():  # built while the kernels run
+    def report():
         rep = ExecutionReport()
         fill_report(rep, prec, a.rows * a.cols, x_len, y_len, _is_zero(beta),
-                    roofline.gemv_flops(prec, a.rows, a.cols, trans), _lib.last_plan())
+                    roofline.gemv_flops(prec, a.rows, a.cols, trans), plan)
         rep.scal_invocations = 1
         return rep
 
-    y_out, rep = _ops.call_hostvec(prec, "g", trans, False, a.rows, a.cols, alpha, ptr, lda, x, x_len, beta, y,
-                                   y_len, dev, while_running=report, keep=keep_list)
-    rep.y_out = y_out
+    rep = _DeferredReport(y_out, report)
     if keep_list is not None:
         keep_list.append(keep)
     del keep
@@ -206,16 +242,15 @@ def symv_hemv(uplo: str, alpha, a: HermitianView, x, beta, y, config: KernelConf
     if _ops.host_vectors(x, y, inplace) and not _is_zero(alpha):
         # numpy x and y: one kblas_mv_hostvec call (copies, kernels, result)
         ptr, lda, keep = _ops.matrix_in(a.base, dev, lower_tri=uplo)
+        y_out, plan = _ops.call_hostvec(prec, "s", uplo, hermitian, d, d, alpha, ptr, lda, x, d, beta, y, d, dev,
+                                        keep=_keep)
 
-        def report():  # built while the kernels run
+        def report():
             rep = ExecutionReport()
-            fill_report(rep, prec, d * (d + 1) // 2, d, d, _is_zero(beta), roofline.symv_flops(prec, d),
-                        _lib.last_plan())
+            fill_report(rep, prec, d * (d + 1) // 2, d, d, _is_zero(beta), roofline.symv_flops(prec, d), plan)
             return rep
 
-        y_out, rep = _ops.call_hostvec(prec, "s", uplo, hermitian, d, d, alpha, ptr, lda, x, d, beta, y, d, dev,
-                                       while_running=report, keep=_keep)
-        rep.y_out = y_out
+        rep = _DeferredReport(y_out, report)
         if _keep is not None:
             _keep.append(keep)
         del keep

@@ -224,3 +224,55 @@ def test_view_of_padded_column_major_tensor():
     assert v.data.numel() == 40
     t[2, 3] = 5.0
     assert float(v.array()[2, 3]) == 5.0
+
+
+class TestHostcallBinding:
+    """csrc/kblas_hostcall.cpp: the CPython fast path of the numpy-vector
+    call.  Off-path operands come back as SLOW_PATH before any device
+    work, so the Python layer can convert and validate them."""
+
+    def test_shares_the_ctypes_library_instance(self):
+        from paper_1410_1726_b200 import _ops
+
+        _lib.load()
+        assert _ops._HC.last_plan() == _lib.last_plan()
+        maps = [ln.split() for ln in open("/proc/self/maps") if "libkblas_b200.so" in ln]
+        assert maps, "libkblas_b200.so is not mapped"
+        assert sum(1 for f in maps if int(f[2], 16) == 0) == 1  # one load of the file
+
+    @pytest.mark.parametrize("x, alpha, y", [
+        ([1.0, 2.0, 3.0, 4.0], 1.0, np.zeros(4)),             # x is a list
+        (np.zeros(4, np.float32), 1.0, np.zeros(4)),          # wrong dtype
+        (np.zeros(5), 1.0, np.zeros(4)),                      # wrong length
+        (np.zeros((4, 8))[:, 0], 1.0, np.zeros(4)),           # strided
+        (np.zeros((2, 2)), 1.0, np.zeros(4)),                 # 2-D
+        (np.zeros(4), 1j, np.zeros(4)),                       # complex alpha, real precision
+        (np.zeros(4), 1.0, np.zeros(3)),                      # y length (beta == 0)
+    ])
+    def test_off_path_operands(self, x, alpha, y):
+        from paper_1410_1726_b200 import _ops
+
+        hc = _ops._HC
+        assert hc.mv_hostvec("d", "g", "n", 0, 4, 4, alpha, 0, 4, 0, 0, x, 4, 0.0, y, 4, 0, 0, True) == hc.SLOW_PATH
+
+    def test_beta_nonzero_checks_y_dtype(self):
+        from paper_1410_1726_b200 import _ops
+
+        hc = _ops._HC
+        y32 = np.zeros(4, np.float32)
+        assert hc.mv_hostvec("d", "g", "n", 0, 4, 4, 1.0, 0, 4, 0, 0, np.zeros(4), 4, 0.5, y32, 4, 0, 0,
+                             True) == hc.SLOW_PATH
+
+    def test_slow_path_validation_messages(self):
+        """The slow path raises the reference's exceptions (kernels.py:395-399)."""
+        from paper_1410_1726_b200 import _ops
+
+        p = precision("d")
+        with pytest.raises(ValueError, match="x must be a vector of length 4"):
+            _ops._hostvec_operands(p, np.zeros(5), 4, 1.0, 0.0, np.zeros(4), 4, np.zeros(4))
+        with pytest.raises(ValueError, match="y must be a vector of length 4"):
+            _ops._hostvec_operands(p, np.zeros(4), 4, 1.0, 0.0, np.zeros(3), 4, np.zeros(4))
+        with pytest.raises(ValueError, match="complex scalar"):
+            _ops._hostvec_operands(p, np.zeros(4), 4, 1j, 0.0, np.zeros(4), 4, np.zeros(4))
+        xa, a, b, ya = _ops._hostvec_operands(p, [1, 2, 3, 4], 4, 2, 0.5, [1, 1, 1, 1], 4, None)
+        assert xa.dtype == np.float64 and ya.dtype == np.float64 and (a, b) == (2.0, 0.5)
