@@ -540,23 +540,34 @@ def e2e_single(args, As, x, y, tag, family, op, herm, m, n, ld, dev, nbytes):
                 return kb.symv_hemv(op, 1.0, kb.HermitianView(view, op), npx, 0.0, npy, hermitian=herm).y_out
             return kb.gemv(op, 1.0, view, npx, 0.0, npy).y_out
 
-        step(0)
+        # warm-up holds three results at once, so the page-locked result
+        # pool has the buffers the steady state rotates through (a first
+        # allocation can take ~10 ms)
+        warm = [step(i) for i in range(3)]
+        del warm
         torch.cuda.synchronize(dev)
+        ts = []
         t0 = time.perf_counter()
         for i in range(steps):
+            t1 = time.perf_counter()
             out = step(i)
+            ts.append(time.perf_counter() - t1)
         torch.cuda.synchronize(dev)
+        run.per_step = sorted(ts)
         return (time.perf_counter() - t0) / steps, out
 
     # resident matrix (rotating over the same copies as the device-timed
     # steps): the headline end-to-end figure
     A = As[0]
-    nsteps = max(args.e2e_steps, 20)
+    nsteps = max(args.e2e_steps, 50)
     el, out = run([kb.MatrixView(a.reshape(-1), m, n, ld, p) for a in As], nsteps)
     y_len = len(out)
+    ps = run.per_step
     res = {"value": round(nbytes / el / 1e9, 3), "unit": "GB/s",
            "h2d_bytes_per_step": int(x_len * eb), "d2h_bytes_per_step": int(y_len * eb),
            "steps": nsteps, "ms_per_step": round(el * 1e3, 4),
+           "step_ms": {"min": round(ps[0] * 1e3, 4), "median": round(ps[len(ps) // 2] * 1e3, 4),
+                       "max": round(ps[-1] * 1e3, 4)},
            "path": f"paper_1410_1726_b200.{'symv_hemv' if family == 'symv' else 'gemv'} with A resident in HBM "
                    "(uploaded once), x from pinned host numpy each step (beta = 0: y is not uploaded), "
                    "y returned as numpy"}
