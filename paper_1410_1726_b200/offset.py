@@ -16,7 +16,7 @@ from dataclasses import dataclass
 
 from . import _lib, _ops, roofline
 from .core import HermitianView, MatrixView
-from .kernels import SEGMENT_BYTES, ExecutionReport, _is_one, _is_zero, _scal_report, fill_report
+from .kernels import SEGMENT_BYTES, ExecutionReport, _DeferredReport, _is_one, _is_zero, _scal_report, fill_report
 from .partition import DEFAULT_CONFIG, KernelConfig
 
 
@@ -81,6 +81,26 @@ def gemv_offset(trans: str, alpha, req: OffsetRequest, x, beta, y,
     _check_alignment(parent)
     x_len, y_len = (req.sub_n, req.sub_m) if trans == "n" else (req.sub_m, req.sub_n)
     dev = _ops.device_for(parent, y, x)
+    if _ops.host_vectors(x, y, False) and not _is_zero(alpha):
+        # numpy x and y: one kblas_mv_hostvec call with the offsets
+        ptr, lda, keep = _ops.matrix_in(parent, dev)
+        try:
+            y_out, plan = _ops.call_hostvec(prec, "g", trans, False, req.sub_m, req.sub_n, alpha, ptr, lda, x,
+                                            x_len, beta, y, y_len, dev, off_r=req.row_off, off_c=req.col_off)
+        except ValueError as e:
+            if "vector of length" not in str(e):
+                raise
+            raise ValueError(f"expected x of length {x_len} and y of length {y_len}") from None
+        del keep
+
+        def report():
+            r = ExecutionReport()
+            fill_report(r, prec, req.sub_m * req.sub_n, x_len, y_len, _is_zero(beta),
+                        roofline.gemv_flops(prec, req.sub_m, req.sub_n, trans), plan)
+            r.scal_invocations = 1
+            return r
+
+        return _DeferredReport(y_out, report)
     try:
         xd = _ops.vector_in(x, x_len, prec, "x", dev)
         bz = _is_zero(beta)
@@ -122,6 +142,25 @@ def symv_hemv_offset(uplo: str, alpha, parent: HermitianView, offset: int, sub_d
         raise ValueError("submatrix exceeds the parent matrix")
     _check_alignment(parent.base)
     dev = _ops.device_for(parent.base, y, x)
+    if _ops.host_vectors(x, y, False) and not _is_zero(alpha):
+        # numpy x and y: one kblas_mv_hostvec call at (offset, offset)
+        ptr, lda, keep = _ops.matrix_in(parent.base, dev, lower_tri=uplo)
+        try:
+            y_out, plan = _ops.call_hostvec(prec, "s", uplo, hermitian, sub_d, sub_d, alpha, ptr, lda, x, sub_d,
+                                            beta, y, sub_d, dev, off_r=offset, off_c=offset)
+        except ValueError as e:
+            if "vector of length" not in str(e):
+                raise
+            raise ValueError(f"expected x and y of length {sub_d}") from None
+        del keep
+
+        def report():
+            r = ExecutionReport()
+            fill_report(r, prec, sub_d * (sub_d + 1) // 2, sub_d, sub_d, _is_zero(beta),
+                        roofline.symv_flops(prec, sub_d), plan)
+            return r
+
+        return _DeferredReport(y_out, report)
     try:
         xd = _ops.vector_in(x, sub_d, prec, "x", dev)
         bz = _is_zero(beta)
