@@ -1,0 +1,239 @@
+// sched_probe.cu — does the SYMV item schedule leave SMs idle at the end?
+//
+// Streams the lower triangle of an n x n double matrix in the SYMV
+// kernel's access pattern (W = 128-column tiles of 128-row chunks, 16 warps
+// x 8 columns, one 256-bit load per lane per column, a CTA barrier per
+// item, one FMA per element) under three item schedules over 148 CTAs:
+//   static  : contiguous stream-K ranges,
+//   inter   : segments of K items dealt round robin (the library's
+//             schedule, without its even tail split),
+//   dynamic : segments of K items taken from a global counter (thread 0
+//             takes the next segment one segment ahead; the index reaches
+//             the other warps through shared memory at an item barrier).
+// Reports the kernel time (events) and the spread of the CTAs' finish times
+// (globaltimer), i.e. how long the first finished SMs sit idle.
+//
+//   nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o scripts/sched_probe scripts/sched_probe.cu
+//   ./scripts/sched_probe N [K]
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+
+#include <algorithm>
+#include <vector>
+
+struct Tile { int col0, chunk0; long long prefix; };
+
+__device__ __forceinline__ void ld256(uint32_t (&w)[8], const void *p, bool pred) {
+  const int pr = pred ? 1 : 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) w[k] = 0u;
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %9, 0;\n\t"
+               "@q ld.global.nc.L1::no_allocate.L2::evict_first.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n\t}"
+               : "+r"(w[0]), "+r"(w[1]), "+r"(w[2]), "+r"(w[3]), "+r"(w[4]), "+r"(w[5]), "+r"(w[6]), "+r"(w[7])
+               : "l"(p), "r"(pr));
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+constexpr int NW = 16, CW = 8;
+
+__device__ __forceinline__ int tile_of(const Tile *tiles, int ntiles, long long q) {
+  int lo = 0, hi = ntiles;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) / 2;
+    if (tiles[mid].prefix <= q) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+// MODE 0 static, 1 interleaved, 2 dynamic
+template <int MODE, bool F32>
+__global__ void __launch_bounds__(NW * 32, 1) sched(const char *A, long long ld, int n, const Tile *tiles,
+                                                    int ntiles, long long total, int P, int K, unsigned *ctr,
+                                                    const int *seg_tile, double *out, unsigned long long *tend) {
+  constexpr int EB = F32 ? 4 : 8, H = 32 * 32 / EB;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ int s_next[2];
+  const long long nseg = (total + K - 1) / K;
+  // current range [q, hi)
+  long long q, hi, seg = 0;
+  unsigned grabbed = 0;
+  if (MODE == 0) {
+    q = (long long)blockIdx.x * total / P;
+    hi = (long long)(blockIdx.x + 1) * total / P;
+  } else if (MODE == 1) {
+    seg = blockIdx.x;
+    q = seg * K;
+    hi = min(total, q + K);
+    if (seg >= nseg) q = hi = total;
+  } else {
+    seg = blockIdx.x;  // first segment: static
+    q = seg * K;
+    hi = min(total, q + K);
+    if (seg >= nseg) q = hi = total;
+    if (threadIdx.x == 0) grabbed = P + atomicAdd(ctr, 1u);  // one segment ahead
+  }
+  double acc = 0.0;
+  uint32_t a[CW][8];
+  int k = q < total ? (MODE == 0 ? tile_of(tiles, ntiles, q) : seg_tile[seg]) : 0;
+  // dynamic: the next segment and its start tile, fetched a segment ahead
+  long long nseg_id = -1;
+  int nk = 0;
+  Tile t = tiles[k];
+  long long tnext = k + 1 < ntiles ? tiles[k + 1].prefix : total;
+  auto load = [&](const Tile &tl, long long qq) {
+    const long long p0 = (long long)(tl.chunk0 + (qq - tl.prefix)) * H;
+#pragma unroll
+    for (int j = 0; j < CW; ++j) {
+      const long long row = p0 + lane * (32 / EB);
+      ld256(a[j], A + ((long long)(tl.col0 + warp * CW + j) * ld + row) * EB, row < n);
+    }
+  };
+  if (q < hi) load(t, q);
+  int par = 0;
+  while (q < hi) {
+#pragma unroll
+    for (int j = 0; j < CW; ++j)
+#pragma unroll
+      for (int v = 0; v < 8; v += 2)
+        acc = fma(__hiloint2double((int)a[j][v + 1], (int)a[j][v]), 1.0000001, acc);
+    if (MODE == 2 && threadIdx.x == 0 && q == seg * K) s_next[par] = (int)grabbed;  // after this item's loads
+    __syncthreads();
+    if (MODE == 2 && q == seg * K) {
+      nseg_id = s_next[par];
+      nk = nseg_id < nseg ? seg_tile[nseg_id] : 0;
+    }
+    long long nq = q + 1;
+    if (nq >= hi) {
+      // next range
+      if (MODE == 0) {
+        nq = hi = total;
+      } else if (MODE == 1) {
+        seg += P;
+        nq = seg * K;
+        hi = min(total, nq + K);
+        if (seg >= nseg) nq = hi = total;
+        if (nq < hi) k = seg_tile[seg];
+      } else {
+        seg = nseg_id;
+        par ^= 1;
+        nq = seg * K;
+        hi = min(total, nq + K);
+        if (seg >= nseg) nq = hi = total;
+        if (threadIdx.x == 0 && seg < nseg) grabbed = P + atomicAdd(ctr, 1u);
+        k = nk;
+      }
+      if (nq < hi) {
+        t = tiles[k];
+        tnext = k + 1 < ntiles ? tiles[k + 1].prefix : total;
+      }
+    } else if (nq >= tnext) {
+      ++k;
+      t = tiles[k];
+      tnext = k + 1 < ntiles ? tiles[k + 1].prefix : total;
+    }
+    if (nq < hi) load(t, nq);
+    q = nq;
+  }
+  out[(long long)blockIdx.x * blockDim.x + threadIdx.x] = acc;
+  if (threadIdx.x == 0) tend[blockIdx.x] = gtimer();
+}
+
+int main(int argc, char **argv) {
+  const int n = argc > 1 ? atoi(argv[1]) : 32768;
+  const int K = argc > 2 ? atoi(argv[2]) : 6;
+  const bool f32 = argc > 3 && argv[3][0] == 's';
+  const int EB = f32 ? 4 : 8, H = 1024 / EB;
+  const long long ld = n;
+  const int W = NW * CW;
+  std::vector<Tile> tiles;
+  long long total = 0;
+  for (int c0 = 0; c0 < n; c0 += W) {
+    const int chunk0 = c0 / H;
+    const int nch = (n + H - 1) / H - chunk0;
+    tiles.push_back({c0, chunk0, total});
+    total += nch;
+  }
+  std::vector<int> segt;
+  for (long long sg = 0; sg * K < total; ++sg) {
+    int kk = 0;
+    while (kk + 1 < (int)tiles.size() && tiles[kk + 1].prefix <= sg * K) ++kk;
+    segt.push_back(kk);
+  }
+  int *dseg;
+  cudaMalloc(&dseg, sizeof(int) * segt.size());
+  cudaMemcpy(dseg, segt.data(), sizeof(int) * segt.size(), cudaMemcpyHostToDevice);
+  char *A;
+  double *out;
+  unsigned *ctr;
+  unsigned long long *tend;
+  Tile *dt;
+  const int P = 148;
+  cudaMalloc(&A, (size_t)EB * ld * n);
+  cudaMemset(A, 0, (size_t)EB * ld * n);
+  cudaMalloc(&out, sizeof(double) * P * NW * 32);
+  cudaMalloc(&ctr, sizeof(unsigned));
+  cudaMalloc(&tend, sizeof(unsigned long long) * P);
+  cudaMalloc(&dt, sizeof(Tile) * tiles.size());
+  cudaMemcpy(dt, tiles.data(), sizeof(Tile) * tiles.size(), cudaMemcpyHostToDevice);
+  const double bytes = (double)EB * ((double)n * (n + 1) / 2);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  auto run = [&](int mode, int reps, float *ms, double *spread, double *mean_idle) {
+    std::vector<unsigned long long> te(P);
+    float best = 1e30f;
+    double bsp = 0, bidle = 0;
+    for (int r = 0; r < reps; ++r) {
+      cudaMemset(ctr, 0, sizeof(unsigned));
+      cudaEventRecord(e0);
+#define SCHED(M, F) sched<M, F><<<P, NW * 32>>>(A, ld, n, dt, (int)tiles.size(), total, P, K, ctr, dseg, out, tend)
+      if (f32) {
+        if (mode == 0) SCHED(0, true);
+        if (mode == 1) SCHED(1, true);
+        if (mode == 2) SCHED(2, true);
+      } else {
+        if (mode == 0) SCHED(0, false);
+        if (mode == 1) SCHED(1, false);
+        if (mode == 2) SCHED(2, false);
+      }
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float t;
+      cudaEventElapsedTime(&t, e0, e1);
+      cudaMemcpy(te.data(), tend, sizeof(unsigned long long) * P, cudaMemcpyDeviceToHost);
+      const unsigned long long mx = *std::max_element(te.begin(), te.end());
+      const unsigned long long mn = *std::min_element(te.begin(), te.end());
+      double idle = 0;
+      for (auto v : te) idle += (double)(mx - v);
+      if (t < best) {
+        best = t;
+        bsp = (mx - mn) * 1e-3;
+        bidle = idle / P * 1e-3;
+      }
+    }
+    *ms = best;
+    *spread = bsp;
+    *mean_idle = bidle;
+  };
+  const char *names[3] = {"static", "interleaved", "dynamic"};
+  for (int pass = 0; pass < 2; ++pass)
+    for (int mode = 0; mode < 3; ++mode) {
+      float ms;
+      double sp, idle;
+      run(mode, 10, &ms, &sp, &idle);
+      if (pass == 1)
+        printf("{\"prec\": \"%c\", \"n\": %d, \"K\": %d, \"schedule\": \"%s\", \"us\": %.1f, \"gbs\": %.0f, \"finish_spread_us\": %.1f, "
+               "\"mean_idle_us\": %.1f, \"items\": %lld}\n",
+               f32 ? 's' : 'd', n, K, names[mode], ms * 1e3, bytes / (ms * 1e-3) / 1e9, sp, idle, total);
+    }
+  cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) printf("error %s\n", cudaGetErrorString(err));
+  return 0;
+}
