@@ -242,6 +242,15 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, cu
 // still reads over PCIe; every main kernel executes griddepcontrol.wait
 // before its first x / y access (a no-op for an ordinary launch).
 inline thread_local bool t_pdl_next = false;
+// 1: the PDL-launched main kernel prefetches its first A segments into L2
+// before griddepcontrol.wait; 2: it only waits.  $KBLAS_HOSTVEC_PREFETCH.
+inline int hostvec_prefetch_mode() {
+  static const int mode = [] {
+    const char *e = std::getenv("KBLAS_HOSTVEC_PREFETCH");
+    return (e != nullptr && e[0] == '0') ? 2 : 1;
+  }();
+  return mode;
+}
 
 template <class... KArgs, class... Args>
 cudaError_t launch_main(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t st,
@@ -464,6 +473,7 @@ bool run_gemv_ro(const Path<T> &pa, long long lda, int m, int n, const T *x, Col
   if (2 * P < dev_sms()) return false;
   GemvParams p{pa.base, lda, m, n, pa.lead, x, nullptr, 0, 0, (int)P, 0, cm,
                y, nullptr, widen(alpha), widen(beta), beta_zero ? 1 : 0, (long long)m};
+  p.pdl = t_pdl_next ? hostvec_prefetch_mode() : 0;
   {
     TimedScope ts(st);
     *err = launch_main(kblas_gemv_ro_kernel<T, V, NW, LR, U>, (unsigned)P, NW * 32, 0, st, p);
@@ -837,7 +847,8 @@ cudaError_t run_symv(const Path<T> &pa, long long lda, int d, const T *x, ColMap
   void *ws = nullptr;
   e = workspace(sym_ws_bytes<T>(d, W, tt), st, &ws);
   if (e != cudaSuccess) return e;
-  const SymParams p = sym_params(pa.base, lda, d, pa.lead, x, ws, W, tt, cm.G == 1 && cm.nb >= d);
+  SymParams p = sym_params(pa.base, lda, d, pa.lead, x, ws, W, tt, cm.G == 1 && cm.nb >= d);
+  p.pdl = t_pdl_next ? hostvec_prefetch_mode() : 0;
   {
     TimedScope ts(st);
     e = launch_main(kfn, (unsigned)P, NW * 32, smem, st, p);

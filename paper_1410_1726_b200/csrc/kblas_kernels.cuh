@@ -59,6 +59,8 @@ struct GemvParams {
   double2 alpha, beta; // scalars of the operand type, widened
   int beta_zero;
   long long nglob;     // T: length of y (global columns); N: m
+  int pdl = 0;         // launched as the programmatic dependent of a hostvec copy-in grid
+                       // (1: prefetch the first A segments before the wait, 2: no prefetch)
 };
 
 template <class T> __device__ __forceinline__ T scalar_of(double2 v);
@@ -362,15 +364,19 @@ __global__ void __launch_bounds__(NW * 32) kblas_gemv_ro_kernel(const GemvParams
   T acc[V];
 #pragma unroll
   for (int v = 0; v < V; ++v) acc[v] = zero<T>();
-  // the first two steps' A segments are prefetched into L2 before
-  // griddepcontrol.wait, so a hostvec call streams A while its copy-in grid
-  // is still fetching x (no registers held across the wait)
+  // hostvec call: the first two steps' A segments are prefetched into L2
+  // before griddepcontrol.wait, so A streams while the copy-in grid is
+  // still fetching x (no registers held across the wait)
+  if (p.pdl) {
+    if (p.pdl == 1) {
 #pragma unroll
-  for (int u = 0; u < 2 * U; ++u) {
-    const int col = warp * CPI + cl + u * STEP;
-    if (col < p.n && rok) prefetch_l2(A + (long long)col * p.lda + pw);
+      for (int u = 0; u < 2 * U; ++u) {
+        const int col = warp * CPI + cl + u * STEP;
+        if (col < p.n && rok) prefetch_l2(A + (long long)col * p.lda + pw);
+      }
+    }
+    griddep_wait();
   }
-  griddep_wait();
   for (int c = warp * CPI + cl; c - cl < p.n; c += U * STEP) {
     Pack<T, V> a[U];
     T xv[U];
@@ -758,6 +764,8 @@ struct SymParams {
   long long base, rem;  // first tail item (rounds * P * K) and tail length
   long long nseg;       // rounds * P + P
   const int *seg_tile;  // per segment: tile of its first item (host-built)
+  int pdl = 0;          // launched as the programmatic dependent of a hostvec copy-in grid
+                        // (1: prefetch the first A segments before the wait, 2: no prefetch)
 };
 
 // first item of segment s (s == nseg gives total)
@@ -916,10 +924,10 @@ __global__ void __launch_bounds__(NW * 32, MINB) kblas_symv_kernel(const SymPara
   auto xcj = [&](int j) -> T {
     if constexpr (XS) return xs_buf[cl + j]; else return xr_c[j];
   };
-  // the first item's A segments are prefetched into L2 before
-  // griddepcontrol.wait, so a hostvec call streams A while its copy-in grid
-  // is still fetching x (no registers held across the wait)
-  {
+  // hostvec call: the first item's A segments are prefetched into L2
+  // before griddepcontrol.wait, so A streams while the copy-in grid is
+  // still fetching x (no registers held across the wait)
+  if (p.pdl == 1) {
     const int p0 = (tl.chunk0 + (int)(c.q - tl.prefix)) * H;
     const int vlo = tl.row0 + p.lead, vhi = tl.row1 + p.lead;
     const T *Aw = A + (long long)(tl.lcol0 + cl) * p.lda;
