@@ -78,9 +78,14 @@ class ExecutionReport:
 class _DeferredReport(ExecutionReport):
     """ExecutionReport of a numpy-vector call whose counters are computed on
     first access (the call itself only records the launch plan), so the
-    bookkeeping costs nothing on the call path when nobody reads it."""
+    bookkeeping costs nothing on the call path when nobody reads it.  It
+    compares equal to an ExecutionReport with the same fields, and pickles
+    and copies (dataclasses.replace included) as an ExecutionReport."""
 
-    def __init__(self, y_out, fill):
+    def __init__(self, y_out=None, fill=None, **fields_):
+        if fill is None:  # dataclasses.replace / plain construction
+            super().__init__(y_out=y_out, **fields_)
+            return
         self.__dict__["_fill"] = fill
         self.y_out = y_out
 
@@ -90,6 +95,22 @@ class _DeferredReport(ExecutionReport):
             rep = fill()
             for name in _COUNTER_FIELDS:
                 self.__dict__.setdefault(name, rep.__dict__[name])
+
+    def _as_tuple(self):
+        return tuple(getattr(self, f.name) for f in fields(ExecutionReport))
+
+    def __eq__(self, other):
+        if not isinstance(other, ExecutionReport):
+            return NotImplemented
+        return self._as_tuple() == tuple(getattr(other, f.name) for f in fields(ExecutionReport))
+
+    __hash__ = None
+
+    def __reduce__(self):
+        self._materialize()
+        rep = ExecutionReport(**{f.name: getattr(self, f.name) for f in fields(ExecutionReport)})
+        extra = {k: v for k, v in self.__dict__.items() if k not in rep.__dict__ and k != "_fill"}
+        return (ExecutionReport, (), {**rep.__dict__, **extra})
 
 
 def _deferred_field(name):

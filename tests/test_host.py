@@ -276,3 +276,38 @@ class TestHostcallBinding:
             _ops._hostvec_operands(p, np.zeros(4), 4, 1j, 0.0, np.zeros(4), 4, np.zeros(4))
         xa, a, b, ya = _ops._hostvec_operands(p, [1, 2, 3, 4], 4, 2, 0.5, [1, 1, 1, 1], 4, None)
         assert xa.dtype == np.float64 and ya.dtype == np.float64 and (a, b) == (2.0, 0.5)
+
+
+def test_deferred_report_behaves_like_execution_report():
+    """The numpy-vector path's report fills its counters on first access and
+    otherwise behaves as the reference's ExecutionReport (kernels.py:37-62):
+    equality, absorb, pickle, copy and dataclasses.replace."""
+    import copy
+    import dataclasses
+    import pickle
+
+    from paper_1410_1726_b200.kernels import ExecutionReport, _DeferredReport
+
+    calls = []
+
+    def fill():
+        calls.append(1)
+        r = ExecutionReport()
+        r.bytes_read, r.flops, r.plan, r.scal_invocations = 40, 7, "gemv_ro d", 1
+        return r
+
+    d = _DeferredReport(np.arange(3.0), fill)
+    assert calls == []
+    assert d.flops == 7 and d.bytes_read == 40 and d.plan == "gemv_ro d" and calls == [1]
+    assert d == ExecutionReport(y_out=d.y_out, bytes_read=40, flops=7, plan="gemv_ro d", scal_invocations=1)
+    tot = ExecutionReport()
+    tot.absorb(_DeferredReport(None, fill))
+    assert tot.bytes_read == 40 and tot.scal_invocations == 1
+    p = pickle.loads(pickle.dumps(_DeferredReport(np.zeros(2), fill)))
+    assert type(p) is ExecutionReport and p.flops == 7
+    assert copy.deepcopy(_DeferredReport(None, fill)).bytes_read == 40
+    r = dataclasses.replace(_DeferredReport(None, fill), flops=9)
+    assert r.flops == 9 and r.bytes_read == 40
+    w = _DeferredReport(None, fill)
+    w.flops += 1
+    assert w.flops == 8 and w.bytes_read == 40
