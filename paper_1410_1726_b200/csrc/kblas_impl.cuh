@@ -1394,7 +1394,14 @@ int hostvec_entry(bool is_gemv, char op, bool herm, int m, int n, T alpha, const
                                                    yin ? ylen * (long long)sizeof(T) : 0);
     launched();
     if ((e = cudaGetLastError()) != cudaSuccess) return (int)e;
-    t_pdl_next = true;
+    // PDL only when x alone is staged: the main kernel reads x after its own
+    // griddepcontrol.wait on the copy-in grid.  A staged y (beta != 0) is
+    // read by the epilogue kernel, a programmatic dependent of the main
+    // kernel only; with the main kernel also launched as a dependent the
+    // epilogue was measured reading stale y staging (tests/
+    // test_gpu_hostvec.py, d = 1001), so then the main kernel waits for
+    // the copy-in grid the ordinary way.
+    t_pdl_next = !yin;
   } else {
     if (xin && (e = cudaMemcpyAsync(dx, hx, xlen * sizeof(T), cudaMemcpyHostToDevice, st)) != cudaSuccess)
       return (int)e;

@@ -89,5 +89,50 @@ for tag in "sdcz":
     ok(f"symv mgpu {tag}", r)
     r = kb.gemv_mgpu("n", 1.0, dist, vec(tag, 600), 0.5, vec(tag, 600))[0].y_out
     ok(f"gemv mgpu {tag}", r)
+# host-vector path: page-locked x / y (copy-in grid + PDL-launched main
+# kernel with the prefetch-before-wait prologue), misaligned pinned views,
+# pageable vectors, and queued calls
+import numpy as np  # noqa: E402
+
+
+def pinned(tag, n, shift=0):
+    p = kb.precision(tag)
+    t = torch.empty(n + shift, dtype=p.torch_dtype, pin_memory=True)
+    (torch.view_as_real(t) if p.is_complex else t).uniform_(-1, 1)
+    return t.numpy()[shift:]
+
+
+def ok_np(name, a):
+    global bad
+    if not np.isfinite(a).all():
+        print("non-finite:", name)
+        bad += 1
+
+
+for tag in "sdcz":
+    herm = tag in "cz"
+    for m, n, ld, ro in ((333, 517, 352, 3), (4100, 77, 4128, 5), (2048, 2048, 2048, 0)):
+        A = mat(tag, m, n, ld, ro)
+        for trans in "ntc":
+            xl, yl = (n, m) if trans == "n" else (m, n)
+            for shift in (0, 1):
+                for beta in (0.0, 0.25):
+                    r = kb.gemv(trans, 0.5, A, pinned(tag, xl, shift), beta, pinned(tag, yl, shift)).y_out
+                    ok_np(f"hostvec gemv {tag} {trans} shift={shift} beta={beta}", r)
+            r = kb.gemv(trans, 0.5, A, pinned(tag, xl).copy(), 0.25, pinned(tag, yl).copy()).y_out
+            ok_np(f"hostvec gemv pageable {tag} {trans}", r)
+    d, ld, ro = 700, 736, 5
+    A = mat(tag, d + 1, d + 1, ld, ro).submatrix(0, 0, d, d)
+    for uplo in "lu":
+        for beta in (0.0, 0.25):
+            r = kb.symv_hemv(uplo, 0.5, kb.HermitianView(A, uplo), pinned(tag, d, 1), beta, pinned(tag, d),
+                             hermitian=herm).y_out
+            ok_np(f"hostvec symv {tag} {uplo} beta={beta}", r)
+    q = kb.CommandQueue()
+    hs = [kb.gemv_async("n", 1.0, A, pinned(tag, d), 0.0, np.zeros(d, dtype=kb.precision(tag).dtype), queue=q)
+          for _ in range(4)]
+    q.synchronize()
+    for h in hs:
+        ok_np(f"hostvec queued {tag}", h.result().y_out)
 print("sanitize probe done, bad =", bad)
 sys.exit(1 if bad else 0)

@@ -56,7 +56,9 @@ def same(got, want):
     got = np.asarray(got)
     want = want.cpu().numpy() if isinstance(want, torch.Tensor) else np.asarray(want)
     assert got.dtype == want.dtype and got.shape == want.shape
-    assert np.array_equal(got, want, equal_nan=True), float(np.max(np.abs(got - want)))
+    bad = np.nonzero(got != want)[0]
+    assert bad.size == 0, (f"{bad.size} of {got.size} differ, first {bad[:5].tolist()}, last {bad[-5:].tolist()}, "
+                           f"max {float(np.max(np.abs(got - want)))}")
 
 
 @pytest.mark.parametrize("tag", "sdcz")
