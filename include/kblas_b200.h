@@ -403,10 +403,13 @@ int kblas_getmatrix_async(int rows, int cols, size_t esize, const void *dA, int 
 /* offsets (offset_r, offset_c) as kblas_xgemv_offset) or 's'           */
 /* (symv/hemv: op = uplo, hermitian selects HEMV for c/z, offset_r ==   */
 /* offset_c = the diagonal offset).  alpha/beta point to one scalar of  */
-/* the precision.  y_in may be NULL when *beta == 0.  Enqueues the      */
-/* H2D copies, the kernels and the D2H copy on `stream` and waits for  */
-/* it.  Same return codes as the entry points it wraps (-1: bad vector  */
-/* arguments).  Replaces blockmv's numpy-in/numpy-out call shape        */
+/* the precision.  y_in may be NULL when *beta == 0.  Enqueues on      */
+/* `stream`: the staging of x (and y_in) -- a copy-in kernel reading    */
+/* page-locked host memory through its device mapping, or cudaMemcpy-  */
+/* Async for pageable memory --, the kernels, and the result write     */
+/* (straight into page-locked y_out when *beta == 0, else a D2H copy),  */
+/* then waits.  Same return codes as the entry points it wraps (-1: bad */
+/* vector arguments).  Replaces blockmv's numpy-in/numpy-out call shape */
 /* (kernels.py:402-440, 443-486; offset.py:83-208).                     */
 int kblas_mv_hostvec(char prec, char kind, char op, int hermitian, int m, int n,
                      const void *alpha, const void *dA, int lda, int offset_r,
