@@ -209,3 +209,52 @@ def test_hostvec_report_counters():
     for f in ("bytes_read", "bytes_written", "transactions", "matrix_transactions", "flops", "tb_count",
               "reduction_events", "scal_invocations", "plan"):
         assert getattr(rep, f) == getattr(dev, f), f
+
+
+# property form: random shapes, views, scalars and vector memory kinds
+from hypothesis import HealthCheck, given, settings  # noqa: E402
+from hypothesis import strategies as st  # noqa: E402
+
+
+@settings(max_examples=120, deadline=None, derandomize=True,
+          suppress_health_check=[HealthCheck.too_slow, HealthCheck.function_scoped_fixture])
+@given(tag=st.sampled_from("sdcz"), kind=st.sampled_from(["gemv", "symv"]), m=st.integers(1, 3000),
+       n=st.integers(1, 3000), op=st.sampled_from("ntclu"), mem=st.sampled_from(["pinned", "shifted", "pageable"]),
+       alpha=st.sampled_from([1.0, -0.5, 2.25]), beta=st.sampled_from([0.0, 1.0, -0.75]),
+       queued=st.booleans(), seed=st.integers(0, 2 ** 16))
+def test_hostvec_property(tag, kind, m, n, op, mem, alpha, beta, queued, seed):
+    """Any shape and op: the numpy-vector call (sync or queued) gives the
+    device-tensor call's result bit for bit."""
+    rng = np.random.default_rng(seed)
+    if kind == "symv":
+        n = m
+        op = op if op in "lu" else "l"
+    else:
+        op = op if op in "ntc" else "n"
+    v, _ = dev_view(rng, m, n, tag, host=False)
+    xl, yl = (m, m) if kind == "symv" else ((n, m) if op == "n" else (m, n))
+    x, y = naive.fill(rng, xl, tag), naive.fill(rng, yl, tag)
+    conv = {"pinned": pinned, "shifted": lambda a: pinned(a, 1), "pageable": lambda a: a.copy()}[mem]
+    hx, hy = conv(x), conv(y)
+    herm = tag in "cz"
+    dx, dy = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+    if kind == "symv":
+        hv = kb.HermitianView(v, op)
+        want = kb.symv_hemv(op, alpha, hv, dx, beta, dy, hermitian=herm).y_out
+        if queued:
+            q = kb.CommandQueue()
+            h = kb.symv_hemv_async(op, alpha, hv, hx, beta, hy, queue=q, hermitian=herm)
+            q.synchronize()
+            got = h.result().y_out
+        else:
+            got = kb.symv_hemv(op, alpha, hv, hx, beta, hy, hermitian=herm).y_out
+    else:
+        want = kb.gemv(op, alpha, v, dx, beta, dy).y_out
+        if queued:
+            q = kb.CommandQueue()
+            h = kb.gemv_async(op, alpha, v, hx, beta, hy, queue=q)
+            q.synchronize()
+            got = h.result().y_out
+        else:
+            got = kb.gemv(op, alpha, v, hx, beta, hy).y_out
+    same(got, want)
