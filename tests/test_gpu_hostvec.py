@@ -9,6 +9,8 @@ kernels), for every op and precision, misaligned page-locked views
 (4-byte copy path) included, and back-to-back queued calls must not see
 each other's staging."""
 
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -216,7 +218,8 @@ from hypothesis import HealthCheck, given, settings  # noqa: E402
 from hypothesis import strategies as st  # noqa: E402
 
 
-@settings(max_examples=120, deadline=None, derandomize=True,
+@settings(max_examples=int(os.environ.get("KB_HYP_EXAMPLES", 120)), deadline=None,
+          derandomize=not os.environ.get("KB_HYP_RANDOM"),
           suppress_health_check=[HealthCheck.too_slow, HealthCheck.function_scoped_fixture])
 @given(tag=st.sampled_from("sdcz"), kind=st.sampled_from(["gemv", "symv"]), m=st.integers(1, 3000),
        n=st.integers(1, 3000), op=st.sampled_from("ntclu"), mem=st.sampled_from(["pinned", "shifted", "pageable"]),

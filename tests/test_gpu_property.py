@@ -6,6 +6,8 @@ the fixed-shape tests with the combinations nobody thought to write down
 (the reference's test_acceptance.py c1 sweep does the same on its
 simulator)."""
 
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -18,7 +20,9 @@ from paper_1410_1726_b200 import _lib
 
 pytestmark = pytest.mark.gpu
 
-SETTINGS = settings(max_examples=150, deadline=None, derandomize=True,
+# KB_HYP_EXAMPLES / KB_HYP_RANDOM=1: longer, randomised stress runs
+SETTINGS = settings(max_examples=int(os.environ.get("KB_HYP_EXAMPLES", 150)), deadline=None,
+                    derandomize=not os.environ.get("KB_HYP_RANDOM"),
                     suppress_health_check=[HealthCheck.too_slow, HealthCheck.function_scoped_fixture])
 
 
