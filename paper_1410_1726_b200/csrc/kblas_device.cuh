@@ -181,19 +181,48 @@ __device__ __forceinline__ void ld_pack(Pack<T, V> &a, const T *p, bool pred, ui
 // V consecutive elements of a vector operand (x): cached in L1 (every warp of
 // a CTA reads the same rows) and kept in L2 (every CTA of a column range
 // does).  One 256-bit load when V * sizeof(T) == 32 (p 32-byte aligned).
+// x (and y_in) reads of a streaming kernel: ordinary coherent loads, never
+// ld.global.nc.  A main kernel launched as the programmatic dependent of
+// the host-vector copy-in grid may read x only after griddepcontrol.wait;
+// ptxas treats .nc loads as reads of invariant memory and was seen hoisting
+// them above the wait (SASS LDG.E.CONSTANT ahead of ACQBULK, stale x in
+// tests/test_gpu_hostvec.py).  The loads are volatile asm, so nvvm keeps
+// them after the wait's (volatile) asm; ptxas keeps coherent loads after
+// ACQBULK.
+__device__ __forceinline__ float ld_x(const float *p) {
+  float v;
+  asm volatile("ld.global.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double ld_x(const double *p) {
+  double v;
+  asm volatile("ld.global.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ float2 ld_x(const float2 *p) {
+  float2 v;
+  asm volatile("ld.global.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double2 ld_x(const double2 *p) {
+  double2 v;
+  asm volatile("ld.global.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+
 template <class T, int V>
 __device__ __forceinline__ void ld_xvec(T (&out)[V], const T *p) {
   if constexpr (V * sizeof(T) == 32) {
     Pack<T, V> a;
-    asm("ld.global.nc.L2::evict_last.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-        : "=r"(a.w[0]), "=r"(a.w[1]), "=r"(a.w[2]), "=r"(a.w[3]), "=r"(a.w[4]), "=r"(a.w[5]), "=r"(a.w[6]),
-          "=r"(a.w[7])
-        : "l"(p));
+    asm volatile("ld.global.L2::evict_last.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(a.w[0]), "=r"(a.w[1]), "=r"(a.w[2]), "=r"(a.w[3]), "=r"(a.w[4]), "=r"(a.w[5]),
+                   "=r"(a.w[6]), "=r"(a.w[7])
+                 : "l"(p));
 #pragma unroll
     for (int v = 0; v < V; ++v) out[v] = a.v(v);
   } else {
 #pragma unroll
-    for (int v = 0; v < V; ++v) out[v] = __ldg(p + v);
+    for (int v = 0; v < V; ++v) out[v] = ld_x(p + v);
   }
 }
 

@@ -188,7 +188,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) kblas_gemv_n_kernel(const GemvP
         const int col = c0 + j;
         const bool cok = col < p.n;
         const long long gx = contiguous ? g0 + j : map_col(p.cm, col);
-        xv[j] = cok ? __ldg(x + gx) : zero<T>();
+        xv[j] = cok ? ld_x(x + gx) : zero<T>();
         const T *colp = A + (long long)col * p.lda + pw + lane * V;
 #pragma unroll
         for (int r = 0; r < R; ++r) ld_pack(a[j][r], colp + r * 32 * V, cok && rok[r], pol);
@@ -295,7 +295,7 @@ __global__ void __launch_bounds__(NW * 32, 2) kblas_gemv_ns_kernel(const GemvPar
     for (int j = 0; j < CW; ++j) {
       const int col = g + j;
       const bool cok = col < c1;
-      xv[j] = cok ? __ldg(x + map_col(p.cm, col)) : zero<T>();
+      xv[j] = cok ? ld_x(x + map_col(p.cm, col)) : zero<T>();
       ld_pack(a[j], A + (long long)col * p.lda + pw + lane * V, cok && rok, pol);
     }
   };
@@ -384,7 +384,7 @@ __global__ void __launch_bounds__(NW * 32) kblas_gemv_ro_kernel(const GemvParams
     for (int u = 0; u < U; ++u) {
       const int col = c + u * STEP;
       const bool cok = col < p.n;
-      xv[u] = cok ? __ldg(x + map_col(p.cm, col)) : zero<T>();
+      xv[u] = cok ? ld_x(x + map_col(p.cm, col)) : zero<T>();
       ld_pack(a[u], A + (long long)col * p.lda + pw, cok && rok, pol);
     }
 #pragma unroll
@@ -448,7 +448,7 @@ __global__ void __launch_bounds__(NW * 32, 2) kblas_gemv_nc_kernel(const GemvPar
     for (int j = 0; j < CW; ++j) {
       const int col = g + j;
       const bool cok = col < c1;
-      xv[j] = cok ? __ldg(x + map_col(p.cm, col)) : zero<T>();
+      xv[j] = cok ? ld_x(x + map_col(p.cm, col)) : zero<T>();
       ld_pack(a[j], A + (long long)col * p.lda + pw + lane * V, cok && rok, pol);
     }
   };
@@ -542,7 +542,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) kblas_gemv_t_kernel(const GemvP
 #pragma unroll
           for (int v = 0; v < V; ++v) {
             const long long i = i0 + v;
-            xr[r][v] = (i >= 0 && i < p.m) ? __ldg(x + i) : zero<T>();
+            xr[r][v] = (i >= 0 && i < p.m) ? ld_x(x + i) : zero<T>();
           }
         }
       }
@@ -650,7 +650,7 @@ __global__ void __launch_bounds__(NW * 32, 2) kblas_gemv_tc_kernel(const GemvPar
       ld_xvec<T, V>(xr, x + i0);
     } else {
 #pragma unroll
-      for (int v = 0; v < V; ++v) xr[v] = (i0 + v >= 0 && i0 + v < p.m) ? __ldg(x + i0 + v) : zero<T>();
+      for (int v = 0; v < V; ++v) xr[v] = (i0 + v >= 0 && i0 + v < p.m) ? ld_x(x + i0 + v) : zero<T>();
     }
 #pragma unroll
     for (int j = 0; j < CB; ++j) ld_pack(a[j], Ac + (long long)j * p.lda + ps, col0 + j < p.n && ps < plimit, pol);
@@ -883,7 +883,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) kblas_symv_kernel(const SymPara
 #pragma unroll
         for (int v = 0; v < V; ++v) {
           const int ps = ps0 + v;
-          xr[r][v] = (ps >= vlo && ps < vhi) ? __ldg(x + (ps - p.lead)) : zero<T>();
+          xr[r][v] = (ps >= vlo && ps < vhi) ? ld_x(x + (ps - p.lead)) : zero<T>();
         }
       }
     }
@@ -914,11 +914,11 @@ __global__ void __launch_bounds__(NW * 32, MINB) kblas_symv_kernel(const SymPara
   auto set_xc = [&](const SymTile &t) {
     if constexpr (XS) {
       __syncwarp();
-      if (lane < CW) xs_buf[cl + lane] = (cl + lane < t.ncols) ? __ldg(x + t.gcol0 + cl + lane) : zero<T>();
+      if (lane < CW) xs_buf[cl + lane] = (cl + lane < t.ncols) ? ld_x(x + t.gcol0 + cl + lane) : zero<T>();
       __syncwarp();
     } else {
 #pragma unroll
-      for (int j = 0; j < CW; ++j) xr_c[j] = (cl + j < t.ncols) ? __ldg(x + t.gcol0 + cl + j) : zero<T>();
+      for (int j = 0; j < CW; ++j) xr_c[j] = (cl + j < t.ncols) ? ld_x(x + t.gcol0 + cl + j) : zero<T>();
     }
   };
   auto xcj = [&](int j) -> T {

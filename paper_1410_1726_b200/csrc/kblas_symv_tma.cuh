@@ -150,7 +150,7 @@ __global__ void __launch_bounds__((NC + 2) * 32, 1)
     T xc[CW], t2[CW];
 #pragma unroll
     for (int j = 0; j < CW; ++j) {
-      xc[j] = (cl + j < tl.ncols) ? __ldg(x + tl.gcol0 + cl + j) : zero<T>();
+      xc[j] = (cl + j < tl.ncols) ? ld_x(x + tl.gcol0 + cl + j) : zero<T>();
       t2[j] = zero<T>();
     }
     for (; !c.done && c.k == k && c.s == seg; c.advance(p), ++qi) {
@@ -166,7 +166,7 @@ __global__ void __launch_bounds__((NC + 2) * 32, 1)
         for (int v = 0; v < VE; ++v) {
           const long long i = r0 + (r * 32 + lane) * VE + v;
           ok[r][v] = i >= tl.row0 && i < tl.row1;
-          xr[r][v] = ok[r][v] ? __ldg(x + i) : zero<T>();
+          xr[r][v] = ok[r][v] ? ld_x(x + i) : zero<T>();
         }
       mbar_wait(&full[s], (uint32_t)(qi / S) & 1);
       const T *box = boxes + (size_t)s * W * HS + (size_t)cl * HS + lane * VE;

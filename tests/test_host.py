@@ -3,6 +3,7 @@ validation mirrored from the reference, layout/partition arithmetic, the
 algorithmic byte/flop counts, and the C-ABI library surface."""
 
 import ctypes
+import os
 
 import numpy as np
 import pytest
@@ -311,3 +312,31 @@ def test_deferred_report_behaves_like_execution_report():
     w = _DeferredReport(None, fill)
     w.flops += 1
     assert w.flops == 8 and w.bytes_read == 40
+
+
+def test_no_noncoherent_x_loads_before_griddepcontrol_wait():
+    """A main kernel launched as the programmatic dependent of the
+    host-vector copy-in grid may read x only after griddepcontrol.wait.
+    ptxas hoists ld.global.nc loads above the wait (SASS LDG.E.CONSTANT
+    ahead of ACQBULK), so x is read with coherent loads (kblas_device.cuh
+    ld_x / ld_xvec); this checks the shipped SASS: before ACQBULK the only
+    non-coherent loads are the A stream's (.NA, L1::no_allocate)."""
+    import re
+    import shutil
+    import subprocess
+
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(tool):
+        pytest.skip("cuobjdump not available")
+    sass = subprocess.run([tool, "-sass", _lib.LIB_PATH], capture_output=True, text=True, check=True).stdout
+    checked, bad = 0, []
+    for fn in re.split(r"\n\s+Function : ", sass)[1:]:
+        if "ACQBULK" not in fn:
+            continue
+        checked += 1
+        name = fn.split("\n", 1)[0].strip()
+        for op in re.findall(r"LDG\.[A-Z0-9.]+", fn[: fn.index("ACQBULK")]):
+            if "CONSTANT" in op and ".NA" not in op:
+                bad.append((name[:80], op))
+    assert checked >= 100, checked
+    assert bad == [], bad[:5]
