@@ -261,3 +261,46 @@ def test_hostvec_property(tag, kind, m, n, op, mem, alpha, beta, queued, seed):
         else:
             got = kb.gemv(op, alpha, v, hx, beta, hy).y_out
     same(got, want)
+
+
+def test_threads_share_a_stream():
+    """Four host threads issue numpy-vector calls on the same (default)
+    stream at once: each call's acquire-and-launch sequence holds the
+    per-(device, stream) lock, so the shared staging buffer and workspace
+    are never interleaved, and every result is its own."""
+    import threading
+
+    rng = np.random.default_rng(108)
+    n = 2048
+    v, _ = dev_view(rng, n, n, "d", host=False)
+    hv = kb.HermitianView(v, "l")
+    xs = [naive.fill(rng, n, "d") for _ in range(4)]
+    wants = []
+    for x in xs:
+        xd = torch.from_numpy(x).cuda()
+        z = torch.zeros(n, dtype=torch.float64, device="cuda")
+        wants.append((kb.gemv("n", 1.0, v, xd, 0.0, z).y_out.cpu().numpy(),
+                      kb.symv_hemv("l", 1.0, hv, xd, 0.0, z).y_out.cpu().numpy()))
+    errors = []
+
+    def work(t):
+        try:
+            hx = pinned(xs[t], t % 2)
+            for i in range(50):
+                if i % 2:
+                    got = kb.symv_hemv("l", 1.0, hv, hx, 0.0, np.zeros(n)).y_out
+                    ok = np.array_equal(got, wants[t][1])
+                else:
+                    got = kb.gemv("n", 1.0, v, hx, 0.0, np.zeros(n)).y_out
+                    ok = np.array_equal(got, wants[t][0])
+                if not ok:
+                    errors.append((t, i))
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append((t, repr(e)))
+
+    threads = [threading.Thread(target=work, args=(t,)) for t in range(4)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    assert errors == []
