@@ -224,9 +224,10 @@ from hypothesis import strategies as st  # noqa: E402
 @given(tag=st.sampled_from("sdcz"), kind=st.sampled_from(["gemv", "symv"]), m=st.integers(1, 3000),
        n=st.integers(1, 3000), op=st.sampled_from("ntclu"), mem=st.sampled_from(["pinned", "shifted", "pageable"]),
        alpha=st.sampled_from([1.0, -0.5, 2.25]), beta=st.sampled_from([0.0, 1.0, -0.75]),
-       queued=st.booleans(), seed=st.integers(0, 2 ** 16))
-def test_hostvec_property(tag, kind, m, n, op, mem, alpha, beta, queued, seed):
-    """Any shape and op: the numpy-vector call (sync or queued) gives the
+       queued=st.booleans(), off=st.sampled_from([0, 0, 1, 7, 13]), seed=st.integers(0, 2 ** 16))
+def test_hostvec_property(tag, kind, m, n, op, mem, alpha, beta, queued, off, seed):
+    """Any shape and op: the numpy-vector call (sync or queued; off > 0:
+    the offset API on a parent `off` rows/columns larger) gives the
     device-tensor call's result bit for bit."""
     rng = np.random.default_rng(seed)
     if kind == "symv":
@@ -234,6 +235,23 @@ def test_hostvec_property(tag, kind, m, n, op, mem, alpha, beta, queued, seed):
         op = op if op in "lu" else "l"
     else:
         op = op if op in "ntc" else "n"
+    if off:
+        queued = False  # the offset API has no queued form
+        pv, _ = dev_view(rng, m + off, n + off, tag, host=False)
+        xl, yl = (m, m) if kind == "symv" else ((n, m) if op == "n" else (m, n))
+        x, y = naive.fill(rng, xl, tag), naive.fill(rng, yl, tag)
+        conv = {"pinned": pinned, "shifted": lambda a: pinned(a, 1), "pageable": lambda a: a.copy()}[mem]
+        dx, dy = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+        if kind == "symv":
+            hv = kb.HermitianView(pv, op)
+            want = kb.symv_hemv_offset(op, alpha, hv, off, m, dx, beta, dy).y_out
+            got = kb.symv_hemv_offset(op, alpha, hv, off, m, conv(x), beta, conv(y)).y_out
+        else:
+            req = kb.OffsetRequest(pv, off, off // 2, m, n)
+            want = kb.gemv_offset(op, alpha, req, dx, beta, dy).y_out
+            got = kb.gemv_offset(op, alpha, req, conv(x), beta, conv(y)).y_out
+        same(got, want)
+        return
     v, _ = dev_view(rng, m, n, tag, host=False)
     xl, yl = (m, m) if kind == "symv" else ((n, m) if op == "n" else (m, n))
     x, y = naive.fill(rng, xl, tag), naive.fill(rng, yl, tag)
