@@ -39,6 +39,7 @@ from .multidevice import (
 from .offset import OffsetRequest, effective_dims, gemv_offset, symv_hemv_offset
 from .partition import KernelConfig, tb_share
 from .roofline import byte_count, flop_count
+from .stages import KernelRequest, run_diag_block, run_gemv_n, run_gemv_t, run_scal, run_symv_offdiag
 
 __version__ = "0.1.0"
 
@@ -51,6 +52,7 @@ __all__ = [
     "ExecutionReport",
     "HermitianView",
     "KernelConfig",
+    "KernelRequest",
     "MatrixView",
     "OffsetRequest",
     "Op",
@@ -74,6 +76,11 @@ __all__ = [
     "precision",
     "precision_of",
     "required_local_elements",
+    "run_diag_block",
+    "run_gemv_n",
+    "run_gemv_t",
+    "run_scal",
+    "run_symv_offdiag",
     "symv",
     "symv_hemv",
     "symv_hemv_async",

@@ -340,3 +340,25 @@ def test_no_noncoherent_x_loads_before_griddepcontrol_wait():
                 bad.append((name[:80], op))
     assert checked >= 100, checked
     assert bad == [], bad[:5]
+
+
+def test_kernel_request_validation():
+    """KernelRequest keeps the reference's checks and messages
+    (kernels.py:74-89)."""
+    import paper_1410_1726_b200 as kb
+
+    v = MatrixView(np.zeros(12), 3, 4, 3, precision("d"))
+    cfg = kb.KernelConfig(64, 4)
+    kb.KernelRequest(kb.Op.GEMV_N, v, np.zeros(4), np.zeros(3), 1.0, 0.0, cfg)
+    kb.KernelRequest(kb.Op.GEMV_T, v, np.zeros(3), np.zeros(4), 1.0, 0.0, cfg)
+    with pytest.raises(ValueError, match="x has length 3, expected 4"):
+        kb.KernelRequest(kb.Op.GEMV_N, v, np.zeros(3), np.zeros(3), 1.0, 0.0, cfg)
+    with pytest.raises(ValueError, match="y has length 4, expected 3"):
+        kb.KernelRequest(kb.Op.GEMV_N, v, np.zeros(4), np.zeros(4), 1.0, 0.0, cfg)
+    with pytest.raises(ValueError, match="symmetric ops need a square matrix, got 3x4"):
+        kb.KernelRequest(kb.Op.SYMV_LOWER, v, np.zeros(4), np.zeros(4), 1.0, 0.0, cfg)
+    sq = MatrixView(np.zeros(9), 3, 3, 3, precision("d"))
+    with pytest.raises(ValueError, match="require a HermitianView"):
+        kb.KernelRequest(kb.Op.SYMV_LOWER, sq, np.zeros(3), np.zeros(3), 1.0, 0.0, cfg)
+    r = kb.KernelRequest(kb.Op.SYMV_LOWER, kb.HermitianView(sq, "l"), np.zeros(3), np.zeros(3), 1.0, 0.0, cfg)
+    assert r.view is sq and r.precision.tag == "d"
