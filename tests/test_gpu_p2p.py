@@ -82,3 +82,19 @@ def test_p2p_exchange_world2_one_gpu(kind, op, tag):
         assert p.exitcode == 0
     tol = 1e-5 if tag in "sc" else 1e-12
     assert q.get(timeout=5) < tol
+
+
+@pytest.mark.parametrize("kind,op,tag", [("s", "l", "d"), ("g", "n", "z")])
+def test_p2p_exchange_world4_one_gpu(kind, op, tag):
+    """Four ranks (the SCALE run's N=4 shape): the root sums three peers'
+    slots in rank order and releases them for the next call."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 4, port, kind, op, tag, q)) for r in range(4)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(300)
+        assert p.exitcode == 0
+    assert q.get(timeout=5) < 1e-12
