@@ -874,3 +874,52 @@ def test_cuda_graph_capture_after_warmup():
         graph.replay()
     torch.cuda.synchronize()
     assert torch.equal(y, want_s) and torch.equal(g_out, want_g)
+
+
+def test_threads_on_their_own_streams():
+    """Four host threads, each on its own CUDA stream, issue device-tensor
+    GEMV / SYMV calls of different shapes concurrently: workspaces and
+    tile tables are per (device, stream) / per shape, so every result
+    equals the same call made alone."""
+    import threading
+
+    rng = np.random.default_rng(77)
+    shapes = [("d", 3000, 2000), ("z", 1500, 1500), ("s", 5000, 300), ("c", 2048, 2048)]
+    cases = []
+    for tag, m, n in shapes:
+        v, _ = dev_matrix(rng, m, n, tag, ld=-(-m // 32) * 32)
+        sq, _ = dev_matrix(rng, n, n, tag, ld=-(-n // 32) * 32)
+        x, xs, y = dvec(naive.fill(rng, n, tag)), dvec(naive.fill(rng, n, tag)), dvec(naive.fill(rng, m, tag))
+        herm = tag in "cz"
+        want_g = kb.gemv("n", 0.5, v, x, -1.0, y).y_out
+        want_s = kb.symv_hemv("l", 0.5, kb.HermitianView(sq, "l"), xs, 0.0, torch.zeros_like(xs),
+                              hermitian=herm).y_out
+        torch.cuda.synchronize()
+        cases.append((v, sq, x, xs, y, herm, want_g, want_s))
+    errors = []
+
+    def work(t):
+        v, sq, x, xs, y, herm, want_g, want_s = cases[t]
+        st = torch.cuda.Stream()
+        try:
+            with torch.cuda.stream(st):
+                for i in range(40):
+                    if i % 2:
+                        got = kb.symv_hemv("l", 0.5, kb.HermitianView(sq, "l"), xs, 0.0, torch.zeros_like(xs),
+                                           hermitian=herm).y_out
+                        want = want_s
+                    else:
+                        got = kb.gemv("n", 0.5, v, x, -1.0, y).y_out
+                        want = want_g
+                    st.synchronize()
+                    if not torch.equal(got, want):
+                        errors.append((t, i))
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append((t, repr(e)))
+
+    threads = [threading.Thread(target=work, args=(t,)) for t in range(4)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    assert errors == []
