@@ -14,7 +14,6 @@ import threading
 import numpy as np
 import torch
 
-from . import _hostcall as _HC
 from . import _lib
 from .core import MatrixView, Precision, _is_torch
 
@@ -281,6 +280,27 @@ def _hostvec_operands(prec: Precision, x, x_len: int, alpha, beta, y, y_len: int
     return xa, alpha, beta, ya
 
 
+_HC_MOD = None
+
+
+def hostcall():
+    """The CPython binding of kblas_mv_hostvec (csrc/kblas_hostcall.cpp,
+    built in-tree next to libkblas_b200.so).  Imported on first use so the
+    package (and its build module) imports before anything is built; a
+    missing binding raises here, there is no other path."""
+    global _HC_MOD
+    if _HC_MOD is None:
+        try:
+            from . import _hostcall
+        except ImportError as e:
+            raise ImportError(
+                f"paper_1410_1726_b200/_hostcall is missing or cannot load ({e}): build it with "
+                "`python -m paper_1410_1726_b200._build` (there is no CPU fallback)"
+            ) from e
+        _HC_MOD = _hostcall
+    return _HC_MOD
+
+
 def call_hostvec(prec: Precision, kind: str, op: str, hermitian: bool, m: int, n: int, alpha, a_ptr: int,
                  lda: int, x, x_len: int, beta, y, y_len: int, device, off_r: int = 0, off_c: int = 0,
                  keep: list | None = None):
@@ -298,6 +318,7 @@ def call_hostvec(prec: Precision, kind: str, op: str, hermitian: bool, m: int, n
     `keep`, which the caller holds until its queue synchronises.  The
     result buffer comes from the same pool; it is not handed out again
     while the returned array (held by the queue's handle) is alive."""
+    _HC = hostcall()
     out, out_np = _PINNED.get(y_len, prec.torch_dtype)
     sync = keep is None
     herm = 1 if hermitian else 0

@@ -236,7 +236,7 @@ class TestHostcallBinding:
         from paper_1410_1726_b200 import _ops
 
         _lib.load()
-        assert _ops._HC.last_plan() == _lib.last_plan()
+        assert _ops.hostcall().last_plan() == _lib.last_plan()
         maps = [ln.split() for ln in open("/proc/self/maps") if "libkblas_b200.so" in ln]
         assert maps, "libkblas_b200.so is not mapped"
         assert sum(1 for f in maps if int(f[2], 16) == 0) == 1  # one load of the file
@@ -253,13 +253,13 @@ class TestHostcallBinding:
     def test_off_path_operands(self, x, alpha, y):
         from paper_1410_1726_b200 import _ops
 
-        hc = _ops._HC
+        hc = _ops.hostcall()
         assert hc.mv_hostvec("d", "g", "n", 0, 4, 4, alpha, 0, 4, 0, 0, x, 4, 0.0, y, 4, 0, 0, True) == hc.SLOW_PATH
 
     def test_beta_nonzero_checks_y_dtype(self):
         from paper_1410_1726_b200 import _ops
 
-        hc = _ops._HC
+        hc = _ops.hostcall()
         y32 = np.zeros(4, np.float32)
         assert hc.mv_hostvec("d", "g", "n", 0, 4, 4, 1.0, 0, 4, 0, 0, np.zeros(4), 4, 0.5, y32, 4, 0, 0,
                              True) == hc.SLOW_PATH
