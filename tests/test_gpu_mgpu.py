@@ -217,3 +217,52 @@ class TestFullSizeConfig5:
         # beta path: y_out = beta*y + A x
         r = kb.symv_hemv_mgpu("l", 1.0, dist, x, -0.5, y, cfg)[0].y_out
         assert (r - (ax - 0.5 * y)).abs().max().item() <= 4 * eps * float((ax.abs() + y.abs()).max())
+
+
+# property form: random shapes, block widths, GPU counts, reduce modes,
+# scalars and vector kinds against the single-GPU API
+import os  # noqa: E402
+
+from hypothesis import HealthCheck, given, settings  # noqa: E402
+from hypothesis import strategies as st  # noqa: E402
+
+
+@settings(max_examples=int(os.environ.get("KB_HYP_EXAMPLES", 60)), deadline=None,
+          derandomize=not os.environ.get("KB_HYP_RANDOM"),
+          suppress_health_check=[HealthCheck.too_slow, HealthCheck.function_scoped_fixture])
+@given(tag=st.sampled_from("sdcz"), kind=st.sampled_from(["gemv", "symv"]), m=st.integers(1, 1500),
+       n=st.integers(1, 1500), nb_pow=st.integers(4, 8), devices=st.integers(1, 8),
+       op=st.sampled_from("ntclu"), reduce=st.sampled_from(["ordered", "nccl"]),
+       beta=st.sampled_from([0.0, 1.0, -0.5]), numpy_vecs=st.booleans(), seed=st.integers(0, 2 ** 16))
+def test_mgpu_property(tag, kind, m, n, nb_pow, devices, op, reduce, beta, numpy_vecs, seed):
+    rng = np.random.default_rng(seed)
+    nb = 1 << nb_pow
+    if kind == "symv":
+        n = m
+        op = op if op in "lu" else "l"
+    else:
+        op = op if op in "ntc" else "n"
+    v, a = dev_matrix(rng, m, n, tag)
+    xl, yl = (n, m) if (kind == "gemv" and op == "n") else ((m, n) if kind == "gemv" else (m, m))
+    x, y = naive.fill(rng, xl, tag), naive.fill(rng, yl, tag)
+    if not numpy_vecs:
+        x, y = torch.from_numpy(x).cuda(), torch.from_numpy(y).cuda()
+    dist_mat = kb.distribute(v, nb, devices)
+    if kind == "symv":
+        herm = tag in "cz"
+        merged, per = kb.symv_hemv_mgpu(op, 0.8, dist_mat, x, beta, y, kb.KernelConfig(nb, 2), hermitian=herm,
+                                        reduce=reduce)
+        single = kb.symv_hemv(op, 0.8, kb.HermitianView(v, op), x, beta, y, hermitian=herm).y_out
+        dense = np.abs(naive.dense_from_triangle(a, op, herm))
+    else:
+        merged, per = kb.gemv_mgpu(op, 0.8, dist_mat, x, beta, y, reduce=reduce)
+        single = kb.gemv(op, 0.8, v, x, beta, y).y_out
+        dense = np.abs(a) if op == "n" else np.abs(a).T
+    got = merged.y_out.cpu().numpy() if isinstance(merged.y_out, torch.Tensor) else merged.y_out
+    want = single.cpu().numpy() if isinstance(single, torch.Tensor) else single
+    assert type(merged.y_out) is type(single)
+    xh = x.cpu().numpy() if isinstance(x, torch.Tensor) else x
+    yh = y.cpu().numpy() if isinstance(y, torch.Tensor) else y
+    bound = 2 * naive.run_bound(tag, 0.8, dense, xh, beta, yh)
+    assert naive.max_abs_error(got, want) <= bound
+    assert len(per) == devices
