@@ -820,6 +820,30 @@ size_t sym_ws_bytes(int d, int W, const TileTable &tt) {
   return align256((size_t)tt.ntiles * d * sizeof(T)) + align256((size_t)tt.nslots * W * sizeof(T));
 }
 
+// SYMV/HEMV epilogue: 128 rows per CTA (contiguous t1 reads, same sums in
+// the same order) when the tiles are 128-column blocks aligned to 128,
+// else 32 rows per CTA.  $KBLAS_SYMV_EPILOGUE=32 forces the latter (A/B).
+inline bool symv_epilogue_r128_enabled() {
+  static const bool on = [] {
+    const char *e = std::getenv("KBLAS_SYMV_EPILOGUE");
+    return !(e != nullptr && e[0] == '3');
+  }();
+  return on;
+}
+
+template <class T, bool LOWER>
+void launch_symv_epilogue(T *y, const SymParams &p, T alpha, T beta, bool beta_zero, const ColMap &cm, int W,
+                          cudaStream_t st) {
+  const kb::Xchg xg = cm.xg ? *cm.xg : kb::Xchg{};
+  const bool aligned = W == 128 && (p.tile_w == 128 || (p.tile_w == 0 && cm.nb % 128 == 0));
+  if (aligned && symv_epilogue_r128_enabled())
+    launch_pdl(kblas_symv_epilogue_r128<T, LOWER, 16>, (unsigned)cdiv(p.d, 128), 512, st, y, p, alpha, beta,
+               (int)beta_zero, xg);
+  else
+    launch_pdl(kblas_symv_epilogue<T, LOWER, 16>, (unsigned)cdiv(p.d, 32), 512, st, y, p, alpha, beta,
+               (int)beta_zero, xg);
+}
+
 template <class T, int V, int NW, int CW, int R, bool LOWER, bool HERM, int MINB = 1, bool XS = false, int B = 1>
 cudaError_t run_symv(const Path<T> &pa, long long lda, int d, const T *x, ColMap cm, int ncols_local, T *y,
                      T alpha, T beta, bool beta_zero, cudaStream_t st) {
@@ -854,8 +878,7 @@ cudaError_t run_symv(const Path<T> &pa, long long lda, int d, const T *x, ColMap
     e = launch_main(kfn, (unsigned)P, NW * 32, smem, st, p);
   }
   if (e != cudaSuccess) return e;
-  launch_pdl(kblas_symv_epilogue<T, LOWER, 16>, (unsigned)cdiv(d, 32), 512, st, y, p, alpha, beta, (int)beta_zero,
-             cm.xg ? *cm.xg : kb::Xchg{});
+  launch_symv_epilogue<T, LOWER>(y, p, alpha, beta, beta_zero, cm, W, st);
   launched(2);
   char buf[256];
   snprintf(buf, sizeof buf, "symv %s %s %s%s lead=%d d=%d W=%d H=%d B=%d tiles=%d items=%lld P=%lld K=%d rounds=%d slots=%lld",
@@ -960,8 +983,7 @@ cudaError_t run_symv_tma(const T *A00, long long lda, int d, const T *x, ColMap 
     e = launch_main(kfn, (unsigned)P, (NC + 2) * 32, smem, st, map, tp);
   }
   if (e != cudaSuccess) return e;
-  launch_pdl(kblas_symv_epilogue<T, LOWER, 16>, (unsigned)cdiv(d, 32), 512, st, y, tp.sp, alpha, beta,
-             (int)beta_zero, cm.xg ? *cm.xg : kb::Xchg{});
+  launch_symv_epilogue<T, LOWER>(y, tp.sp, alpha, beta, beta_zero, cm, W, st);
   launched(2);
   char buf[256];
   snprintf(buf, sizeof buf, "symv_tma %s %s%s lead=%d d=%d W=%d H=%d S=%d tiles=%d items=%lld P=%lld K=%d rounds=%d slots=%lld smem=%zu",

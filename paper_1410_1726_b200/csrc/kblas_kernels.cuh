@@ -1242,6 +1242,135 @@ __global__ void __launch_bounds__(EW * 32) kblas_symv_epilogue(T *y, const SymPa
   }
 }
 
+// The same sums as kblas_symv_epilogue, added in the same order (so y is
+// bit-identical), for operands whose tiles are 128 columns starting at
+// multiples of 128: the wide kernel's tiles on one GPU, or mgpu block
+// columns with nb % 128 == 0.  One CTA per 128 rows, which is exactly one
+// column block: the block's tile range and owning tile are shared by all
+// its rows, and lane l owns rows 32v + l (v = 0..3), so a warp reads a
+// tile's t1 partials of the block as one contiguous 128-element run
+// (1 KiB for d) instead of 32-element pieces d elements apart.  Measured at
+// DSYMV N = 100000 (ws1 of 310 MB, read from HBM): see DESIGN.md §4.
+template <class T, bool LOWER, int EW>
+__global__ void __launch_bounds__(EW * 32, 2) kblas_symv_epilogue_r128(T *y, const SymParams p, T alpha, T beta,
+                                                              int beta_zero, const Xchg xg) {
+  griddep_wait();
+  if (xg.G > 0 && xg.rank != 0 && xg.seq > 1) {
+    if (threadIdx.x == 0) spin_until(xg.consumed, xg.seq - 1);
+    __syncthreads();
+  }
+  constexpr int RB = 128, VR = RB / 32;
+  constexpr int BATCH = sizeof(T) == 16 ? 2 : 4;
+  __shared__ T part[EW][RB];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const long long r0 = (long long)blockIdx.x * RB;
+  const T *ws1 = static_cast<const T *>(p.ws1);
+  const T *ws2 = static_cast<const T *>(p.ws2);
+  // local tiles with gcol0 <= r0 (= with gcol0 <= any row of the block)
+  int nle;
+  if (p.tile_w > 0) {
+    nle = min(p.ntiles, (int)(r0 / p.tile_w) + 1);
+  } else {
+    int lo = 0, hi = p.ntiles;
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (p.tiles[mid].gcol0 <= r0) lo = mid + 1; else hi = mid;
+    }
+    nle = lo;
+  }
+  SymTile own{};
+  if (nle > 0) own = p.tiles[nle - 1];
+  const bool owned = nle > 0 && own.gcol0 == r0;  // this GPU holds column block r0 / 128
+  int kb, ke;
+  if (LOWER) {
+    kb = 0;
+    ke = nle;
+  } else {
+    kb = owned ? nle - 1 : nle;
+    ke = p.ntiles;
+  }
+  bool ok[VR];
+  long long row[VR];
+#pragma unroll
+  for (int v = 0; v < VR; ++v) {
+    row[v] = r0 + 32 * v + lane;
+    ok[v] = row[v] < p.d;
+  }
+  T acc[VR];
+#pragma unroll
+  for (int v = 0; v < VR; ++v) acc[v] = zero<T>();
+  for (int k = kb + warp; k < ke; k += BATCH * EW) {
+    T t[BATCH][VR];
+#pragma unroll
+    for (int u = 0; u < BATCH; ++u) {
+      const T *src = ws1 + (long long)(k + u * EW) * p.ws1_ld;
+#pragma unroll
+      for (int v = 0; v < VR; ++v) t[u][v] = (k + u * EW < ke && ok[v]) ? src[row[v]] : zero<T>();
+    }
+#pragma unroll
+    for (int u = 0; u < BATCH; ++u)
+      if (k + u * EW < ke) {
+#pragma unroll
+        for (int v = 0; v < VR; ++v) acc[v] = add_(acc[v], t[u][v]);
+      }
+  }
+  // t2: the slot rows of the block's own tile (one per segment)
+  if (owned) {
+    const T *col = ws2 + (long long)own.slot0 * p.ws2_ld;
+    for (int sl = warp; sl < own.nseg; sl += EW) {
+#pragma unroll
+      for (int v = 0; v < VR; ++v)
+        if (ok[v] && 32 * v + lane < own.ncols) acc[v] = add_(acc[v], col[(long long)sl * p.ws2_ld + 32 * v + lane]);
+    }
+  }
+#pragma unroll
+  for (int v = 0; v < VR; ++v) part[warp][32 * v + lane] = acc[v];
+  __syncthreads();
+  const int t = threadIdx.x;
+  const long long i = r0 + t;
+  const bool valid = t < RB && i < p.d;
+  T s = zero<T>();
+  if (valid) {
+    s = part[0][t];
+#pragma unroll
+    for (int w = 1; w < EW; ++w) s = add_(s, part[w][t]);
+  }
+  if (xg.G == 0) {
+    if (valid) store_axpby(y, i, alpha, s, beta, beta_zero);
+    return;
+  }
+  const T r0v = mul_(alpha, s);  // this rank's partial (multidevice.py:224-276)
+  if (xg.rank == 0) {
+    // the other ranks' slots, in rank order (multidevice.py:276), then
+    // beta * y (282-283)
+    if (threadIdx.x == 0)
+      for (int g = 1; g < xg.G; ++g) spin_until(xg.flags + g, xg.seq);
+    __syncthreads();
+    const T *slots = static_cast<const T *>(xg.slots);
+    if (valid) {
+      T r = r0v;
+      for (int g = 1; g < xg.G; ++g) r = add_(r, __ldcv(slots + g * xg.slot_ld + i));
+      if (!beta_zero) r = fma_(beta, static_cast<const T *>(xg.y_in)[i], r);
+      y[i] = r;
+    }
+  } else if (valid) {
+    y[i] = r0v;  // a store into the root's HBM
+  }
+  // the last CTA to finish publishes this rank's arrival (or, on the root,
+  // that every slot has been consumed)
+  __shared__ bool last;
+  if (xg.rank == 0) __threadfence(); else __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    last = atomicAdd(xg.counter, 1u) == gridDim.x - 1;
+    if (last) {
+      *xg.counter = 0u;
+      __threadfence_system();
+      st_release_sys(xg.rank == 0 ? xg.consumed : xg.flags + xg.rank, xg.seq);
+    }
+  }
+}
+
 // Stages a numpy-vector call's x (and y when beta != 0) from page-locked
 // host memory, mapped into the device address space, into the call's
 // device staging buffer (replaces two cudaMemcpyAsync H2D copies and their
