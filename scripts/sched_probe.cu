@@ -52,11 +52,13 @@ __device__ __forceinline__ int tile_of(const Tile *tiles, int ntiles, long long 
   return lo;
 }
 
-// MODE 0 static, 1 interleaved, 2 dynamic
+// MODE 0 static, 1 interleaved, 2 dynamic, 3 hybrid (interleaved for the
+// first s_static segments, the rest taken from the counter)
 template <int MODE, bool F32>
 __global__ void __launch_bounds__(NW * 32, 1) sched(const char *A, long long ld, int n, const Tile *tiles,
                                                     int ntiles, long long total, int P, int K, unsigned *ctr,
-                                                    const int *seg_tile, double *out, unsigned long long *tend) {
+                                                    const int *seg_tile, double *out, unsigned long long *tend,
+                                                    long long s_static) {
   constexpr int EB = F32 ? 4 : 8, H = 32 * 32 / EB;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __shared__ int s_next[2];
@@ -72,12 +74,19 @@ __global__ void __launch_bounds__(NW * 32, 1) sched(const char *A, long long ld,
     q = seg * K;
     hi = min(total, q + K);
     if (seg >= nseg) q = hi = total;
-  } else {
+  } else if (MODE == 2) {
     seg = blockIdx.x;  // first segment: static
     q = seg * K;
     hi = min(total, q + K);
     if (seg >= nseg) q = hi = total;
     if (threadIdx.x == 0) grabbed = P + atomicAdd(ctr, 1u);  // one segment ahead
+  } else {
+    seg = blockIdx.x;
+    q = seg * K;
+    hi = min(total, q + K);
+    if (seg >= nseg) q = hi = total;
+    if (threadIdx.x == 0)
+      grabbed = seg + P < s_static ? (unsigned)(seg + P) : (unsigned)(s_static + atomicAdd(ctr, 1u));
   }
   double acc = 0.0;
   uint32_t a[CW][8];
@@ -103,9 +112,9 @@ __global__ void __launch_bounds__(NW * 32, 1) sched(const char *A, long long ld,
 #pragma unroll
       for (int v = 0; v < 8; v += 2)
         acc = fma(__hiloint2double((int)a[j][v + 1], (int)a[j][v]), 1.0000001, acc);
-    if (MODE == 2 && threadIdx.x == 0 && q == seg * K) s_next[par] = (int)grabbed;  // after this item's loads
+    if (MODE >= 2 && threadIdx.x == 0 && q == seg * K) s_next[par] = (int)grabbed;  // after this item's loads
     __syncthreads();
-    if (MODE == 2 && q == seg * K) {
+    if (MODE >= 2 && q == seg * K) {
       nseg_id = s_next[par];
       nk = nseg_id < nseg ? seg_tile[nseg_id] : 0;
     }
@@ -126,7 +135,10 @@ __global__ void __launch_bounds__(NW * 32, 1) sched(const char *A, long long ld,
         nq = seg * K;
         hi = min(total, nq + K);
         if (seg >= nseg) nq = hi = total;
-        if (threadIdx.x == 0 && seg < nseg) grabbed = P + atomicAdd(ctr, 1u);
+        if (threadIdx.x == 0 && seg < nseg) {
+          if (MODE == 2) grabbed = P + atomicAdd(ctr, 1u);
+          else grabbed = seg + P < s_static ? (unsigned)(seg + P) : (unsigned)(s_static + atomicAdd(ctr, 1u));
+        }
         k = nk;
       }
       if (nq < hi) {
@@ -149,6 +161,7 @@ int main(int argc, char **argv) {
   const int n = argc > 1 ? atoi(argv[1]) : 32768;
   const int K = argc > 2 ? atoi(argv[2]) : 6;
   const bool f32 = argc > 3 && argv[3][0] == 's';
+  const double frac = argc > 4 ? atof(argv[4]) : 0.1;  // hybrid: dynamic share of the segments
   const int EB = f32 ? 4 : 8, H = 1024 / EB;
   const long long ld = n;
   const int W = NW * CW;
@@ -186,6 +199,8 @@ int main(int argc, char **argv) {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
+  const long long nseg_h = (total + K - 1) / K;
+  const long long s_static = (long long)(nseg_h * (1.0 - frac)) / P * P;
   auto run = [&](int mode, int reps, float *ms, double *spread, double *mean_idle) {
     std::vector<unsigned long long> te(P);
     float best = 1e30f;
@@ -193,15 +208,17 @@ int main(int argc, char **argv) {
     for (int r = 0; r < reps; ++r) {
       cudaMemset(ctr, 0, sizeof(unsigned));
       cudaEventRecord(e0);
-#define SCHED(M, F) sched<M, F><<<P, NW * 32>>>(A, ld, n, dt, (int)tiles.size(), total, P, K, ctr, dseg, out, tend)
+#define SCHED(M, F) sched<M, F><<<P, NW * 32>>>(A, ld, n, dt, (int)tiles.size(), total, P, K, ctr, dseg, out, tend, s_static)
       if (f32) {
         if (mode == 0) SCHED(0, true);
         if (mode == 1) SCHED(1, true);
         if (mode == 2) SCHED(2, true);
+        if (mode == 3) SCHED(3, true);
       } else {
         if (mode == 0) SCHED(0, false);
         if (mode == 1) SCHED(1, false);
         if (mode == 2) SCHED(2, false);
+        if (mode == 3) SCHED(3, false);
       }
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
@@ -222,16 +239,16 @@ int main(int argc, char **argv) {
     *spread = bsp;
     *mean_idle = bidle;
   };
-  const char *names[3] = {"static", "interleaved", "dynamic"};
+  const char *names[4] = {"static", "interleaved", "dynamic", "hybrid"};
   for (int pass = 0; pass < 2; ++pass)
-    for (int mode = 0; mode < 3; ++mode) {
+    for (int mode = 0; mode < 4; ++mode) {
       float ms;
       double sp, idle;
       run(mode, 10, &ms, &sp, &idle);
       if (pass == 1)
-        printf("{\"prec\": \"%c\", \"n\": %d, \"K\": %d, \"schedule\": \"%s\", \"us\": %.1f, \"gbs\": %.0f, \"finish_spread_us\": %.1f, "
+        printf("{\"prec\": \"%c\", \"n\": %d, \"K\": %d, \"frac\": %.2f, \"schedule\": \"%s\", \"us\": %.1f, \"gbs\": %.0f, \"finish_spread_us\": %.1f, "
                "\"mean_idle_us\": %.1f, \"items\": %lld}\n",
-               f32 ? 's' : 'd', n, K, names[mode], ms * 1e3, bytes / (ms * 1e-3) / 1e9, sp, idle, total);
+               f32 ? 's' : 'd', n, K, mode == 3 ? frac : 0.0, names[mode], ms * 1e3, bytes / (ms * 1e-3) / 1e9, sp, idle, total);
     }
   cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) printf("error %s\n", cudaGetErrorString(err));
