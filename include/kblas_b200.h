@@ -532,6 +532,12 @@ int kblas_set_symv_mid(int max_order);
 /* items <= 0 gives each CTA one contiguous range (stream-K).  Returns  */
 /* the previous value (default 6).                                      */
 int kblas_set_symv_segment(int items);
+/* Instrumentation: a device buffer of >= 3 * (CTAs) unsigned 64-bit    */
+/* words, or NULL to stop.  While set, the register SYMV/HEMV kernel     */
+/* writes each CTA's %globaltimer at start and end and its SM id        */
+/* (3*cta, 3*cta + 1, 3*cta + 2); scripts/symv_trace.py turns them into */
+/* the finish-time spread.                                              */
+int kblas_set_symv_trace(void *dev_buf);
 /* Register SYMV/HEMV kernel (orders above the mid threshold): row      */
 /* chunks per CTA barrier window (1, 2 or 4; the warps' t1 partials of  */
 /* a window are reduced together).  Returns the previous value (2).      */

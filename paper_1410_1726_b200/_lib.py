@@ -193,6 +193,8 @@ def load():
         lib.kblas_set_symv_window.restype = c_int
         lib.kblas_set_symv_segment.argtypes = [c_int]
         lib.kblas_set_symv_segment.restype = c_int
+        lib.kblas_set_symv_trace.argtypes = [c_void_p]
+        lib.kblas_set_symv_trace.restype = c_int
         lib.kblas_set_symv_narrow.argtypes = [c_int]
         lib.kblas_set_symv_narrow.restype = c_int
         LL = ctypes.c_longlong

@@ -145,6 +145,13 @@ template <class T, int V> struct Pack {
   }
 };
 
+// %globaltimer in ns (instrumentation only)
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 // L2 prefetch of the 32-byte segment at p (no register destination)
 __device__ __forceinline__ void prefetch_l2(const void *p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));

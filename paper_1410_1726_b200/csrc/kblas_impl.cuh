@@ -689,6 +689,9 @@ inline std::map<std::vector<long long>, TileTable> g_tiles;
 // SYMV segment length K (items dealt round robin per CTA, see SymParams);
 // <= 0: contiguous stream-K.  kblas_set_symv_segment.
 inline int g_symv_seg = 6;
+// instrumentation (kblas_set_symv_trace): the register SYMV kernel writes
+// each CTA's start / end %globaltimer and SM id here (3 per CTA); nullptr = off
+inline unsigned long long *g_symv_trace = nullptr;
 // register SYMV/HEMV (wide kernel): items per CTA barrier window, 1, 2 or
 // 4 (kblas_set_symv_window)
 inline int g_symv_window = 2;
@@ -813,6 +816,7 @@ SymParams sym_params(const T *A, long long lda, int d, int lead, const T *x, voi
   p.rem = tt.rem;
   p.nseg = tt.nseg;
   p.seg_tile = tt.seg_tile;
+  p.trace = g_symv_trace;
   return p;
 }
 template <class T>

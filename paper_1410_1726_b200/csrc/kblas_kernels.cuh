@@ -764,6 +764,7 @@ struct SymParams {
   long long base, rem;  // first tail item (rounds * P * K) and tail length
   long long nseg;       // rounds * P + P
   const int *seg_tile;  // per segment: tile of its first item (host-built)
+  unsigned long long *trace = nullptr;  // instrumentation: per-CTA start / end globaltimer, SM id (kblas_set_symv_trace)
   int pdl = 0;          // launched as the programmatic dependent of a hostvec copy-in grid
                         // (1: prefetch the first A segments before the wait, 2: no prefetch)
 };
@@ -860,7 +861,16 @@ __global__ void __launch_bounds__(NW * 32, MINB) kblas_symv_kernel(const SymPara
   const uint64_t pol = policy_evict_first();
   const uint64_t keep = policy_evict_last();
   SymCursor c;
-  if (!c.init(p)) return;
+  if (p.trace != nullptr && threadIdx.x == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    p.trace[3 * blockIdx.x] = globaltimer_ns();
+    p.trace[3 * blockIdx.x + 2] = smid;
+  }
+  if (!c.init(p)) {
+    if (p.trace != nullptr && threadIdx.x == 0) p.trace[3 * blockIdx.x + 1] = globaltimer_ns();
+    return;
+  }
   const int cl = warp * CW;
   const bool xvec = V > 1 && p.lead == 0 && (reinterpret_cast<uintptr_t>(x) % (V * sizeof(T))) == 0;
 
@@ -1050,6 +1060,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) kblas_symv_kernel(const SymPara
     }
     if (c.done) break;
   }
+  if (p.trace != nullptr && threadIdx.x == 0) p.trace[3 * blockIdx.x + 1] = globaltimer_ns();
 }
 
 // ---------------------------------------------------------------------------

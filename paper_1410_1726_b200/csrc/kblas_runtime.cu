@@ -368,6 +368,11 @@ int kblas_set_symv_window(int items) {
   return prev;
 }
 
+int kblas_set_symv_trace(void *dev_buf) {
+  g_symv_trace = static_cast<unsigned long long *>(dev_buf);
+  return 0;
+}
+
 int kblas_set_symv_segment(int items) {
   const int prev = g_symv_seg;
   g_symv_seg = items;
