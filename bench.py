@@ -698,6 +698,8 @@ def bench_mgpu(args, dev, rank, world, opname, n, nb, exchanges=("p2p", "nccl"),
             partial_step()
             combine(out, None, 0.0)
         steps_fn["nccl"] = nccl_step
+    if not steps_fn:
+        raise SystemExit("no exchange available: p2p failed and NCCL cannot run with ranks sharing a GPU")
     if headline not in steps_fn:
         headline = next(iter(steps_fn))
 

@@ -166,6 +166,19 @@ def matrix_in(view: MatrixView, device, lower_tri: str | None = None):
     return dev.data_ptr() + view.row_offset * esize, ld, dev
 
 
+INT_MAX = 2**31 - 1
+
+
+def c_int_dims(what: str, **dims) -> None:
+    """The C ABI takes BLAS-style 32-bit int dimensions, leading dimensions
+    and offsets (include/kblas_b200.h); a larger value would wrap in the
+    call, so it is rejected here (the reference's Python kernels have no
+    such limit, so this is the one argument error the drop-in adds)."""
+    for k, v in dims.items():
+        if v > INT_MAX:
+            raise ValueError(f"{what}: {k} = {v} exceeds the C ABI's 32-bit int range ({INT_MAX})")
+
+
 _FN_CACHE: dict = {}
 
 
@@ -179,6 +192,7 @@ def _fn(name: str):
 def call_gemv(prec: Precision, trans: str, m: int, n: int, alpha, a_ptr: int, lda: int,
               x: torch.Tensor, beta, y: torch.Tensor, device, off_r: int = 0, off_c: int = 0):
     f = _fn(f"kblas_{prec.tag}gemv_offset_async")
+    c_int_dims("gemv", m=m, n=n, lda=lda, offset_r=off_r, offset_c=off_c)
     with _on_device(device):
         rc = f(trans.encode(), m, n, _lib.scalar(prec.tag, alpha), a_ptr, lda, x.data_ptr(), 1,
                _lib.scalar(prec.tag, beta), y.data_ptr(), 1, off_r, off_c, stream_handle(device))
@@ -191,6 +205,7 @@ def call_symv(prec: Precision, hermitian: bool, uplo: str, d: int, alpha, a_ptr:
     """offset: the (offset, offset) diagonal position of the d x d operand from a_ptr."""
     name = SYMV_FN[(prec.tag, bool(hermitian))]
     f = _fn(f"kblas_{name}_offset_async")
+    c_int_dims(name, n=d, lda=lda, offset=offset)
     with _on_device(device):
         rc = f(uplo.encode(), d, _lib.scalar(prec.tag, alpha), a_ptr, lda, x.data_ptr(), 1,
                _lib.scalar(prec.tag, beta), y.data_ptr(), 1, offset, stream_handle(device))
@@ -319,6 +334,7 @@ def call_hostvec(prec: Precision, kind: str, op: str, hermitian: bool, m: int, n
     result buffer comes from the same pool; it is not handed out again
     while the returned array (held by the queue's handle) is alive."""
     _HC = hostcall()
+    c_int_dims("gemv" if kind == "g" else "symv/hemv", m=m, n=n, lda=lda, offset_r=off_r, offset_c=off_c)
     out, out_np = _PINNED.get(y_len, prec.torch_dtype)
     sync = keep is None
     herm = 1 if hermitian else 0

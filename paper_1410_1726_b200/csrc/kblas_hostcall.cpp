@@ -19,6 +19,7 @@
 
 #include <cstdint>
 #include <cstring>
+#include <initializer_list>
 
 #include "../../include/kblas_b200.h"
 
@@ -140,6 +141,11 @@ PyObject *mv_hostvec(PyObject *, PyObject *const *args, Py_ssize_t nargs) {
   const uintptr_t stream = (uintptr_t)PyLong_AsUnsignedLongLong(args[17]);
   const int sync = PyObject_IsTrue(args[18]);
   if (PyErr_Occurred()) return nullptr;
+  for (long v : {m, n, lda, off_r, off_c})
+    if (v > 2147483647L) {
+      PyErr_SetString(PyExc_ValueError, "mv_hostvec: a dimension exceeds the C ABI's 32-bit int range");
+      return nullptr;
+    }
   if (prec != 's' && prec != 'd' && prec != 'c' && prec != 'z') return PyLong_FromLong(SLOW_PATH);
   alignas(16) unsigned char alpha[16], beta[16];
   if (!get_scalar(args[6], prec, alpha) || !get_scalar(args[13], prec, beta)) return PyLong_FromLong(SLOW_PATH);

@@ -98,34 +98,59 @@ class P2PExchange:
         esize = torch.empty(0, dtype=dtype).element_size()
         self.ld = -(-n * esize // 256) * 256 // esize  # 256-byte aligned slots
         self.seq = 0
+        # every rank learns whether every rank could map the slots, so a
+        # failure on one rank raises on all of them (a rank left on the p2p
+        # path would otherwise wait for peers that took another path)
+        err = None
+        payload = [None]
         if self.rank == 0:
-            self._slots = torch.zeros(self.world * self.ld, dtype=dtype, device=self.dev)
-            self._ctl = torch.zeros(self.world + 2, dtype=torch.int64, device=self.dev)  # flags, consumed, counter
-            handles = []
-            for t in (self._slots, self._ctl):
-                h = (ctypes.c_char * 64)()
-                _lib.check(self._lib.kblas_ipc_get_handle(t.data_ptr(), h), "kblas_ipc_get_handle")
-                # the allocation may start before the tensor (caching allocator)
-                handles.append((bytes(h), t.data_ptr() - self._base_of(t)))
-            payload = [handles]
-        else:
-            payload = [None]
+            try:
+                self._slots = torch.zeros(self.world * self.ld, dtype=dtype, device=self.dev)
+                self._ctl = torch.zeros(self.world + 2, dtype=torch.int64, device=self.dev)  # flags, consumed, counter
+                handles = []
+                for t in (self._slots, self._ctl):
+                    h = (ctypes.c_char * 64)()
+                    _lib.check(self._lib.kblas_ipc_get_handle(t.data_ptr(), h), "kblas_ipc_get_handle")
+                    # the allocation may start before the tensor (caching allocator)
+                    handles.append((bytes(h), t.data_ptr() - self._base_of(t)))
+                payload = [handles]
+            except Exception as e:  # noqa: BLE001 - reported on every rank below
+                err = f"rank 0: {e}"
+                payload = [err]
         dist.broadcast_object_list(payload, src=0, group=group)
         self._opened = []
+        ptrs = []
+        if isinstance(payload[0], str):
+            err = payload[0]
+        elif self.rank != 0:
+            try:
+                for h, off in payload[0]:
+                    p = ctypes.c_void_p()
+                    _lib.check(self._lib.kblas_ipc_open_handle(h, ctypes.byref(p)), "kblas_ipc_open_handle")
+                    self._opened.append(p.value)
+                    ptrs.append(p.value + off)
+            except Exception as e:  # noqa: BLE001
+                err = f"rank {self.rank}: {e}"
+        ok = self._agree(err is None, group)
+        if not ok:
+            self.close()
+            raise RuntimeError(f"p2p exchange unavailable on some rank ({err or 'another rank failed'})")
         if self.rank == 0:
             self.slots_ptr, ctl_ptr = self._slots.data_ptr(), self._ctl.data_ptr()
         else:
-            ptrs = []
-            for h, off in payload[0]:
-                p = ctypes.c_void_p()
-                _lib.check(self._lib.kblas_ipc_open_handle(h, ctypes.byref(p)), "kblas_ipc_open_handle")
-                self._opened.append(p.value)
-                ptrs.append(p.value + off)
             self.slots_ptr, ctl_ptr = ptrs
         self.flags_ptr = ctl_ptr
         self.consumed_ptr = ctl_ptr + 8 * self.world
         self.counter_ptr = ctl_ptr + 8 * (self.world + 1)
         self._esize = esize
+
+    @staticmethod
+    def _agree(ok: bool, group) -> bool:
+        """True on every rank iff ok on every rank (one MIN all-reduce)."""
+        dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else "cpu"
+        t = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+        return bool(t.item())
 
     @staticmethod
     def _base_of(t: torch.Tensor) -> int:
@@ -155,7 +180,7 @@ def p2p_mv(prec, kind: str, op: str, m: int, n: int, alpha, panel, x: torch.Tens
     kernel.  Returns the result on rank 0, None elsewhere."""
     import ctypes
 
-    from . import _lib
+    from . import _lib, _ops
     from ._ops import stream_handle
 
     lib = _lib.load()
@@ -173,6 +198,7 @@ def p2p_mv(prec, kind: str, op: str, m: int, n: int, alpha, panel, x: torch.Tens
             raise ValueError(f"y must be a vector of length {plen}")
         y = y.to(device=x.device, dtype=x.dtype).contiguous()
     al, be = _lib.scalar(prec.tag, alpha), _lib.scalar(prec.tag, beta)
+    _ops.c_int_dims("mgpu p2p partial", m=m, n=n, lda=lda)
     rc = lib.kblas_mv_mgpu_partial_p2p_async(
         prec.tag.encode(), kind.encode(), op.encode(), m, n, ctypes.addressof(al), a_ptr, lda, x.data_ptr(),
         ex.world, ex.rank, nb, 1 if hermitian else 0, ex.slots_ptr, ex.ld, ex.flags_ptr, ex.consumed_ptr,

@@ -164,6 +164,7 @@ def partial_mv(prec: Precision, kind: str, op: str, m: int, n: int, alpha, local
         a_ptr = local.data.data_ptr() + local.linear_index(0, 0) * prec.element_bytes
         lda = local.ld
     al = _lib.scalar(prec.tag, alpha)
+    _ops.c_int_dims("mgpu partial", m=m, n=n, lda=lda)
     with _ops._on_device(dev):
         rc = lib.kblas_mv_mgpu_partial_async(
             prec.tag.encode(), kind.encode(), op.encode(), m, n, ctypes.cast(ctypes.byref(al), ctypes.c_void_p),
@@ -221,6 +222,7 @@ def _mgpu_common(kind: str, op: str, alpha, dist: DistributedMatrix, x, beta, y,
     eb = prec.element_bytes
     a_ptrs = [(v.data.data_ptr() + v.linear_index(0, 0) * eb) if v is not None else 0 for v in dist.local_views]
     lda = next((v.ld for v in dist.local_views if v is not None), local_ld(dist.global_m))
+    _ops.c_int_dims("mgpu", m=dist.global_m, n=dist.global_n, lda=lda)
     streams = [_ops.stream_handle(dev) for dev in dist.devices]
     distinct = len({d.index for d in dist.devices}) == G
     al, be = _lib.scalar(prec.tag, alpha), _lib.scalar(prec.tag, beta)

@@ -98,3 +98,51 @@ def test_p2p_exchange_world4_one_gpu(kind, op, tag):
         p.join(300)
         assert p.exitcode == 0
     assert q.get(timeout=5) < 1e-12
+
+
+def _fail_worker(rank, world, port, failing, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(torch.device("cuda", rank % torch.cuda.device_count()))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1410_1726_b200 import _lib
+    from paper_1410_1726_b200.dist import P2PExchange
+
+    if rank == failing:
+        lib = _lib.load()
+
+        class _Broken:  # this rank cannot map the root's allocations
+            def __getattr__(self, name):
+                if name in ("kblas_ipc_open_handle", "kblas_ipc_get_handle"):
+                    return lambda *a: 1  # cudaErrorInvalidValue
+                return getattr(lib, name)
+
+        _lib.load = lambda: _Broken()
+    try:
+        P2PExchange(1000, torch.float64)
+        q.put((rank, "constructed"))
+    except RuntimeError as e:
+        q.put((rank, str(e)))
+    dist.barrier()  # every rank got here: nobody is left waiting on the exchange
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("failing", [0, 1])
+def test_p2p_exchange_failure_raises_on_every_rank(failing):
+    """A rank that cannot set up the IPC mapping (here: rank `failing`'s
+    handle calls fail) makes the constructor raise on EVERY rank, so the
+    ranks agree on the fallback instead of one waiting on the others."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_fail_worker, args=(r, 2, port, failing, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    got = dict(q.get(timeout=5) for _ in range(2))
+    assert set(got) == {0, 1}
+    for r, msg in got.items():
+        assert "p2p exchange unavailable" in msg, (r, msg)
+    assert f"rank {failing}" in got[failing]

@@ -362,3 +362,34 @@ def test_kernel_request_validation():
         kb.KernelRequest(kb.Op.SYMV_LOWER, sq, np.zeros(3), np.zeros(3), 1.0, 0.0, cfg)
     r = kb.KernelRequest(kb.Op.SYMV_LOWER, kb.HermitianView(sq, "l"), np.zeros(3), np.zeros(3), 1.0, 0.0, cfg)
     assert r.view is sq and r.precision.tag == "d"
+
+
+class TestIntDimensions:
+    """The C ABI's dimensions are 32-bit ints (BLAS convention); anything
+    larger is rejected before a call instead of wrapping in ctypes."""
+
+    def test_c_int_dims(self):
+        from paper_1410_1726_b200 import _ops
+
+        _ops.c_int_dims("gemv", m=2**31 - 1, n=5)
+        with pytest.raises(ValueError, match=r"gemv: m = 2147483648 exceeds the C ABI's 32-bit int range"):
+            _ops.c_int_dims("gemv", m=2**31, n=5)
+
+    def test_call_sites_reject_before_any_device_work(self):
+        import torch
+
+        from paper_1410_1726_b200 import _ops
+
+        p = precision("d")
+        v = torch.zeros(4, dtype=torch.float64)
+        with pytest.raises(ValueError, match="lda = 3000000000"):
+            _ops.call_gemv(p, "n", 4, 4, 1.0, 0, 3_000_000_000, v, 0.0, v, "cpu")
+        with pytest.raises(ValueError, match="n = 2147483648"):
+            _ops.call_symv(p, False, "l", 2**31, 1.0, 0, 2**31, v, 0.0, v, "cpu")
+        with pytest.raises(ValueError, match="offset_c = 2147483648"):
+            _ops.call_hostvec(p, "g", "n", False, 4, 4, 1.0, 0, 4, np.zeros(4), 4, 0.0, np.zeros(4), 4, "cpu",
+                              off_c=2**31)
+        hc = _ops.hostcall()
+        with pytest.raises(ValueError, match="32-bit int range"):
+            hc.mv_hostvec("d", "g", "n", 0, 2**31, 4, 1.0, 0, 2**31, 0, 0, np.zeros(4), 4, 0.0, np.zeros(2**0), 1,
+                          0, 0, True)
