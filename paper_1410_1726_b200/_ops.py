@@ -192,7 +192,8 @@ def _fn(name: str):
 def call_gemv(prec: Precision, trans: str, m: int, n: int, alpha, a_ptr: int, lda: int,
               x: torch.Tensor, beta, y: torch.Tensor, device, off_r: int = 0, off_c: int = 0):
     f = _fn(f"kblas_{prec.tag}gemv_offset_async")
-    c_int_dims("gemv", m=m, n=n, lda=lda, offset_r=off_r, offset_c=off_c)
+    if max(m, n, lda, off_r, off_c) > INT_MAX:
+        c_int_dims("gemv", m=m, n=n, lda=lda, offset_r=off_r, offset_c=off_c)
     with _on_device(device):
         rc = f(trans.encode(), m, n, _lib.scalar(prec.tag, alpha), a_ptr, lda, x.data_ptr(), 1,
                _lib.scalar(prec.tag, beta), y.data_ptr(), 1, off_r, off_c, stream_handle(device))
@@ -205,7 +206,8 @@ def call_symv(prec: Precision, hermitian: bool, uplo: str, d: int, alpha, a_ptr:
     """offset: the (offset, offset) diagonal position of the d x d operand from a_ptr."""
     name = SYMV_FN[(prec.tag, bool(hermitian))]
     f = _fn(f"kblas_{name}_offset_async")
-    c_int_dims(name, n=d, lda=lda, offset=offset)
+    if max(d, lda, offset) > INT_MAX:
+        c_int_dims(name, n=d, lda=lda, offset=offset)
     with _on_device(device):
         rc = f(uplo.encode(), d, _lib.scalar(prec.tag, alpha), a_ptr, lda, x.data_ptr(), 1,
                _lib.scalar(prec.tag, beta), y.data_ptr(), 1, offset, stream_handle(device))
@@ -334,7 +336,6 @@ def call_hostvec(prec: Precision, kind: str, op: str, hermitian: bool, m: int, n
     result buffer comes from the same pool; it is not handed out again
     while the returned array (held by the queue's handle) is alive."""
     _HC = hostcall()
-    c_int_dims("gemv" if kind == "g" else "symv/hemv", m=m, n=n, lda=lda, offset_r=off_r, offset_c=off_c)
     out, out_np = _PINNED.get(y_len, prec.torch_dtype)
     sync = keep is None
     herm = 1 if hermitian else 0
