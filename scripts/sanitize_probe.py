@@ -82,6 +82,20 @@ for tag in "sdcz":
         r = kb.symv_hemv(uplo, 0.5, kb.HermitianView(A, uplo), vec(tag, d), 0.25, vec(tag, d), hermitian=herm).y_out
         ok(f"symv-tma {tag} {uplo}", r)
         _lib.set_tma(prev)
+    # 128-wide tiles (the 128-row epilogue): the 2-CTA/SM variant off, on
+    # the single-GPU path (uniform tiles) and on mgpu panels with nb = 128
+    prev_mid = lib.kblas_set_symv_mid(0)
+    for uplo in "lu":
+        for beta in (0.0, 0.25):
+            r = kb.symv_hemv(uplo, 0.5, kb.HermitianView(A, uplo), vec(tag, d), beta, vec(tag, d),
+                             hermitian=herm).y_out
+            ok(f"symv wide {tag} {uplo} beta={beta}", r)
+    lib.kblas_set_symv_mid(prev_mid)
+    dist = kb.distribute(kb.view_of(torch.rand(1000, 1000, device="cuda", dtype=kb.precision(tag).torch_dtype).T),
+                         128, 3)
+    r = kb.symv_hemv_mgpu("l", 1.0, dist, vec(tag, 1000), 0.5, vec(tag, 1000), kb.KernelConfig(128, 2),
+                          hermitian=herm)[0].y_out
+    ok(f"symv mgpu nb=128 {tag}", r)
     dist = kb.distribute(kb.view_of(torch.rand(600, 600, device="cuda", dtype=kb.precision(tag).torch_dtype).T),
                          64, 3)
     r = kb.symv_hemv_mgpu("l", 1.0, dist, vec(tag, 600), 0.5, vec(tag, 600), kb.KernelConfig(64, 2),
