@@ -405,8 +405,10 @@ int kblas_getmatrix_async(int rows, int cols, size_t esize, const void *dA, int 
 /* offset_c = the diagonal offset).  alpha/beta point to one scalar of  */
 /* the precision.  y_in may be NULL when *beta == 0.  Enqueues on      */
 /* `stream`: the staging of x (and y_in) -- a copy-in kernel reading    */
-/* page-locked host memory through its device mapping, or cudaMemcpy-  */
-/* Async for pageable memory --, the kernels, and the result write     */
+/* page-locked host memory through its device mapping (launched as a   */
+/* programmatic dependent of the stream's previous kernel; it stores   */
+/* only after that kernel has completed), or cudaMemcpyAsync for       */
+/* pageable memory --, the kernels, and the result write               */
 /* (straight into page-locked y_out when *beta == 0, else a D2H copy),  */
 /* then waits.  Same return codes as the entry points it wraps (-1: bad */
 /* vector arguments).  Replaces blockmv's numpy-in/numpy-out call shape */

@@ -252,6 +252,17 @@ inline int hostvec_prefetch_mode() {
   return mode;
 }
 
+// The hostvec copy-in grid launched as a programmatic dependent of the
+// stream's previous kernel (1, default) or the ordinary way
+// ($KBLAS_HOSTVEC_EARLY=0).
+inline bool hostvec_early_copy() {
+  static const bool on = [] {
+    const char *e = std::getenv("KBLAS_HOSTVEC_EARLY");
+    return !(e != nullptr && e[0] == '0');
+  }();
+  return on;
+}
+
 template <class... KArgs, class... Args>
 cudaError_t launch_main(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t st,
                         Args &&...args) {
@@ -1414,12 +1425,24 @@ int hostvec_entry(bool is_gemv, char op, bool herm, int m, int n, T alpha, const
   if ((xin || yin) && (!xin || mapped_host(hx, &dhx)) && (!yin || mapped_host(hy_in, &dhy))) {
     const long long units = cdiv(std::max(xin ? xlen : 0LL, yin ? ylen : 0LL) * (long long)sizeof(T), 16);
     const unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>(cdiv(units, 256), 2LL * dev_sms()));
-    kblas_hostvec_in_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<char *>(dx), static_cast<const char *>(dhx),
-                                                   xin ? xlen * (long long)sizeof(T) : 0, reinterpret_cast<char *>(dy),
-                                                   static_cast<const char *>(dhy),
-                                                   yin ? ylen * (long long)sizeof(T) : 0);
+    // programmatic stream serialization: on a queue of calls the grid's
+    // PCIe reads overlap the previous call's last kernel (it waits before
+    // its first store into the staging buffer)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = hostvec_early_copy() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, kblas_hostvec_in_kernel, reinterpret_cast<char *>(dx),
+                           static_cast<const char *>(dhx), xin ? xlen * (long long)sizeof(T) : 0,
+                           reinterpret_cast<char *>(dy), static_cast<const char *>(dhy),
+                           yin ? ylen * (long long)sizeof(T) : 0);
+    if (e != cudaSuccess) return (int)e;
     launched();
-    if ((e = cudaGetLastError()) != cudaSuccess) return (int)e;
     // PDL only when x alone is staged: the main kernel reads x after its own
     // griddepcontrol.wait on the copy-in grid.  A staged y (beta != 0) is
     // read by the epilogue kernel, a programmatic dependent of the main

@@ -33,7 +33,12 @@ namespace kb {
 // ---------------------------------------------------------------------------
 // Programmatic dependent launch: the epilogue grid is launched while the
 // streaming kernel runs (launch latency hidden) and blocks here until the
-// streaming grid has completed and its writes are visible.
+// streaming grid has completed and its writes are visible.  Every library
+// kernel releases its dependents at its start and executes griddep_wait()
+// before it touches data an earlier kernel of the stream may still write
+// or read; the programmatic dependents are the epilogues, the main kernel
+// of a host-vector call (after its copy-in grid) and the copy-in grid
+// itself (after the stream's previous kernel).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void griddep_launch_dependents() {
@@ -273,6 +278,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) kblas_gemv_n_kernel(const GemvP
 // ---------------------------------------------------------------------------
 template <class T, int V, int NW, int CW>
 __global__ void __launch_bounds__(NW * 32, 2) kblas_gemv_ns_kernel(const GemvParams p) {
+  griddep_launch_dependents();
   griddep_wait();  // x / y staged by a hostvec copy-in grid (no-op otherwise)
   constexpr int RB = 32 * V;
   __shared__ T red[NW][RB];
@@ -351,6 +357,7 @@ __global__ void __launch_bounds__(NW * 32, 2) kblas_gemv_ns_kernel(const GemvPar
 // ---------------------------------------------------------------------------
 template <class T, int V, int NW, int LR, int U>
 __global__ void __launch_bounds__(NW * 32) kblas_gemv_ro_kernel(const GemvParams p) {
+  griddep_launch_dependents();
   constexpr int CPI = 32 / LR, RBo = LR * V, STEP = NW * CPI;
   __shared__ T red[NW][RBo];
   const T *__restrict__ A = static_cast<const T *>(p.A);
@@ -423,6 +430,7 @@ __global__ void __launch_bounds__(NW * 32) kblas_gemv_ro_kernel(const GemvParams
 // ---------------------------------------------------------------------------
 template <class T, int V, int NW, int CW>
 __global__ void __launch_bounds__(NW * 32, 2) kblas_gemv_nc_kernel(const GemvParams p) {
+  griddep_launch_dependents();
   griddep_wait();  // x / y staged by a hostvec copy-in grid (no-op otherwise)
   namespace cg = cooperative_groups;
   constexpr int RB = 32 * V;
@@ -628,6 +636,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) kblas_gemv_t_kernel(const GemvP
 // ---------------------------------------------------------------------------
 template <class T, int V, int NW, int CB, bool CONJ>
 __global__ void __launch_bounds__(NW * 32, 2) kblas_gemv_tc_kernel(const GemvParams p) {
+  griddep_launch_dependents();
   griddep_wait();  // x / y staged by a hostvec copy-in grid (no-op otherwise)
   constexpr int H = 32 * V;
   __shared__ T part[NW][CB];
@@ -1095,6 +1104,7 @@ template <class T, int EW>
 __global__ void __launch_bounds__(EW * 32) kblas_gemv_n_epilogue(T *y, const T *__restrict__ ws, long long ws_ld, int m,
                                                           int lead, int RB, int KS, long long total, int P,
                                                           T alpha, T beta, int beta_zero) {
+  griddep_launch_dependents();
   griddep_wait();
   __shared__ T part[EW][32];
   const long long i = (long long)blockIdx.x * 32 + (threadIdx.x & 31);
@@ -1114,6 +1124,7 @@ template <class T, int EW>
 __global__ void __launch_bounds__(EW * 32) kblas_gemv_t_epilogue(T *y, const T *__restrict__ ws, long long ws_ld,
                                                           long long nglob, int CBW, int KS, long long total, int P,
                                                           ColMap cm, T alpha, T beta, int beta_zero) {
+  griddep_launch_dependents();
   griddep_wait();
   __shared__ T part[EW][32];
   const long long c = (long long)blockIdx.x * 32 + (threadIdx.x & 31);
@@ -1156,6 +1167,7 @@ struct Xchg {
 template <class T, bool LOWER, int EW>
 __global__ void __launch_bounds__(EW * 32) kblas_symv_epilogue(T *y, const SymParams p, T alpha, T beta, int beta_zero,
                                                          const Xchg xg) {
+  griddep_launch_dependents();
   griddep_wait();
   if (xg.G > 0 && xg.rank != 0 && xg.seq > 1) {
     // this rank's slot is free once the root consumed the previous call
@@ -1265,6 +1277,7 @@ __global__ void __launch_bounds__(EW * 32) kblas_symv_epilogue(T *y, const SymPa
 template <class T, bool LOWER, int EW>
 __global__ void __launch_bounds__(EW * 32, 2) kblas_symv_epilogue_r128(T *y, const SymParams p, T alpha, T beta,
                                                               int beta_zero, const Xchg xg) {
+  griddep_launch_dependents();
   griddep_wait();
   if (xg.G > 0 && xg.rank != 0 && xg.seq > 1) {
     if (threadIdx.x == 0) spin_until(xg.consumed, xg.seq - 1);
@@ -1388,13 +1401,21 @@ __global__ void __launch_bounds__(EW * 32, 2) kblas_symv_epilogue_r128(T *y, con
 // copy-engine round trips).  It releases its dependents at once: the main
 // kernel, launched with programmatic stream serialization, streams A
 // meanwhile and waits in griddepcontrol.wait before it reads x or y.
+//
+// The grid is itself launched with programmatic stream serialization: on a
+// queue of calls it starts while the previous call's last kernel drains.
+// Each thread reads its first 16-byte unit of x and y over PCIe first and
+// waits in griddepcontrol.wait before its first store, so the staging
+// buffer is written only after every earlier kernel of the stream is done
+// with it (each library kernel waits on its own primary before it
+// completes, so the wait covers the whole stream).
 __device__ __forceinline__ void hostvec_copy(char *dst, const char *src, long long bytes, long long tid,
-                                             long long nt) {
+                                             long long nt, bool first_done) {
   if (bytes <= 0) return;
   long long done = 0;
   if (((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0) {
     const long long n16 = bytes >> 4;
-    for (long long i = tid; i < n16; i += nt)
+    for (long long i = tid + (first_done ? nt : 0); i < n16; i += nt)
       reinterpret_cast<uint4 *>(dst)[i] = reinterpret_cast<const uint4 *>(src)[i];
     done = n16 << 4;
   }
@@ -1407,13 +1428,24 @@ static __global__ void kblas_hostvec_in_kernel(char *dx, const char *hx, long lo
                                         long long ybytes) {
   griddep_launch_dependents();
   const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x, nt = (long long)gridDim.x * blockDim.x;
-  hostvec_copy(dx, hx, xbytes, tid, nt);
-  hostvec_copy(dy, hy, ybytes, tid, nt);
+  auto aligned = [](const char *d, const char *s) {
+    return ((reinterpret_cast<uintptr_t>(d) | reinterpret_cast<uintptr_t>(s)) & 15) == 0;
+  };
+  const bool px = aligned(dx, hx) && tid < (xbytes >> 4), py = aligned(dy, hy) && tid < (ybytes >> 4);
+  uint4 ux = make_uint4(0, 0, 0, 0), uy = make_uint4(0, 0, 0, 0);
+  if (px) ux = reinterpret_cast<const uint4 *>(hx)[tid];
+  if (py) uy = reinterpret_cast<const uint4 *>(hy)[tid];
+  griddep_wait();  // earlier kernels of the stream are done with the staging buffer
+  if (px) reinterpret_cast<uint4 *>(dx)[tid] = ux;
+  if (py) reinterpret_cast<uint4 *>(dy)[tid] = uy;
+  hostvec_copy(dx, hx, xbytes, tid, nt, aligned(dx, hx));
+  hostvec_copy(dy, hy, ybytes, tid, nt, aligned(dy, hy));
 }
 
 // y <- beta * y (beta == 0: zero fill); run_scal semantics (kernels.py:127-146)
 template <class T>
 __global__ void kblas_scal_kernel(T *y, long long n, T beta, int beta_zero) {
+  griddep_launch_dependents();
   griddep_wait();  // y staged by a hostvec copy-in grid (no-op otherwise)
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;

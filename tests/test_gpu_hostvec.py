@@ -182,6 +182,67 @@ def test_queued_pinned_calls_do_not_share_staging(op):
         assert h.result().flops > 0  # the deferred report fills on access
 
 
+@pytest.mark.parametrize("tag", "dz")
+def test_queued_mixed_calls(tag):
+    """A long queue mixing every form of the host-vector path on one stream
+    (row-owning and split GEMV-N, GEMV-T/C, SYMV/HEMV with its epilogue,
+    beta != 0 with y staged, alpha = 0 scal, a 100k-element x that takes
+    several copy-in passes, shifted page-locked views): each copy-in grid
+    starts while the previous call drains and writes the shared staging
+    buffer only after it, so every result equals its device-tensor call."""
+    rng = np.random.default_rng(106)
+    dt = naive.DTYPES[tag]
+    sq, _ = dev_view(rng, 2048, 2048, tag, host=False)
+    tall, _ = dev_view(rng, 100000, 48, tag, host=False)
+    wide, _ = dev_view(rng, 300, 6000, tag, host=False)
+    hv = kb.HermitianView(sq, "l")
+    herm = tag in "cz"
+    calls = []
+    for i in range(48):
+        kind = ["gemv_sq", "symv", "gemv_t_tall", "gemv_n_wide", "scal", "gemv_c_sq"][i % 6]
+        beta = 0.0 if i % 4 else -0.5
+        shift = i % 3 == 2
+        if kind == "gemv_sq":
+            args = ("n", 0.75, sq, 2048, 2048)
+        elif kind == "gemv_c_sq":
+            args = ("c", 0.75, sq, 2048, 2048)
+        elif kind == "gemv_t_tall":
+            args = ("t", 1.25, tall, 100000, 48)
+        elif kind == "gemv_n_wide":
+            args = ("n", 1.25, wide, 6000, 300)
+        elif kind == "scal":
+            args = ("n", 0.0, sq, 2048, 2048)
+        else:
+            args = None
+        if kind == "symv":
+            x = pinned(naive.fill(rng, 2048, tag), 1 if shift else 0)
+            y = pinned(naive.fill(rng, 2048, tag))
+            calls.append((kind, x, y, beta, None))
+        else:
+            trans, alpha, view, xl, yl = args
+            x = pinned(naive.fill(rng, xl, tag), 1 if shift else 0)
+            y = pinned(naive.fill(rng, yl, tag))
+            calls.append((kind, x, y, beta, (trans, alpha, view)))
+    q = kb.CommandQueue()
+    hs = []
+    for kind, x, y, beta, g in calls:
+        if kind == "symv":
+            hs.append(kb.symv_hemv_async("l", 0.5, hv, x, beta, y, queue=q, hermitian=herm))
+        else:
+            trans, alpha, view = g
+            hs.append(kb.gemv_async(trans, alpha, view, x, beta, y, queue=q))
+    q.synchronize()
+    for (kind, x, y, beta, g), h in zip(calls, hs):
+        xd = torch.from_numpy(np.array(x, dtype=dt)).cuda()
+        yd = torch.from_numpy(np.array(y, dtype=dt)).cuda()
+        if kind == "symv":
+            want = kb.symv_hemv("l", 0.5, hv, xd, beta, yd, hermitian=herm).y_out
+        else:
+            trans, alpha, view = g
+            want = kb.gemv(trans, alpha, view, xd, beta, yd).y_out
+        same(h.result().y_out, want)
+
+
 def test_queue_orders_after_callers_stream():
     """A queued call sees work the caller enqueued on its own stream before
     submitting (kblas_stream_order), without a host wait."""

@@ -342,6 +342,28 @@ def test_no_noncoherent_x_loads_before_griddepcontrol_wait():
     assert bad == [], bad[:5]
 
 
+def test_hostvec_copy_in_stores_only_after_griddepcontrol_wait():
+    """The host-vector copy-in grid is launched as a programmatic dependent
+    of the stream's previous kernel, which may still read the staging
+    buffer: it may read host memory before griddepcontrol.wait but must
+    not store before it (shipped SASS: no STG ahead of ACQBULK)."""
+    import re
+    import shutil
+    import subprocess
+
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(tool):
+        pytest.skip("cuobjdump not available")
+    sass = subprocess.run([tool, "-sass", _lib.LIB_PATH], capture_output=True, text=True, check=True).stdout
+    fns = [f for f in re.split(r"\n\s+Function : ", sass)[1:] if f.startswith("_ZN2kb23kblas_hostvec_in_kernel")]
+    assert fns  # one static copy per translation unit
+    for fn in fns:
+        assert "ACQBULK" in fn and "PREEXIT" in fn
+        head = fn[: fn.index("ACQBULK")]
+        assert re.findall(r"STG\.", head) == []
+        assert re.findall(r"LDG\.E\.128", head), "the first 16-byte host reads are issued before the wait"
+
+
 def test_kernel_request_validation():
     """KernelRequest keeps the reference's checks and messages
     (kernels.py:74-89)."""
