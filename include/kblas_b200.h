@@ -538,7 +538,9 @@ int kblas_set_symv_segment(int items);
 /* words, or NULL to stop.  While set, the register SYMV/HEMV kernel     */
 /* writes each CTA's %globaltimer at start and end and its SM id        */
 /* (3*cta, 3*cta + 1, 3*cta + 2); scripts/symv_trace.py turns them into */
-/* the finish-time spread.                                              */
+/* the finish-time spread.  Only in a library built with                */
+/* -DKBLAS_SYMV_TRACE=1 (KBLAS_NVCC_EXTRA); the product build returns   */
+/* -1 and compiles the trace branches out of the kernel.                */
 int kblas_set_symv_trace(void *dev_buf);
 /* Register SYMV/HEMV kernel (orders above the mid threshold): row      */
 /* chunks per CTA barrier window (1, 2 or 4; the warps' t1 partials of  */

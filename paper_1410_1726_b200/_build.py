@@ -77,7 +77,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
     for src in SOURCES:
         obj = os.path.join(CSRC, os.path.basename(src)[:-3] + ".o")
         objs.append(obj)
-        cmd = [nvcc(), *NVCC_FLAGS, "-c", src, "-o", obj]
+        # $KBLAS_NVCC_EXTRA: extra nvcc flags for investigation builds (e.g.
+        # -DKBLAS_SYMV_TRACE=1, scripts/symv_trace.py); empty for the product
+        extra = os.environ.get("KBLAS_NVCC_EXTRA", "").split()
+        cmd = [nvcc(), *NVCC_FLAGS, *extra, "-c", src, "-o", obj]
         procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
     reports = []
     failed = None

@@ -12,7 +12,9 @@ import threading
 from ctypes import POINTER, c_char, c_double, c_float, c_int, c_size_t, c_ulonglong, c_void_p
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libkblas_b200.so")
+# KBLAS_LIB: load another build of the library (same-box A/B runs of two
+# builds, scripts/*_ab.sh); the default is the in-tree build
+LIB_PATH = os.environ.get("KBLAS_LIB") or os.path.join(HERE, "libkblas_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "kblas_b200.h")
 
 

@@ -827,7 +827,9 @@ SymParams sym_params(const T *A, long long lda, int d, int lead, const T *x, voi
   p.rem = tt.rem;
   p.nseg = tt.nseg;
   p.seg_tile = tt.seg_tile;
+#if KBLAS_SYMV_TRACE
   p.trace = g_symv_trace;
+#endif
   return p;
 }
 template <class T>

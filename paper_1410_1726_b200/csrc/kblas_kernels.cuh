@@ -28,6 +28,10 @@
 
 #include "kblas_device.cuh"
 
+#ifndef KBLAS_SYMV_TRACE
+#define KBLAS_SYMV_TRACE 0
+#endif
+
 namespace kb {
 
 // ---------------------------------------------------------------------------
@@ -773,7 +777,9 @@ struct SymParams {
   long long base, rem;  // first tail item (rounds * P * K) and tail length
   long long nseg;       // rounds * P + P
   const int *seg_tile;  // per segment: tile of its first item (host-built)
+#if KBLAS_SYMV_TRACE
   unsigned long long *trace = nullptr;  // instrumentation: per-CTA start / end globaltimer, SM id (kblas_set_symv_trace)
+#endif
   int pdl = 0;          // launched as the programmatic dependent of a hostvec copy-in grid
                         // (1: prefetch the first A segments before the wait, 2: no prefetch)
 };
@@ -870,6 +876,10 @@ __global__ void __launch_bounds__(NW * 32, MINB) kblas_symv_kernel(const SymPara
   const uint64_t pol = policy_evict_first();
   const uint64_t keep = policy_evict_last();
   SymCursor c;
+#if KBLAS_SYMV_TRACE
+  // investigation builds only: the two trace branches cost the 2-CTA/SM
+  // variant 5-11 % at d = 4096..8192 (register allocation), so the product
+  // build compiles them out
   if (p.trace != nullptr && threadIdx.x == 0) {
     unsigned smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
@@ -880,6 +890,9 @@ __global__ void __launch_bounds__(NW * 32, MINB) kblas_symv_kernel(const SymPara
     if (p.trace != nullptr && threadIdx.x == 0) p.trace[3 * blockIdx.x + 1] = globaltimer_ns();
     return;
   }
+#else
+  if (!c.init(p)) return;
+#endif
   const int cl = warp * CW;
   const bool xvec = V > 1 && p.lead == 0 && (reinterpret_cast<uintptr_t>(x) % (V * sizeof(T))) == 0;
 
@@ -1069,7 +1082,9 @@ __global__ void __launch_bounds__(NW * 32, MINB) kblas_symv_kernel(const SymPara
     }
     if (c.done) break;
   }
+#if KBLAS_SYMV_TRACE
   if (p.trace != nullptr && threadIdx.x == 0) p.trace[3 * blockIdx.x + 1] = globaltimer_ns();
+#endif
 }
 
 // ---------------------------------------------------------------------------

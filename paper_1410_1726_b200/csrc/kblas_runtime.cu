@@ -369,8 +369,13 @@ int kblas_set_symv_window(int items) {
 }
 
 int kblas_set_symv_trace(void *dev_buf) {
+#if KBLAS_SYMV_TRACE
   g_symv_trace = static_cast<unsigned long long *>(dev_buf);
   return 0;
+#else
+  (void)dev_buf;
+  return -1;  // product build: the trace branches are compiled out
+#endif
 }
 
 int kblas_set_symv_segment(int items) {

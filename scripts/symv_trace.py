@@ -1,7 +1,8 @@
 #!/usr/bin/env python
 """Per-CTA start / end times of the register SYMV/HEMV kernel
 (kblas_set_symv_trace): how long the first CTAs to finish sit idle while
-the last ones stream.  Prints JSON lines.
+the last ones stream.  Prints JSON lines.  Needs an investigation build:
+KBLAS_NVCC_EXTRA=-DKBLAS_SYMV_TRACE=1 python -m paper_1410_1726_b200._build --force
 
     python scripts/symv_trace.py [--ops dsymv,zhemv] [--sizes 32768,100000]
 """
@@ -48,7 +49,9 @@ for opname in args.ops.split(","):
         res = []
         for r in range(args.reps):
             trace.zero_()
-            lib.kblas_set_symv_trace(trace.data_ptr())
+            if lib.kblas_set_symv_trace(trace.data_ptr()) != 0:
+                sys.exit("this library was built without the trace: rebuild with "
+                         "KBLAS_NVCC_EXTRA=-DKBLAS_SYMV_TRACE=1 python -m paper_1410_1726_b200._build --force")
             call()
             lib.kblas_set_symv_trace(None)
             torch.cuda.synchronize()
