@@ -694,6 +694,11 @@ struct TileTable {
   int K = 1, rounds = 0;
   long long base = 0, rem = 0, nseg = 0;
   long long nslots = 0;     // ws2 slot rows (sum over tiles of the segments touching them)
+  // split schedule (tail_items > 0): the tail [base, total) is cut into
+  // Ptail segments of ~tail_items items for the tail grid; dev_tail is the
+  // tile array with seg0 counted from the first tail segment (rounds * P)
+  int Ptail = 1;
+  SymTile *dev_tail = nullptr;
 };
 inline std::map<std::vector<long long>, TileTable> g_tiles;
 
@@ -706,6 +711,26 @@ inline unsigned long long *g_symv_trace = nullptr;
 // register SYMV/HEMV (wide kernel): items per CTA barrier window, 1, 2 or
 // 4 (kblas_set_symv_window)
 inline int g_symv_window = 2;
+// split schedule of the wide kernel (see kblas_symv_kernel): the last
+// symv_tail_pct() % of the items run as a tail grid of symv_tail_items()-item
+// CTAs.  $KBLAS_SYMV_TAIL_PCT / $KBLAS_SYMV_TAIL_ITEMS override them
+// (share 0: one grid).
+inline int symv_tail_pct() {
+  static const int pct = [] {
+    const char *e = std::getenv("KBLAS_SYMV_TAIL_PCT");
+    return e != nullptr ? std::max(0, std::atoi(e)) : 6;
+  }();
+  return pct;
+}
+inline int symv_tail_items() {
+  static const int items = [] {
+    const char *e = std::getenv("KBLAS_SYMV_TAIL_ITEMS");
+    return e != nullptr ? std::max(1, std::atoi(e)) : 4;
+  }();
+  return items;
+}
+// fewest interleaved rounds that leave a split worth it (below: one grid)
+constexpr int kSymvSplitMinRounds = 8;
 
 // Tiles for the local panel of GPU g under the block-cyclic layout (G=1,
 // nb=d for a single GPU): every owned block column is cut into W-wide tiles.
@@ -714,10 +739,11 @@ inline int g_symv_window = 2;
 // schedule (segments of K items round robin over P CTAs, then a
 // contiguous tail) and each tile's ws2 slot rows are fixed here too.
 inline cudaError_t tile_table(int d, int lead, bool lower, int W, int H, ColMap cm, int ncols_local, long long P,
-                              int K, TileTable *out, bool exact = false) {
+                              int K, TileTable *out, bool exact = false, int tail_pct = 0, int tail_items = 0) {
   int dev = 0;
   cudaGetDevice(&dev);
-  std::vector<long long> key{dev, d, lead, lower, W, H, cm.G, cm.g, cm.nb, ncols_local, P, K, exact};
+  std::vector<long long> key{dev, d, lead, lower, W, H, cm.G, cm.g, cm.nb, ncols_local, P, K, exact,
+                             tail_pct, tail_items};
   {
     std::lock_guard<std::mutex> lk(g_mu);
     auto it = g_tiles.find(key);
@@ -757,12 +783,20 @@ inline cudaError_t tile_table(int d, int lead, bool lower, int W, int H, ColMap 
   tt.K = K > 0 ? K : 1;
   // the tail keeps >= 1 item per CTA, so no segment is empty and every
   // slot row a tile owns is written
-  tt.rounds = K > 0 ? (int)(std::max<long long>(0, prefix - Pe) / (Pe * K)) : 0;
+  const bool split = K > 0 && tail_items > 0 && tail_pct > 0;
+  const long long tail_min = split ? std::max<long long>(Pe, prefix * tail_pct / 100) : Pe;
+  tt.rounds = K > 0 ? (int)(std::max<long long>(0, prefix - tail_min) / (Pe * K)) : 0;
   tt.base = (long long)tt.rounds * Pe * tt.K;
   tt.rem = prefix - tt.base;
-  tt.nseg = (long long)tt.rounds * Pe + Pe;
-  auto seg_of = [&](long long q) { return sym_seg_of(q, tt.K, tt.rounds, (int)Pe, tt.base, tt.rem); };
-  auto seg_lo = [&](long long sg) { return sym_seg_lo(sg, tt.K, tt.rounds, (int)Pe, tt.base, tt.rem); };
+  tt.Ptail = split ? (int)std::min<long long>(tt.rem, cdiv(tt.rem, tail_items)) : (int)Pe;
+  tt.nseg = (long long)tt.rounds * Pe + tt.Ptail;
+  const long long full = (long long)tt.rounds * Pe;
+  auto seg_of = [&](long long q) {
+    return q < tt.base ? q / tt.K : full + sk_owner(q - tt.base, tt.rem, tt.Ptail);
+  };
+  auto seg_lo = [&](long long sg) {
+    return sg < full ? sg * tt.K : tt.base + (sg - full) * tt.rem / tt.Ptail;
+  };
   long long slots = 0;
   for (size_t k = 0; k < tiles.size(); ++k) {
     const long long a = tiles[k].prefix;
@@ -786,14 +820,22 @@ inline cudaError_t tile_table(int d, int lead, bool lower, int W, int H, ColMap 
     }
     const size_t tb = align256(tiles.size() * sizeof(SymTile));
     void *mem = nullptr;
-    cudaError_t e = cudaMalloc(&mem, tb + segt.size() * sizeof(int));
+    cudaError_t e = cudaMalloc(&mem, tb * (split ? 2 : 1) + segt.size() * sizeof(int));
     if (e != cudaSuccess) return e;
     tt.dev = static_cast<SymTile *>(mem);
-    tt.seg_tile = reinterpret_cast<int *>(static_cast<char *>(mem) + tb);
+    tt.seg_tile = reinterpret_cast<int *>(static_cast<char *>(mem) + tb * (split ? 2 : 1));
     e = cudaMemcpy(tt.dev, tiles.data(), tiles.size() * sizeof(SymTile), cudaMemcpyHostToDevice);
     if (e != cudaSuccess) return e;
     e = cudaMemcpy(tt.seg_tile, segt.data(), segt.size() * sizeof(int), cudaMemcpyHostToDevice);
     if (e != cudaSuccess) return e;
+    if (split) {
+      // the tail grid numbers its segments from 0: same tiles, seg0 rebased
+      std::vector<SymTile> tail = tiles;
+      for (auto &t : tail) t.seg0 -= (int)full;
+      tt.dev_tail = reinterpret_cast<SymTile *>(static_cast<char *>(mem) + tb);
+      e = cudaMemcpy(tt.dev_tail, tail.data(), tail.size() * sizeof(SymTile), cudaMemcpyHostToDevice);
+      if (e != cudaSuccess) return e;
+    }
   }
   std::lock_guard<std::mutex> lk(g_mu);
   g_tiles[key] = tt;
@@ -877,8 +919,15 @@ cudaError_t run_symv(const Path<T> &pa, long long lda, int d, const T *x, ColMap
   }
   const long long Pmax = (long long)dev_sms() * occupancy((const void *)kfn, NW * 32, smem);
   TileTable tt;
-  cudaError_t e = tile_table(d, pa.lead, LOWER, W, H, cm, ncols_local, Pmax, g_symv_seg, &tt);
+  // wide 1-CTA/SM kernel: split schedule when there are enough rounds
+  const int tail_pct = (MINB == 1 && W == 128 && g_symv_seg > 0) ? symv_tail_pct() : 0;
+  cudaError_t e = tile_table(d, pa.lead, LOWER, W, H, cm, ncols_local, Pmax, g_symv_seg, &tt, false, tail_pct,
+                             tail_pct > 0 ? symv_tail_items() : 0);
   if (e != cudaSuccess) return e;
+  if (tt.dev_tail != nullptr && tt.rounds < kSymvSplitMinRounds) {
+    e = tile_table(d, pa.lead, LOWER, W, H, cm, ncols_local, Pmax, g_symv_seg, &tt);
+    if (e != cudaSuccess) return e;
+  }
   if (tt.ntiles == 0 || tt.total == 0) {  // idle GPU: partial is zero
     kblas_scal_kernel<T><<<(unsigned)cdiv(d, 256), 256, 0, st>>>(y, d, zero<T>(), 1);
     launched();
@@ -889,18 +938,50 @@ cudaError_t run_symv(const Path<T> &pa, long long lda, int d, const T *x, ColMap
   e = workspace(sym_ws_bytes<T>(d, W, tt), st, &ws);
   if (e != cudaSuccess) return e;
   SymParams p = sym_params(pa.base, lda, d, pa.lead, x, ws, W, tt, cm.G == 1 && cm.nb >= d);
-  p.pdl = t_pdl_next ? hostvec_prefetch_mode() : 0;
+  const bool hostvec = t_pdl_next;
+  p.pdl = hostvec ? hostvec_prefetch_mode() : 0;
+  const bool split = tt.dev_tail != nullptr;
+  SymParams pt = p;  // tail grid
+  if (split) {
+    unsigned *cnt = nullptr;  // slot 1023 of the stream's counters: the tail grid's (left at 0)
+    if ((e = counters(1024, st, &cnt)) != cudaSuccess) return e;
+    cnt += 1023;
+    p.nseg = (long long)tt.rounds * P;  // the first grid stops at the tail
+    pt.tiles = tt.dev_tail;
+    pt.seg_tile = tt.seg_tile + p.nseg;
+    pt.P = tt.Ptail;
+    pt.rounds = 0;
+    pt.nseg = tt.Ptail;
+    pt.tail_ctr = cnt;
+    pt.pdl = hostvec ? 2 : 0;  // with x staged the tail grid waits for the first one
+  }
   {
+    // one timing bracket over both grids of a split call (the streaming
+    // time the roofline divides by)
     TimedScope ts(st);
     e = launch_main(kfn, (unsigned)P, NW * 32, smem, st, p);
+    if (e == cudaSuccess && split) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)tt.Ptail);
+      cfg.blockDim = dim3(NW * 32);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      e = cudaLaunchKernelEx(&cfg, kfn, pt);
+      if (e == cudaSuccess) launched(1);
+    }
   }
   if (e != cudaSuccess) return e;
   launch_symv_epilogue<T, LOWER>(y, p, alpha, beta, beta_zero, cm, W, st);
   launched(2);
   char buf[256];
-  snprintf(buf, sizeof buf, "symv %s %s %s%s lead=%d d=%d W=%d H=%d B=%d tiles=%d items=%lld P=%lld K=%d rounds=%d slots=%lld",
+  snprintf(buf, sizeof buf, "symv %s %s %s%s lead=%d d=%d W=%d H=%d B=%d tiles=%d items=%lld P=%lld K=%d rounds=%d slots=%lld tail=%d",
            tname<T>(), V > 1 ? "v256" : "scalar", LOWER ? "L" : "U", HERM ? " herm" : "", pa.lead, d, W, H, B,
-           tt.ntiles, tt.total, P, tt.K, tt.rounds, tt.nslots);
+           tt.ntiles, tt.total, P, tt.K, tt.rounds, tt.nslots, split ? tt.Ptail : 0);
   g_last_plan = buf;
   return cudaGetLastError();
 }

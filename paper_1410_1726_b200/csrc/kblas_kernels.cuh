@@ -782,6 +782,7 @@ struct SymParams {
 #endif
   int pdl = 0;          // launched as the programmatic dependent of a hostvec copy-in grid
                         // (1: prefetch the first A segments before the wait, 2: no prefetch)
+  unsigned *tail_ctr = nullptr;  // tail grid of a split call (see run_symv): CTA counter, else nullptr
 };
 
 // first item of segment s (s == nseg gives total)
@@ -857,9 +858,19 @@ struct SymT1Meta { int k, p0, clo, chi; };
 // drift freely inside a window, so one late load no longer stalls all 16
 // warps at every item (ncu: barrier stalls were ~46 % of warp samples with
 // B = 1, profiles/r2a_ncu_summary.md).
+//
+// Split calls (1-CTA/SM kernels, run_symv): the interleaved rounds run in one
+// grid and the last few percent of the items in a second, programmatic-
+// dependent grid of small CTAs (tail_ctr != nullptr) that the block
+// scheduler hands to SMs as the first grid's CTAs finish, so the SMs that
+// finish early take the tail instead of idling.  The tail grid does not
+// wait for the first one (it writes other ws1 rows and its own ws2 slots);
+// its last CTA does, so the pair completes together for the epilogue.  The
+// first grid releases its dependents after its own wait, so the tail grid
+// of a host-vector call starts only once x is staged.
 template <class T, int V, int NW, int CW, int R, bool LOWER, bool HERM, int MINB = 1, bool XS = false, int B = 1>
 __global__ void __launch_bounds__(NW * 32, MINB) kblas_symv_kernel(const SymParams p) {
-  griddep_launch_dependents();
+  if constexpr (MINB != 1) griddep_launch_dependents();
   constexpr int NT = NW * 32;
   constexpr int H = 32 * V * R;
   // t1 partials, double-buffered windows: red[buf][item][warp][row]
@@ -891,7 +902,15 @@ __global__ void __launch_bounds__(NW * 32, MINB) kblas_symv_kernel(const SymPara
     return;
   }
 #else
-  if (!c.init(p)) return;
+  if (!c.init(p)) {
+    if constexpr (MINB == 1) {  // (the host gives every tail CTA work; kept for safety)
+      if (p.tail_ctr != nullptr && threadIdx.x == 0 && atomicAdd(p.tail_ctr, 1u) == gridDim.x - 1) {
+        griddep_wait();
+        *p.tail_ctr = 0u;
+      }
+    }
+    return;
+  }
 #endif
   const int cl = warp * CW;
   const bool xvec = V > 1 && p.lead == 0 && (reinterpret_cast<uintptr_t>(x) % (V * sizeof(T))) == 0;
@@ -971,7 +990,13 @@ __global__ void __launch_bounds__(NW * 32, MINB) kblas_symv_kernel(const SymPara
         if (cl + j < tl.ncols && vs < vhi && vs + V > vlo) prefetch_l2(Aw + (long long)j * p.lda + vs);
       }
   }
-  griddep_wait();
+  if constexpr (MINB == 1) {
+    // the tail grid of a split call skips the wait unless x is staged
+    if (p.tail_ctr == nullptr || p.pdl != 0) griddep_wait();
+    griddep_launch_dependents();
+  } else {
+    griddep_wait();
+  }
   set_xc(tl);
 #pragma unroll
   for (int j = 0; j < CW; ++j) t2[j] = zero<T>();
@@ -1085,6 +1110,14 @@ __global__ void __launch_bounds__(NW * 32, MINB) kblas_symv_kernel(const SymPara
 #if KBLAS_SYMV_TRACE
   if (p.trace != nullptr && threadIdx.x == 0) p.trace[3 * blockIdx.x + 1] = globaltimer_ns();
 #endif
+  if constexpr (MINB == 1) {
+    // tail grid: the last CTA to finish waits for the first grid, so the
+    // epilogue (a dependent of this grid) sees both grids' partials
+    if (p.tail_ctr != nullptr && threadIdx.x == 0 && atomicAdd(p.tail_ctr, 1u) == gridDim.x - 1) {
+      griddep_wait();
+      *p.tail_ctr = 0u;
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------

@@ -103,6 +103,22 @@ for tag in "sdcz":
     ok(f"symv mgpu {tag}", r)
     r = kb.gemv_mgpu("n", 1.0, dist, vec(tag, 600), 0.5, vec(tag, 600))[0].y_out
     ok(f"gemv mgpu {tag}", r)
+# split SYMV schedule (tail grid of small CTAs, last CTA waits for the
+# first grid): device vectors and a page-locked x (tail grid waits at start)
+for tag, d in (("d", 16384), ("c", 16384)):
+    p = kb.precision(tag)
+    A = torch.empty(d, d, dtype=p.torch_dtype, device="cuda")
+    (torch.view_as_real(A) if p.is_complex else A).uniform_(-1, 1)
+    hv = kb.HermitianView(kb.view_of(A.T), "l")
+    r = kb.symv_hemv("l", 1.0, hv, vec(tag, d), 0.5, vec(tag, d)).y_out
+    ok(f"symv split {tag} plan={_lib.last_plan().split()[-1]}", r)
+    hx = torch.empty(d, dtype=p.torch_dtype, pin_memory=True)
+    hx.copy_(vec(tag, d))
+    r = kb.symv_hemv("l", 1.0, hv, hx.numpy(), 0.0, torch.zeros(d, dtype=p.torch_dtype).numpy()).y_out
+    if not (r == r).all():
+        print("non-finite: symv split hostvec", tag)
+        bad += 1
+    del A
 # host-vector path: page-locked x / y (copy-in grid + PDL-launched main
 # kernel with the prefetch-before-wait prologue), misaligned pinned views,
 # pageable vectors, and queued calls

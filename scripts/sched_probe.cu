@@ -58,9 +58,10 @@ template <int MODE, bool F32>
 __global__ void __launch_bounds__(NW * 32, 1) sched(const char *A, long long ld, int n, const Tile *tiles,
                                                     int ntiles, long long total, int P, int K, unsigned *ctr,
                                                     const int *seg_tile, double *out, unsigned long long *tend,
-                                                    long long s_static) {
+                                                    long long s_static, int part = 0, int KB = 2) {
   constexpr int EB = F32 ? 4 : 8, H = 32 * 32 / EB;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (MODE == 4) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   __shared__ int s_next[2];
   const long long nseg = (total + K - 1) / K;
   // current range [q, hi)
@@ -80,17 +81,26 @@ __global__ void __launch_bounds__(NW * 32, 1) sched(const char *A, long long ld,
     hi = min(total, q + K);
     if (seg >= nseg) q = hi = total;
     if (threadIdx.x == 0) grabbed = P + atomicAdd(ctr, 1u);  // one segment ahead
-  } else {
+  } else if (MODE == 3) {
     seg = blockIdx.x;
     q = seg * K;
     hi = min(total, q + K);
     if (seg >= nseg) q = hi = total;
     if (threadIdx.x == 0)
       grabbed = seg + P < s_static ? (unsigned)(seg + P) : (unsigned)(s_static + atomicAdd(ctr, 1u));
+  } else if (part == 0) {  // MODE 4, first kernel: interleaved segments below s_static
+    seg = blockIdx.x;
+    q = seg * K;
+    hi = min(total, q + K);
+    if (seg >= s_static) q = hi = total;
+  } else {  // MODE 4, second kernel: KB-item CTAs over the rest
+    q = s_static * K + (long long)blockIdx.x * KB;
+    hi = min(total, q + KB);
+    if (q >= total) q = hi = total;
   }
   double acc = 0.0;
   uint32_t a[CW][8];
-  int k = q < total ? (MODE == 0 ? tile_of(tiles, ntiles, q) : seg_tile[seg]) : 0;
+  int k = q < total ? ((MODE == 0 || (MODE == 4 && part == 1)) ? tile_of(tiles, ntiles, q) : seg_tile[seg]) : 0;
   // dynamic: the next segment and its start tile, fetched a segment ahead
   long long nseg_id = -1;
   int nk = 0;
@@ -121,8 +131,14 @@ __global__ void __launch_bounds__(NW * 32, 1) sched(const char *A, long long ld,
     long long nq = q + 1;
     if (nq >= hi) {
       // next range
-      if (MODE == 0) {
+      if (MODE == 0 || (MODE == 4 && part == 1)) {
         nq = hi = total;
+      } else if (MODE == 4) {
+        seg += P;
+        nq = seg * K;
+        hi = min(total, nq + K);
+        if (seg >= s_static) nq = hi = total;
+        if (nq < hi) k = seg_tile[seg];
       } else if (MODE == 1) {
         seg += P;
         nq = seg * K;
@@ -152,6 +168,16 @@ __global__ void __launch_bounds__(NW * 32, 1) sched(const char *A, long long ld,
     }
     if (nq < hi) load(t, nq);
     q = nq;
+  }
+  if (MODE == 4 && part == 1) {
+    // the last CTA of the second kernel waits for the first one, so the
+    // pair completes together (what an epilogue would wait for)
+    if (threadIdx.x == 0 && atomicAdd(ctr, 1u) == gridDim.x - 1) {
+      asm volatile("griddepcontrol.wait;" ::: "memory");
+      *ctr = 0u;
+    }
+    if (acc == 12345.0) out[0] = acc;
+    return;
   }
   out[(long long)blockIdx.x * blockDim.x + threadIdx.x] = acc;
   if (threadIdx.x == 0) tend[blockIdx.x] = gtimer();
@@ -201,6 +227,29 @@ int main(int argc, char **argv) {
   cudaEventCreate(&e1);
   const long long nseg_h = (total + K - 1) / K;
   const long long s_static = (long long)(nseg_h * (1.0 - frac)) / P * P;
+  const int KB = argc > 5 ? atoi(argv[5]) : 2;
+  const long long s_split = (long long)(nseg_h * (1.0 - frac));  // split: first-kernel segments
+  const long long tail_items = std::max<long long>(0, total - s_split * K);
+  // split: interleaved segments below s_split in one kernel, the rest as
+  // KB-item CTAs in a programmatic dependent that the block scheduler
+  // hands to the SMs as the first kernel's CTAs finish
+  auto split = [&](bool is32) {
+    if (is32) sched<4, true><<<P, NW * 32>>>(A, ld, n, dt, (int)tiles.size(), total, P, K, ctr, dseg, out, tend, s_split, 0, KB);
+    else sched<4, false><<<P, NW * 32>>>(A, ld, n, dt, (int)tiles.size(), total, P, K, ctr, dseg, out, tend, s_split, 0, KB);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)std::max<long long>(1, (tail_items + KB - 1) / KB));
+    cfg.blockDim = dim3(NW * 32);
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    const Tile *ct = dt;
+    const int nt = (int)tiles.size();
+    const int one = 1;
+    if (is32) cudaLaunchKernelEx(&cfg, sched<4, true>, (const char *)A, ld, n, ct, nt, total, P, K, ctr, (const int *)dseg, out, tend, s_split, one, KB);
+    else cudaLaunchKernelEx(&cfg, sched<4, false>, (const char *)A, ld, n, ct, nt, total, P, K, ctr, (const int *)dseg, out, tend, s_split, one, KB);
+  };
   auto run = [&](int mode, int reps, float *ms, double *spread, double *mean_idle) {
     std::vector<unsigned long long> te(P);
     float best = 1e30f;
@@ -214,11 +263,13 @@ int main(int argc, char **argv) {
         if (mode == 1) SCHED(1, true);
         if (mode == 2) SCHED(2, true);
         if (mode == 3) SCHED(3, true);
+        if (mode == 4) split(true);
       } else {
         if (mode == 0) SCHED(0, false);
         if (mode == 1) SCHED(1, false);
         if (mode == 2) SCHED(2, false);
         if (mode == 3) SCHED(3, false);
+        if (mode == 4) split(false);
       }
       cudaEventRecord(e1);
       cudaEventSynchronize(e1);
@@ -239,16 +290,16 @@ int main(int argc, char **argv) {
     *spread = bsp;
     *mean_idle = bidle;
   };
-  const char *names[4] = {"static", "interleaved", "dynamic", "hybrid"};
+  const char *names[5] = {"static", "interleaved", "dynamic", "hybrid", "split"};
   for (int pass = 0; pass < 2; ++pass)
-    for (int mode = 0; mode < 4; ++mode) {
+    for (int mode = 1; mode < 5; mode += (mode == 1 ? 3 : 1)) {
       float ms;
       double sp, idle;
       run(mode, 10, &ms, &sp, &idle);
       if (pass == 1)
         printf("{\"prec\": \"%c\", \"n\": %d, \"K\": %d, \"frac\": %.2f, \"schedule\": \"%s\", \"us\": %.1f, \"gbs\": %.0f, \"finish_spread_us\": %.1f, "
-               "\"mean_idle_us\": %.1f, \"items\": %lld}\n",
-               f32 ? 's' : 'd', n, K, mode == 3 ? frac : 0.0, names[mode], ms * 1e3, bytes / (ms * 1e-3) / 1e9, sp, idle, total);
+               "\"mean_idle_us\": %.1f, \"items\": %lld, \"KB\": %d}\n",
+               f32 ? 's' : 'd', n, K, mode >= 3 ? frac : 0.0, names[mode], ms * 1e3, bytes / (ms * 1e-3) / 1e9, sp, idle, total, KB);
     }
   cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) printf("error %s\n", cudaGetErrorString(err));
