@@ -46,7 +46,7 @@ def main():
              "(cold caches, one kernel at a time: compare shares, not absolute step times).", "",
              "| kernel | time (us) | DRAM read (MB) | DRAM write (MB) | DRAM % peak | occupancy % | regs | top stalls (per issue) |",
              "|---|---|---|---|---|---|---|---|"]
-    main_bytes = None
+    main_bytes, main_name = None, None
     for d in rows:
         name = d["Kernel Name"]
         t = num(d.get("gpu__time_duration.sum")) * {"ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3,
@@ -67,8 +67,14 @@ def main():
                      f"{num(d.get('sm__warps_active.avg.pct_of_peak_sustained_active')):.1f} | "
                      f"{d.get('launch__registers_per_thread', '')} | "
                      + ", ".join(f"{n} {x:.1f}" for x, n in stalls[:4]) + " |")
-        if "epilogue" not in name and "scal" not in name and main_bytes is None:
-            main_bytes = int((rd * scale_r + wr * scale_w) * 1e6)
+        # the streaming kernel's bytes per call: the first streaming row,
+        # plus every later row of the same kernel (the tail grid of a split
+        # SYMV call; capture exactly one call's grids, e.g. -k regex:symv_kernel -c 2)
+        if "epilogue" not in name and "scal" not in name:
+            if main_bytes is None:
+                main_name, main_bytes = name, 0
+            if name == main_name:
+                main_bytes += int((rd * scale_r + wr * scale_w) * 1e6)
     if launches:
         agg = defaultdict(list)
         rws = list(csv.reader(open(launches)))
