@@ -953,7 +953,11 @@ cudaError_t run_symv(const Path<T> &pa, long long lda, int d, const T *x, ColMap
     pt.rounds = 0;
     pt.nseg = tt.Ptail;
     pt.tail_ctr = cnt;
-    pt.pdl = hostvec ? 2 : 0;  // with x staged the tail grid waits for the first one
+    // no wait in the tail grid, host-vector calls included: it launches
+    // only after every CTA of the first grid has passed its own wait on the
+    // copy-in grid (the first grid releases its dependents after that
+    // wait), so a staged x is complete before the tail grid starts
+    pt.pdl = 0;
   }
   {
     // one timing bracket over both grids of a split call (the streaming

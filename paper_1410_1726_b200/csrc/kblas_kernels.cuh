@@ -867,7 +867,9 @@ struct SymT1Meta { int k, p0, clo, chi; };
 // wait for the first one (it writes other ws1 rows and its own ws2 slots);
 // its last CTA does, so the pair completes together for the epilogue.  The
 // first grid releases its dependents after its own wait, so the tail grid
-// of a host-vector call starts only once x is staged.
+// of a host-vector call starts only once x is staged (it never waits at
+// its start; p.pdl != 0 would make it wait, the run_symv launch does not
+// set it).
 template <class T, int V, int NW, int CW, int R, bool LOWER, bool HERM, int MINB = 1, bool XS = false, int B = 1>
 __global__ void __launch_bounds__(NW * 32, MINB) kblas_symv_kernel(const SymParams p) {
   if constexpr (MINB != 1) griddep_launch_dependents();
@@ -991,7 +993,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) kblas_symv_kernel(const SymPara
       }
   }
   if constexpr (MINB == 1) {
-    // the tail grid of a split call skips the wait unless x is staged
+    // the tail grid of a split call does not wait for the first grid
     if (p.tail_ctr == nullptr || p.pdl != 0) griddep_wait();
     griddep_launch_dependents();
   } else {
