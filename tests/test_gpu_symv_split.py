@@ -93,3 +93,55 @@ def test_split_mgpu_partials():
     assert " tail=" in _lib.last_plan()
     err = float((got - want).abs().max() / want.abs().max())
     assert err <= 1e-12, err
+
+
+def test_split_in_cuda_graph_and_threads():
+    """A split call captured into a CUDA graph (programmatic edges to the
+    tail grid and the epilogue) replays to the eager result; two threads
+    on their own streams run split calls concurrently (per-stream tail
+    counter) with unchanged results."""
+    import threading
+
+    d = 20000
+    g = torch.Generator(device="cuda").manual_seed(7)
+    A = torch.empty(d, d, dtype=torch.float64, device="cuda").uniform_(-1, 1, generator=g)
+    hv = kb.HermitianView(kb.view_of(A.T), "l")
+    x = torch.empty(d, dtype=torch.float64, device="cuda").uniform_(-1, 1, generator=g)
+    y = torch.empty(d, dtype=torch.float64, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        kb.symv_hemv("l", 1.0, hv, x, 0.0, y, inplace=True)
+        s.synchronize()
+        assert " tail=" in _lib.last_plan() and "tail=0" not in _lib.last_plan()
+        want = y.clone()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=s):
+            kb.symv_hemv("l", 1.0, hv, x, 0.0, y, inplace=True)
+    y.zero_()
+    for _ in range(3):
+        graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(y, want)
+
+    outs, errs = [None, None], []
+
+    def work(i):
+        try:
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                r = None
+                for _ in range(5):
+                    r = kb.symv_hemv("l", 1.0, hv, x, 0.0, torch.empty_like(x)).y_out
+                st.synchronize()
+                outs[i] = r
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+
+    ts = [threading.Thread(target=work, args=(i,)) for i in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
+    for r in outs:
+        assert torch.equal(r, want)
