@@ -11,6 +11,6 @@ timeout 900 python bench.py > $O/bench_$TAG.log 2>&1
 timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > $O/bench_ref_$TAG.log 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
   --log-file $O/launches_$TAG.csv python bench.py --steps 4 --warmup 2 --no-e2e --no-cpu > /dev/null 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:symv -s 4 -c 2 -o $O/prof_bench_$TAG \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:symv_kernel -s 2 -c 2 -o $O/prof_bench_$TAG \
   python bench.py --steps 3 --warmup 1 --no-e2e --no-cpu > /dev/null 2>&1
 grep -h '^{' $O/bench_$TAG.log $O/bench_ref_$TAG.log | cut -c1-300
