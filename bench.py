@@ -437,9 +437,10 @@ def bench_single(args, dev, rank, opname=None, n=None, m=None, steps=None, warmu
     # column-major A: a (n, ld) row-major tensor whose row j is column j
     A = torch.empty(n, ld, dtype=p.torch_dtype, device=dev)
     (torch.view_as_real(A) if p.is_complex else A).uniform_(-1, 1)
-    # operands smaller than 4x the 126 MB L2 rotate over copies of A (>= 512
-    # MB together), so every step streams its matrix from HBM
-    ncopies = max(1, min(16, -(-(512 << 20) // A.numel() // p.element_bytes)))
+    # operands smaller than 8x the 126 MB L2 rotate over copies of A (>= 1
+    # GiB together), so every step streams its matrix from HBM even with
+    # consecutive steps overlapping (programmatic dependent launch)
+    ncopies = max(1, min(16, -(-(1 << 30) // A.numel() // p.element_bytes)))
     As = [A] + [A.clone() for _ in range(ncopies - 1)]
     x_len, y_len = (n, m) if (family == "symv" or op == "n") else (m, n)
     x = torch.empty(x_len, dtype=p.torch_dtype, device=dev)
@@ -841,7 +842,7 @@ def single_block(res, hbm_peak, peak_src, workload):
                             kernel_timing=res.get("kern_timing")),
            "gpu_launches": res["launches"], "plan": res["plan"],
            "l2": ("inputs > 126 MB L2 (A streamed from HBM every step), no flush" if res["ncopies"] == 1 else
-                  f"{res['ncopies']} rotating copies of A (>= 512 MB together, > 4x the L2)")}
+                  f"{res['ncopies']} rotating copies of A (>= 1 GiB together, > 8x the L2)")}
     if res.get("clocks"):
         out["clocks"] = res["clocks"]
     for k in ("cublas", "e2e"):

@@ -263,6 +263,22 @@ inline bool hostvec_early_copy() {
   return on;
 }
 
+// Every main kernel launched as a programmatic dependent of the stream's
+// previous kernel (1, default; $KBLAS_PDL_CHAIN=0: only in host-vector
+// calls).  Safe because every library kernel executes griddepcontrol.wait
+// before it reads or writes anything an earlier kernel of the stream may
+// still touch (the loads before it are A prefetches into L2 and the
+// host-built tile tables), and before it completes, so the wait covers the
+// whole stream; back-to-back calls then overlap a launch with the previous
+// call's last kernel.
+inline bool pdl_chain() {
+  static const bool on = [] {
+    const char *e = std::getenv("KBLAS_PDL_CHAIN");
+    return !(e != nullptr && e[0] == '0');
+  }();
+  return on;
+}
+
 template <class... KArgs, class... Args>
 cudaError_t launch_main(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t st,
                         Args &&...args) {
@@ -275,7 +291,7 @@ cudaError_t launch_main(void (*kern)(KArgs...), unsigned grid, unsigned block, s
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = t_pdl_next ? 1 : 0;
+  cfg.numAttrs = (t_pdl_next || pdl_chain()) ? 1 : 0;
   t_pdl_next = false;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
@@ -458,7 +474,7 @@ cudaError_t run_gemv_nc(const Path<T> &pa, long long lda, int m, int n, const T 
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = t_pdl_next ? 2 : 1;
+  cfg.numAttrs = (t_pdl_next || pdl_chain()) ? 2 : 1;
   t_pdl_next = false;
   cudaError_t e;
   {
@@ -484,7 +500,10 @@ bool run_gemv_ro(const Path<T> &pa, long long lda, int m, int n, const T *x, Col
   if (2 * P < dev_sms()) return false;
   GemvParams p{pa.base, lda, m, n, pa.lead, x, nullptr, 0, 0, (int)P, 0, cm,
                y, nullptr, widen(alpha), widen(beta), beta_zero ? 1 : 0, (long long)m};
-  p.pdl = t_pdl_next ? hostvec_prefetch_mode() : 0;
+  // the row-owning kernel executes griddepcontrol.wait only when p.pdl != 0
+  // (its prologue is laid out for the ordinary launch): a chained launch
+  // must set it
+  p.pdl = t_pdl_next ? hostvec_prefetch_mode() : (pdl_chain() ? 2 : 0);
   {
     TimedScope ts(st);
     *err = launch_main(kblas_gemv_ro_kernel<T, V, NW, LR, U>, (unsigned)P, NW * 32, 0, st, p);

@@ -55,7 +55,7 @@ def main():
         fn.argtypes = [ctypes.c_char] + dims + [S, P, I, P, I, S, P, I, P]
         for n in sizes:
             ld = -(-n // 32) * 32
-            nc = max(1, min(64, -(-(512 << 20) // (n * ld * eb))))
+            nc = max(1, min(64, -(-(1 << 30) // (n * ld * eb))))
             As = []
             for _ in range(nc):
                 A = torch.empty(n, ld, dtype=dt, device="cuda")

@@ -152,7 +152,7 @@ def main():
             if n * ld * p.element_bytes > args.max_gb * 1e9:
                 continue
             mat_alloc = n * ld * p.element_bytes
-            ncop = max(1, min(64, -(-(512 << 20) // mat_alloc)))
+            ncop = max(1, min(64, -(-(1 << 30) // mat_alloc)))
             As = []
             for _ in range(ncop):
                 A = torch.empty(n, ld, dtype=p.torch_dtype, device=dev)
