@@ -294,8 +294,9 @@ class _Bench:
         g.manual_seed(seed)
         abytes = n * n * prec.element_bytes
         free = torch.cuda.mem_get_info(dev)[0]
-        # rotating copies: together > 4x L2, so every call streams from HBM
-        copies = max(1, min(64, math.ceil(4 * self.L2_BYTES / max(1, abytes)), int(0.5 * free // max(1, abytes))))
+        # rotating copies: together > 8x L2, so every call streams from HBM
+        # (consecutive calls overlap under chained launches)
+        copies = max(1, min(64, math.ceil(8 * self.L2_BYTES / max(1, abytes)), int(0.5 * free // max(1, abytes))))
 
         def rnd(*shape):
             t = torch.empty(*shape, dtype=prec.torch_dtype, device=dev)
