@@ -22,6 +22,12 @@
  *     fixed-order two-pass sum (no floating-point atomics).
  *   - Synchronous variants launch on the legacy default stream (0);
  *     `_async` variants take an explicit stream.
+ *   - Kernels are launched as programmatic dependents of the stream's
+ *     previous kernel and release their own dependents early; each waits
+ *     (griddepcontrol.wait) before touching data an earlier kernel may
+ *     still use.  A caller's kernel launched with the programmatic-
+ *     serialization attribute after a call must do the same before it
+ *     reads the call's output ($KBLAS_PDL_CHAIN=0: ordinary launches).
  *
  * Return codes
  *   0   success
