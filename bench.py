@@ -207,7 +207,7 @@ def host_symv_operand(tag: str, n: int):
 
     dt = streamed.DTYPES[tag]
     buf = np.empty(n * n, dtype=dt)
-    rc = streamed.load().oracle_gen_fill_tri(tag.encode(), b"l", n, 5, n, buf.ctypes.data, n, 0)
+    rc = streamed.load().oracle_gen_fill_tri(tag.encode(), b"l", n, 5, n, buf.ctypes.data, n, host_threads())
     assert rc == 0
     return buf.reshape(n, n).T  # column-major view
 
@@ -244,11 +244,21 @@ def _cpu_problem(opname: str, n: int):
     return tag, family, op, herm, a, x, y, nbytes
 
 
-def _cpu_call(streamed, family, op, herm, a, x, y):
+def host_threads() -> int:
+    """Every host core this process may run on.  Passed explicitly to the
+    CPU legs: torchrun sets OMP_NUM_THREADS=1 for its workers, which would
+    otherwise leave the N > 1 reference arm on one core."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def _cpu_call(streamed, family, op, herm, a, x, y, threads=0):
     if family == "symv":
-        streamed.symv(op, 1.0, a, x, 0.0, y, hermitian=herm)
+        streamed.symv(op, 1.0, a, x, 0.0, y, hermitian=herm, nthreads=threads)
     else:
-        streamed.gemv(op, 1.0, a, x, 0.0, y)
+        streamed.gemv(op, 1.0, a, x, 0.0, y, nthreads=threads)
 
 
 def cpu_baseline(seconds: float, opname: str, n: int, n_work: int, max_calls: int | None = None):
@@ -258,11 +268,11 @@ def cpu_baseline(seconds: float, opname: str, n: int, n_work: int, max_calls: in
     from oracle import streamed  # CPU baseline leg only
 
     tag, family, op, herm, a, x, y, nbytes = _cpu_problem(opname, n)
-    threads = streamed.max_threads()
-    _cpu_call(streamed, family, op, herm, a, x, y)  # warm
+    threads = host_threads()
+    _cpu_call(streamed, family, op, herm, a, x, y, threads)  # warm
     calls, t0 = 0, time.perf_counter()
     while True:
-        _cpu_call(streamed, family, op, herm, a, x, y)
+        _cpu_call(streamed, family, op, herm, a, x, y, threads)
         calls += 1
         el = time.perf_counter() - t0
         if el >= seconds or (max_calls and calls >= max_calls):
@@ -299,12 +309,12 @@ def run_reference(args):
     n = cpu_symv_n(n_work) if (northstar or n_work > CPU_SAMPLE_N and OPS[opname][1] == "symv") else min(
         n_work, CPU_SAMPLE_N)
     tag, family, op, herm, a, x, y, nbytes = _cpu_problem(opname, n)
-    threads = streamed.max_threads()
+    threads = host_threads()
     for _ in range(args.warmup):
-        _cpu_call(streamed, family, op, herm, a, x, y)
+        _cpu_call(streamed, family, op, herm, a, x, y, threads)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        _cpu_call(streamed, family, op, herm, a, x, y)
+        _cpu_call(streamed, family, op, herm, a, x, y, threads)
     el = time.perf_counter() - t0
     gbs = nbytes * args.steps / el / 1e9
     whole = n == n_work
