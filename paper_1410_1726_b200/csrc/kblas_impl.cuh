@@ -498,11 +498,16 @@ bool run_gemv_ro(const Path<T> &pa, long long lda, int m, int n, const T *x, Col
   // every CTA streams all n columns of its rows: needs enough row blocks to
   // cover the GPU, else the caller falls back to the other forms
   if (2 * P < dev_sms()) return false;
-  // ... and they must all be resident at once: a second, partial wave of
-  // whole-row CTAs runs alone at the end (measured: from one CTA past the
-  // SM count x CTAs per SM the form drops 10-40 % below stream-K,
-  // profiles/r2s_audit_rowown.log)
-  if (P > (long long)dev_sms() * occupancy((const void *)kblas_gemv_ro_kernel<T, V, NW, LR, U>, NW * 32)) return false;
+  // ... and a last, partial wave must not run nearly alone: every CTA
+  // streams a whole row block across all n columns, so a wave holding a
+  // few CTAs costs as much as a full one (measured: one CTA past the SM
+  // count x CTAs per SM drops the form 10-40 % below stream-K,
+  // profiles/r2s_audit_rowown.log; three waves at 87 % stay ahead)
+  {
+    const long long slots =
+        (long long)dev_sms() * occupancy((const void *)kblas_gemv_ro_kernel<T, V, NW, LR, U>, NW * 32);
+    if (slots > 0 && (double)P / (double)(cdiv(P, slots) * slots) < 0.75) return false;
+  }
   GemvParams p{pa.base, lda, m, n, pa.lead, x, nullptr, 0, 0, (int)P, 0, cm,
                y, nullptr, widen(alpha), widen(beta), beta_zero ? 1 : 0, (long long)m};
   // the row-owning kernel executes griddepcontrol.wait only when p.pdl != 0
