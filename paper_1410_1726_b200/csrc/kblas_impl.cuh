@@ -506,7 +506,7 @@ bool run_gemv_ro(const Path<T> &pa, long long lda, int m, int n, const T *x, Col
   {
     const long long slots =
         (long long)dev_sms() * occupancy((const void *)kblas_gemv_ro_kernel<T, V, NW, LR, U>, NW * 32);
-    if (slots > 0 && (double)P / (double)(cdiv(P, slots) * slots) < 0.75) return false;
+    if (slots > 0 && P > slots && (double)P / (double)(cdiv(P, slots) * slots) < 0.75) return false;
   }
   GemvParams p{pa.base, lda, m, n, pa.lead, x, nullptr, 0, 0, (int)P, 0, cm,
                y, nullptr, widen(alpha), widen(beta), beta_zero ? 1 : 0, (long long)m};
