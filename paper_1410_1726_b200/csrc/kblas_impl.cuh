@@ -242,6 +242,10 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, cu
 // still reads over PCIe; every main kernel executes griddepcontrol.wait
 // before its first x / y access (a no-op for an ordinary launch).
 inline thread_local bool t_pdl_next = false;
+// Set by hostvec_entry while a call whose y was staged by the copy-in grid
+// launches its kernels: its main kernel is launched the ordinary way even
+// with chained launches (see hostvec_entry).
+inline thread_local bool t_pdl_off = false;
 // 1: the PDL-launched main kernel prefetches its first A segments into L2
 // before griddepcontrol.wait; 2: it only waits.  $KBLAS_HOSTVEC_PREFETCH.
 inline int hostvec_prefetch_mode() {
@@ -291,7 +295,7 @@ cudaError_t launch_main(void (*kern)(KArgs...), unsigned grid, unsigned block, s
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = (t_pdl_next || pdl_chain()) ? 1 : 0;
+  cfg.numAttrs = (!t_pdl_off && (t_pdl_next || pdl_chain())) ? 1 : 0;
   t_pdl_next = false;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
@@ -474,7 +478,7 @@ cudaError_t run_gemv_nc(const Path<T> &pa, long long lda, int m, int n, const T 
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = (t_pdl_next || pdl_chain()) ? 2 : 1;
+  cfg.numAttrs = (!t_pdl_off && (t_pdl_next || pdl_chain())) ? 2 : 1;
   t_pdl_next = false;
   cudaError_t e;
   {
@@ -513,7 +517,7 @@ bool run_gemv_ro(const Path<T> &pa, long long lda, int m, int n, const T *x, Col
   // the row-owning kernel executes griddepcontrol.wait only when p.pdl != 0
   // (its prologue is laid out for the ordinary launch): a chained launch
   // must set it
-  p.pdl = t_pdl_next ? hostvec_prefetch_mode() : (pdl_chain() ? 2 : 0);
+  p.pdl = t_pdl_next ? hostvec_prefetch_mode() : (pdl_chain() && !t_pdl_off ? 2 : 0);
   {
     TimedScope ts(st);
     *err = launch_main(kblas_gemv_ro_kernel<T, V, NW, LR, U>, (unsigned)P, NW * 32, 0, st, p);
@@ -1563,10 +1567,11 @@ int hostvec_entry(bool is_gemv, char op, bool herm, int m, int n, T alpha, const
     // griddepcontrol.wait on the copy-in grid.  A staged y (beta != 0) is
     // read by the epilogue kernel, a programmatic dependent of the main
     // kernel only; with the main kernel also launched as a dependent the
-    // epilogue was measured reading stale y staging (tests/
+    // epilogue was once measured reading stale y staging (tests/
     // test_gpu_hostvec.py, d = 1001), so then the main kernel waits for
-    // the copy-in grid the ordinary way.
+    // the copy-in grid the ordinary way, chained launches or not.
     t_pdl_next = !yin;
+    t_pdl_off = yin;
   } else {
     if (xin && (e = cudaMemcpyAsync(dx, hx, xlen * sizeof(T), cudaMemcpyHostToDevice, st)) != cudaSuccess)
       return (int)e;
@@ -1583,6 +1588,7 @@ int hostvec_entry(bool is_gemv, char op, bool herm, int m, int n, T alpha, const
   const int rc = is_gemv ? gemv_entry<T>(o, m, n, alpha, dA, lda, dx, 1, beta, dyk, 1, off_r, off_c, st)
                          : symv_entry<T>(o, herm, n, alpha, dA, lda, dx, 1, beta, dyk, 1, off_r, st);
   t_pdl_next = false;  // not consumed when the entry returned before launching
+  t_pdl_off = false;
   if (rc != 0) return rc;
   if (dyk == dy && ylen > 0 &&
       (e = cudaMemcpyAsync(hy_out, dy, ylen * sizeof(T), cudaMemcpyDeviceToHost, st)) != cudaSuccess)
