@@ -367,3 +367,29 @@ class TestBuiltinTable:
         for rs in by.values():
             rs.sort()
             assert all(a[1] < b[0] for a, b in zip(rs, rs[1:]))
+
+
+@pytest.mark.gpu
+class TestShippedTableGuards:
+    """The shipped table together with the dispatch guards."""
+
+    def test_rowown_wave_guard(self):
+        # D GEMV-N 3548..5016 is a row-owning row (config 1: 16 rows per CTA
+        # of 8 warps).  At P = 290 CTAs the grid is one wave on a B200 and
+        # the form runs; at P = 302 the last wave would hold 6 CTAs and the
+        # guard hands the call to the built-in rule.
+        _, plan_in = _gemv_call("d", "n", 290 * 16)()
+        _, plan_out = _gemv_call("d", "n", 302 * 16)()
+        assert plan_in.startswith("gemv_ro "), plan_in
+        assert not plan_out.startswith("gemv_ro "), plan_out
+
+    @pytest.mark.parametrize("trans", ["t", "c"])
+    def test_c_column_owning_rows(self, trans):
+        _, plan = _gemv_call("c", trans, 24576)()
+        assert plan.startswith("gemv_tc "), plan
+
+    def test_z_cluster_rows_stop_at_the_cliff(self):
+        _, below = _gemv_call("z", "n", 4224)()
+        _, above = _gemv_call("z", "n", 4288)()
+        assert below.startswith("gemv_nc "), below
+        assert not above.startswith("gemv_nc "), above
