@@ -738,6 +738,17 @@ inline std::map<std::vector<long long>, TileTable> g_tiles;
 // SYMV segment length K (items dealt round robin per CTA, see SymParams);
 // <= 0: contiguous stream-K.  kblas_set_symv_segment.
 inline int g_symv_seg = 6;
+// kblas_set_symv_segment not called: the wide kernel's split schedule uses
+// K = 12 where that still leaves the split its minimum rounds (+0.4-1 % at
+// 32k-65k, profiles/r2t_seg_scan_split.jsonl).  $KBLAS_SYMV_SEG_AUTO=0: K = 6.
+inline bool g_symv_seg_auto = true;
+inline bool symv_seg_auto() {
+  static const bool env = [] {
+    const char *e = std::getenv("KBLAS_SYMV_SEG_AUTO");
+    return !(e != nullptr && e[0] == '0');
+  }();
+  return env && g_symv_seg_auto;
+}
 // instrumentation (kblas_set_symv_trace): the register SYMV kernel writes
 // each CTA's start / end %globaltimer and SM id here (3 per CTA); nullptr = off
 inline unsigned long long *g_symv_trace = nullptr;
@@ -954,9 +965,19 @@ cudaError_t run_symv(const Path<T> &pa, long long lda, int d, const T *x, ColMap
   TileTable tt;
   // wide 1-CTA/SM kernel: split schedule when there are enough rounds
   const int tail_pct = (MINB == 1 && W == 128 && g_symv_seg > 0) ? symv_tail_pct() : 0;
-  cudaError_t e = tile_table(d, pa.lead, LOWER, W, H, cm, ncols_local, Pmax, g_symv_seg, &tt, false, tail_pct,
-                             tail_pct > 0 ? symv_tail_items() : 0);
-  if (e != cudaSuccess) return e;
+  cudaError_t e = cudaSuccess;
+  bool have = false;
+  if (tail_pct > 0 && symv_seg_auto() && g_symv_seg == 6) {
+    // longer segments when they keep enough rounds for the split
+    e = tile_table(d, pa.lead, LOWER, W, H, cm, ncols_local, Pmax, 12, &tt, false, tail_pct, symv_tail_items());
+    if (e != cudaSuccess) return e;
+    have = tt.dev_tail != nullptr && tt.rounds >= kSymvSplitMinRounds;
+  }
+  if (!have) {
+    e = tile_table(d, pa.lead, LOWER, W, H, cm, ncols_local, Pmax, g_symv_seg, &tt, false, tail_pct,
+                   tail_pct > 0 ? symv_tail_items() : 0);
+    if (e != cudaSuccess) return e;
+  }
   if (tt.dev_tail != nullptr && tt.rounds < kSymvSplitMinRounds) {
     e = tile_table(d, pa.lead, LOWER, W, H, cm, ncols_local, Pmax, g_symv_seg, &tt);
     if (e != cudaSuccess) return e;

@@ -381,6 +381,7 @@ int kblas_set_symv_trace(void *dev_buf) {
 int kblas_set_symv_segment(int items) {
   const int prev = g_symv_seg;
   g_symv_seg = items;
+  g_symv_seg_auto = false;  // an explicit K is used as given
   return prev;
 }
 
