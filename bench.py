@@ -617,7 +617,11 @@ def e2e_single(args, As, x, y, tag, family, op, herm, m, n, ld, dev, nbytes):
                     float(h.result().y_out[0])  # host read of the step's result
                 hs = []
 
-    qrun(16)
+    # warm-up of three batches: while a batch's results are being read the
+    # previous batch's are still referenced, so the page-locked result pool
+    # needs two batches of buffers before the timed steps (a pinned
+    # allocation inside them costs milliseconds)
+    qrun(48)
     torch.cuda.synchronize(dev)
     qsteps = max(64, nsteps)
     t0 = time.perf_counter()
